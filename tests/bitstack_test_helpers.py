@@ -1,0 +1,12 @@
+"""Small helpers shared by the test modules (no method arithmetic)."""
+
+
+def read_golden(path):
+    rows = []
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            rows.append(line.split())
+    return rows
