@@ -1,0 +1,169 @@
+/*
+ * bitstack.h -- C ABI of the B200-native BitStack hot path (arXiv 2410.23918).
+ *
+ * One handle = one weight stack of one linear layer (optionally one row shard of
+ * it for tensor parallelism).  The weight is held ONLY as n stacked residual
+ * blocks, block i being a packed sign matrix S_i with rank-k magnitude factors
+ * U_i [d_out,k] (paper's B'), V_i [d_in,k] (paper's A'):
+ *
+ *     W_iavd^(i) = S_i (.) (U_i V_i^T)                 PAPER.md Eq.7
+ *     W_hat_n    = (sum_{i<n} W_iavd^(i)) diag(1/s)    Eq.8 + Eq.4
+ *     y          = W_hat_n x
+ *                = sum_i sum_r u_{i,r} (.) (S_i (v_{i,r} (.) (x / s)))   (north star)
+ *
+ * Orientation: [d_out, d_in], y = W x (reading R1; the paper writes
+ * X W with W in R^{m x n}, m = input channels).  s indexes input channels.
+ *
+ * Conventions for every entry point
+ *   - returns bitstack_status: 0 = OK, < 0 = error; bitstack_last_error() gives a
+ *     thread-local message for the last non-OK status of the calling thread.
+ *   - no exception or abort crosses the ABI.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - the library owns the device block store; the caller owns x, y, w.
+ *   - a handle is not safe for concurrent mutation; matmul calls on different
+ *     streams may overlap if no load/set call runs in between.
+ *   - a CUDA fault inside an asynchronous kernel surfaces at a later call (or
+ *     cudaStreamSynchronize) as BITSTACK_E_CUDA.
+ */
+#ifndef BITSTACK_H_
+#define BITSTACK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BITSTACK_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define BITSTACK_API __attribute__((visibility("default")))
+#else
+#define BITSTACK_API
+#endif
+
+typedef struct bitstack_layer_s* bitstack_layer;
+
+typedef enum {
+  BITSTACK_F32 = 0,
+  BITSTACK_BF16 = 1,
+  BITSTACK_F16 = 2
+} bitstack_dtype;
+
+typedef enum {
+  BITSTACK_OK = 0,
+  BITSTACK_E_INVALID_ARG = -1,        /* null pointer, k<1, k>min(d_out,d_in), bad dtype */
+  BITSTACK_E_DIM_MISMATCH = -2,       /* row range outside [0,d_out), empty shard */
+  BITSTACK_E_LEVEL_OUT_OF_RANGE = -3, /* n > resident, first_block > resident */
+  BITSTACK_E_MALFORMED_BUFFER = -4,   /* non-zero pad bits in a packed sign buffer */
+  BITSTACK_E_CAPACITY = -5,           /* first_block + count > n_capacity */
+  BITSTACK_E_OOM = -6,                /* device allocation failed */
+  BITSTACK_E_CUDA = -7,               /* CUDA runtime error (message has the CUDA string) */
+  BITSTACK_E_UNSUPPORTED = -8         /* not an sm_100 device, k != 16 on a tensor-core path, ... */
+} bitstack_status;
+
+/* Kernel selection for bitstack_matmul (bitstack_set_kernel). */
+typedef enum {
+  BITSTACK_KERNEL_AUTO = 0,   /* tcgen05 decode kernel when supported, else SIMT */
+  BITSTACK_KERNEL_TC = 1,     /* force the tcgen05/TMEM decode kernel (E_UNSUPPORTED if not possible) */
+  BITSTACK_KERNEL_SIMT = 2    /* force the CUDA-core FP32 reference kernel (any shape) */
+} bitstack_kernel;
+
+typedef struct {
+  int64_t d_out, d_in, row_begin, row_end;
+  int32_t k, n_capacity, n_resident, n_active;
+  bitstack_dtype factor_dtype;
+  int32_t device;
+  int64_t device_bytes;          /* bytes of device memory owned by the handle */
+  int64_t block_bytes_device;    /* device bytes per resident block (signs + factors, padded) */
+} bitstack_info;
+
+/* Create an empty weight stack for a [d_out, d_in] matrix, keeping rows
+ * [row_begin, row_end) (row sharding); capacity n_capacity blocks,
+ * rank k, factors stored as factor_dtype (Q7: the paper stores FP16).
+ * Allocates all device memory up front on `device`.
+ * Errors: E_INVALID_ARG (k<1, k>min(d_out,d_in), k>32, n_capacity<1, bad dtype, out==NULL),
+ *         E_DIM_MISMATCH (bad row range), E_UNSUPPORTED (device not sm_100), E_OOM, E_CUDA. */
+BITSTACK_API bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t n_capacity,
+                                bitstack_dtype factor_dtype, int64_t row_begin, int64_t row_end,
+                                int32_t device, bitstack_layer* out);
+
+/* Free the handle and its device memory (waits for the device). NULL is a no-op. */
+BITSTACK_API bitstack_status bitstack_destroy(bitstack_layer layer);
+
+/* Push blocks [first_block, first_block+count) onto the stack -- "load more
+ * weight residuals from storage when available memory increases" (Fig.2,
+ * P:72).  first_block <= resident; afterwards resident = first_block + count
+ * (re-pushing after an offload overwrites).  All buffers describe the FULL
+ * matrix, in host or device memory (detected per pointer):
+ *   signs : count x ceil(d_out*d_in/8) bytes, canonical packing (R11):
+ *           bit j*d_in + c is S[j,c], LSB-first, 1 = +1, 0 = -1, pad bits 0
+ *   u     : count x d_out x k   (factor_dtype, row-major)
+ *   v     : count x d_in  x k   (factor_dtype, row-major)
+ *   s     : d_in float32 > 0 (Eq.3 scaling vector); required iff first_block == 0,
+ *           must be NULL otherwise.
+ * The library copies its row shard and repacks signs into its device tile
+ * layout (stream-ordered on `stream`); the call returns after the host-side
+ * copies are done, so caller buffers are reusable on return.  active n is
+ * clamped to the new resident count.
+ * Errors: E_INVALID_ARG, E_CAPACITY, E_LEVEL_OUT_OF_RANGE (first_block > resident),
+ *         E_MALFORMED_BUFFER (pad bits), E_CUDA. */
+BITSTACK_API bitstack_status bitstack_load_blocks(bitstack_layer layer, int32_t first_block, int32_t count,
+                                     const uint8_t* signs, const void* u, const void* v,
+                                     const float* s, void* stream);
+
+/* Select how many resident blocks take part in matmul/reconstruct: 0 <= n <= resident.
+ * Host-side O(1) ("dynamically load or offload"); affects calls enqueued
+ * after it.  Blocks >= n stay resident until overwritten ("offload ... in
+ * reverse order").  Errors: E_LEVEL_OUT_OF_RANGE, E_INVALID_ARG. */
+BITSTACK_API bitstack_status bitstack_set_num_blocks(bitstack_layer layer, int32_t n);
+
+/* y[b, :] = W_hat_n[row_begin:row_end, :] x[b, :]  for b < batch.
+ *   x : device [batch, d_in] row-major, dtype F32 | BF16 | F16
+ *   y : device [batch, row_end-row_begin] row-major, dtype F32 | BF16, overwritten
+ * x and y must not alias.  batch == 0 is a no-op; n == 0 writes y = 0.
+ * Asynchronous on `stream`; argument errors are reported synchronously.
+ * Numerics: factors and the activation product V (.) (x/s) are
+ * rounded once to fp16 (one digit for BF16/F16 factors, two digits for F32
+ * factors) on the tensor-core path, accumulation in fp32.
+ * Errors: E_INVALID_ARG, E_UNSUPPORTED (forced TC kernel not possible), E_CUDA. */
+BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x, bitstack_dtype x_dtype,
+                                void* y, bitstack_dtype y_dtype, int64_t batch, void* stream);
+
+/* w = W_hat_n[row_begin:row_end, :] = sum_{i<n} (S_i (.) U_i V_i^T) diag(1/s)
+ * (Eq.8 + Eq.4) written densely to device w [row_end-row_begin, d_in] row-major,
+ * dtype F32 | BF16 | F16.  A test / export path ("restoration").
+ * Errors: E_INVALID_ARG, E_CUDA. */
+BITSTACK_API bitstack_status bitstack_reconstruct(bitstack_layer layer, void* w, bitstack_dtype w_dtype,
+                                     void* stream);
+
+/* Handle metadata and memory accounting.  Errors: E_INVALID_ARG. */
+BITSTACK_API bitstack_status bitstack_get_info(bitstack_layer layer, bitstack_info* out);
+
+/* Kernel selection for subsequent matmul calls.  Errors: E_INVALID_ARG. */
+BITSTACK_API bitstack_status bitstack_set_kernel(bitstack_layer layer, bitstack_kernel kernel);
+
+/* Eq.9: delta_W = m*n + factor_bits*k*(m+n) bits (factor_bits = 16 in
+ * the paper).  Pure host arithmetic, never fails. */
+BITSTACK_API int64_t bitstack_block_size_bits(int64_t m, int64_t n, int32_t k, int32_t factor_bits);
+
+/* Thread-local message of the last error on this thread ("" if none). */
+BITSTACK_API const char* bitstack_last_error(void);
+
+/* ---- measurement hooks (used by bench.py; not part of the paper's problem) ----
+ * While enabled, every decode-kernel launch made by bitstack_matmul is bracketed
+ * by a pair of CUDA events recorded on the launching stream.  profile_end
+ * synchronises those events and returns the number of bracketed launches and the
+ * sum of their device durations in milliseconds.  Errors: E_INVALID_ARG, E_CUDA. */
+BITSTACK_API bitstack_status bitstack_profile_begin(int32_t max_launches);
+BITSTACK_API bitstack_status bitstack_profile_end(int32_t* launches, double* total_ms);
+
+/* Number of kernel launches issued by this library since process start
+ * (monotonic counter; bench.py reports the difference as gpu_launches). */
+BITSTACK_API int64_t bitstack_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BITSTACK_H_ */

@@ -330,6 +330,10 @@ def relative_l2(y: np.ndarray, y_ref: np.ndarray) -> float:
     row, max over rows.  A row with y_ref == 0 must match exactly."""
     y = np.atleast_2d(np.asarray(y, dtype=np.float64))
     y_ref = np.atleast_2d(np.asarray(y_ref, dtype=np.float64))
+    if y.shape != y_ref.shape:
+        raise ValueError(f"shape mismatch {y.shape} vs {y_ref.shape}")
+    if not (np.all(np.isfinite(y)) and np.all(np.isfinite(y_ref))):
+        return float("inf")          # NaN / inf never pass a tolerance
     worst = 0.0
     for a, b in zip(y, y_ref):
         nb = np.linalg.norm(b)

@@ -1,0 +1,220 @@
+// Load-time and reference kernels of the BitStack library (sm_100a):
+//   repack_signs_kernel   canonical packed bits -> device tile layout (bijective, bit-exact)
+//   prep_factors_kernel   per-(block, r) power-of-two rebalancing U' = U 2^-e, V' = V 2^e
+//   inv_s_kernel          1/s (Eq.4 P:111 diag(1/s)), zero in the pad
+//   matmul_simt_kernel    K0: FP32 CUDA-core y = sum_i sum_r u (.) S (v (.) x/s) (any shape)
+//   reconstruct_kernel    K2: W_hat_n = sum_i (S_i (.) U_i V_i^T) diag(1/s)  (Eq.8 + Eq.4)
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace bs {
+
+// Device sign layout: per block, per 128-column subchunk q, per
+// (padded) local row j, one uint4 = 4 words; bit p of word w holds column
+//   c = 128 q + 32 w + 2 (p & 15) + (p >> 4)
+// i.e. fp16 pairs (2t', 2t'+1) sit in bits (t', t'+16) so that one LOP3 + one
+// IMAD expands a pair.  Pad rows/columns hold bit 0 (-1); Z and U are 0 there.
+__device__ __forceinline__ int dev_bit_to_col(int w, int p) { return 32 * w + 2 * (p & 15) + (p >> 4); }
+__host__ __device__ __forceinline__ int col_to_dev_bit(int cl /*0..31*/) { return (cl >> 1) + 16 * (cl & 1); }
+
+__global__ void repack_signs_kernel(const uint8_t* __restrict__ canon, uint32_t* __restrict__ dev,
+                                    int count, long long canon_bytes, long long d_in, int nq,
+                                    int rows_pad, long long rows_local, long long row_begin) {
+  const long long words_per_block = (long long)nq * rows_pad * 4;
+  const long long total = words_per_block * count;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int blk = (int)(e / words_per_block);
+    long long rem = e % words_per_block;
+    const int q = (int)(rem / ((long long)rows_pad * 4));
+    rem %= (long long)rows_pad * 4;
+    const int j = (int)(rem / 4);
+    const int w = (int)(rem % 4);
+    uint32_t word = 0;
+    if (j < rows_local) {
+      const long long rowg = row_begin + j;
+      const uint8_t* src = canon + (long long)blk * canon_bytes;
+#pragma unroll 4
+      for (int pb = 0; pb < 32; ++pb) {
+        const long long c = 128LL * q + dev_bit_to_col(w, pb);
+        if (c < d_in) {
+          const long long bit = rowg * d_in + c;
+          word |= (uint32_t)((src[bit >> 3] >> (bit & 7)) & 1u) << pb;
+        }
+      }
+    }
+    dev[e] = word;
+  }
+}
+
+__device__ __forceinline__ float ld_factor(const void* p, long long idx, int dt) {
+  if (dt == 0) return reinterpret_cast<const float*>(p)[idx];
+  if (dt == 1) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
+  return __half2float(reinterpret_cast<const __half*>(p)[idx]);
+}
+
+// One CTA per block. Input u:[d_out][k], v:[d_in][k] in the user's dtype (staging);
+// output U' [rows_pad][16], V' [d_in_pad][16] in the device dtype (0 f32, 1 bf16),
+// columns r >= k and pad rows zero.  e_r = floor(log2(256 / max_c |V[c, r]|)).
+__global__ void prep_factors_kernel(const void* __restrict__ u_in, const void* __restrict__ v_in,
+                                    int in_dt, int k, long long d_out, long long d_in,
+                                    long long row_begin, long long rows_local, int rows_pad,
+                                    long long d_in_pad, void* u_out, void* v_out, int out_dt,
+                                    float* zscale_out) {
+  const int blk = blockIdx.x;
+  __shared__ float red[16][32];
+  __shared__ float scale[16];
+  const int tid = threadIdx.x;
+  const long long ub = (long long)blk * d_out * k, vb = (long long)blk * d_in * k;
+  // per-r max |V|
+  for (int r = 0; r < 16; ++r) {
+    float m = 0.f;
+    if (r < k)
+      for (long long c = tid; c < d_in; c += blockDim.x) m = fmaxf(m, fabsf(ld_factor(v_in, vb + c * k + r, in_dt)));
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((tid & 31) == 0) red[r][tid >> 5] = m;
+  }
+  __syncthreads();
+  if (tid < 16) {
+    float m = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[tid][w]);
+    int e = 0;
+    if (m > 0.f && isfinite(m)) {
+      e = (int)floorf(log2f(256.0f / m));
+      e = e > 60 ? 60 : (e < -60 ? -60 : e);
+    }
+    scale[tid] = ldexpf(1.0f, e);
+    if (zscale_out) zscale_out[blk * 16 + tid] = scale[tid];
+  }
+  __syncthreads();
+  const long long ou = (long long)blk * rows_pad * 16, ov = (long long)blk * d_in_pad * 16;
+  for (long long e = tid; e < (long long)rows_pad * 16; e += blockDim.x) {
+    const long long j = e / 16;
+    const int r = (int)(e % 16);
+    float val = 0.f;
+    if (j < rows_local && r < k) val = ld_factor(u_in, ub + (row_begin + j) * k + r, in_dt) / scale[r];
+    if (out_dt == 0) reinterpret_cast<float*>(u_out)[ou + e] = val;
+    else reinterpret_cast<__nv_bfloat16*>(u_out)[ou + e] = __float2bfloat16_rn(val);
+  }
+  for (long long e = tid; e < d_in_pad * 16; e += blockDim.x) {
+    const long long c = e / 16;
+    const int r = (int)(e % 16);
+    float val = 0.f;
+    if (c < d_in && r < k) val = ld_factor(v_in, vb + c * k + r, in_dt) * scale[r];
+    if (out_dt == 0) reinterpret_cast<float*>(v_out)[ov + e] = val;
+    else reinterpret_cast<__nv_bfloat16*>(v_out)[ov + e] = __float2bfloat16_rn(val);
+  }
+}
+
+__global__ void inv_s_kernel(const float* __restrict__ s, float* __restrict__ inv_s, long long d_in,
+                             long long d_in_pad) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d_in_pad;
+       c += (long long)gridDim.x * blockDim.x)
+    inv_s[c] = c < d_in ? 1.0f / s[c] : 0.0f;
+}
+
+__device__ __forceinline__ float ld_dev_factor(const void* p, long long idx, int dt) {
+  return dt == 0 ? reinterpret_cast<const float*>(p)[idx]
+                 : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
+}
+__device__ __forceinline__ float ld_act(const void* p, long long idx, int dt) {
+  if (dt == 0) return reinterpret_cast<const float*>(p)[idx];
+  if (dt == 1) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
+  return __half2float(reinterpret_cast<const __half*>(p)[idx]);
+}
+
+// K0: one CTA = one 128-row tile x one batch column; one thread = one row.
+// T_r = sum_c S[j,c] Z[c,r] in FP32 FMA, then y += sum_r U'[j,r] T_r per block.
+__global__ void __launch_bounds__(128) matmul_simt_kernel(
+    const uint4* __restrict__ signs, const void* __restrict__ u, const void* __restrict__ v,
+    const float* __restrict__ inv_s, const void* __restrict__ x, void* __restrict__ y, int n,
+    int nq, int rows_pad, long long rows_local, long long d_in, long long d_in_pad, int f_dt,
+    int x_dt, int y_dt, long long x_stride, long long y_stride) {
+  __shared__ float zs[128][17];
+  const int tile = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int row = tile * 128 + tid;
+  float yv = 0.f;
+  for (int i = 0; i < n; ++i) {
+    float t[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) t[r] = 0.f;
+    for (int q = 0; q < nq; ++q) {
+      __syncthreads();
+      {
+        const long long c = (long long)q * 128 + tid;
+        const float xs = c < d_in ? ld_act(x, b * x_stride + c, x_dt) * inv_s[c] : 0.f;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          zs[tid][r] = ld_dev_factor(v, ((long long)i * d_in_pad + c) * 16 + r, f_dt) * xs;
+      }
+      __syncthreads();
+      const uint4 sw = signs[((long long)i * nq + q) * rows_pad + row];
+      const uint32_t words[4] = {sw.x, sw.y, sw.z, sw.w};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        for (int pb = 0; pb < 32; ++pb) {
+          const float sg = ((words[w] >> pb) & 1u) ? 1.f : -1.f;
+          const int c = 32 * w + 2 * (pb & 15) + (pb >> 4);
+#pragma unroll
+          for (int r = 0; r < 16; ++r) t[r] = fmaf(sg, zs[c][r], t[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) yv = fmaf(ld_dev_factor(u, ((long long)i * rows_pad + row) * 16 + r, f_dt), t[r], yv);
+  }
+  if (row < rows_local) {
+    const long long o = b * y_stride + row;
+    if (y_dt == 0) reinterpret_cast<float*>(y)[o] = yv;
+    else reinterpret_cast<__nv_bfloat16*>(y)[o] = __float2bfloat16_rn(yv);
+  }
+}
+
+// K2: one thread per output element, 32x8 tiles; U'/V' of the tile cached in SMEM per block.
+__global__ void __launch_bounds__(256) reconstruct_kernel(
+    const uint4* __restrict__ signs, const void* __restrict__ u, const void* __restrict__ v,
+    const float* __restrict__ inv_s, void* __restrict__ w, int n, int nq, int rows_pad,
+    long long rows_local, long long d_in, long long d_in_pad, int f_dt, int w_dt) {
+  __shared__ float us[8][16];
+  __shared__ float vs[32][17];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const long long c = (long long)blockIdx.x * 32 + tx;
+  const long long row = (long long)blockIdx.y * 8 + ty;
+  float acc = 0.f;
+  for (int i = 0; i < n; ++i) {
+    __syncthreads();
+    if (threadIdx.x < 128) {
+      const int rr = threadIdx.x / 16, r = threadIdx.x % 16;
+      const long long rw = (long long)blockIdx.y * 8 + rr;
+      us[rr][r] = rw < rows_pad ? ld_dev_factor(u, ((long long)i * rows_pad + rw) * 16 + r, f_dt) : 0.f;
+    }
+    for (int e = threadIdx.x; e < 32 * 16; e += 256) {
+      const int cc = e / 16, r = e % 16;
+      const long long cg = (long long)blockIdx.x * 32 + cc;
+      vs[cc][r] = cg < d_in_pad ? ld_dev_factor(v, ((long long)i * d_in_pad + cg) * 16 + r, f_dt) : 0.f;
+    }
+    __syncthreads();
+    if (row < rows_local && c < d_in) {
+      float m = 0.f;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) m = fmaf(us[ty][r], vs[tx][r], m);
+      const int q = (int)(c / 128), cl = (int)(c % 128);
+      const uint4 sw = signs[((long long)i * nq + q) * rows_pad + row];
+      const uint32_t words[4] = {sw.x, sw.y, sw.z, sw.w};
+      const uint32_t word = words[cl / 32];
+      const int pb = col_to_dev_bit(cl % 32);
+      acc += ((word >> pb) & 1u) ? m : -m;
+    }
+  }
+  if (row < rows_local && c < d_in) {
+    const float val = acc * inv_s[c];
+    const long long o = row * d_in + c;
+    if (w_dt == 0) reinterpret_cast<float*>(w)[o] = val;
+    else if (w_dt == 1) reinterpret_cast<__nv_bfloat16*>(w)[o] = __float2bfloat16_rn(val);
+    else reinterpret_cast<__half*>(w)[o] = __float2half_rn(val);
+  }
+}
+
+}  // namespace bs

@@ -1,0 +1,528 @@
+// Host side of the BitStack C ABI (include/bitstack.h): handle lifetime,
+// validation, the device block store, and stream-ordered kernel launches.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -shared (see build.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bitstack.h"
+#include "aux_kernels.cuh"
+#include "decode_tc.cuh"
+
+struct bitstack_layer_s {
+  int64_t d_out = 0, d_in = 0, row_begin = 0, row_end = 0, rows_local = 0;
+  int rows_pad = 0, nq = 0, row_tiles = 0;
+  int64_t d_in_pad = 0;
+  int32_t k = 0, n_cap = 0, n_res = 0, n_act = 0;
+  bitstack_dtype fdt = BITSTACK_BF16;
+  int dev_fdt = 1;  // device factor storage: 0 f32, 1 bf16
+  int device = 0;
+  int sm_count = 148;
+  bitstack_kernel kernel = BITSTACK_KERNEL_AUTO;
+  uint4* signs = nullptr;
+  void* u = nullptr;
+  void* v = nullptr;
+  float* inv_s = nullptr;
+  float* zscale = nullptr;
+  float* y_acc = nullptr;  // [16][rows_pad]
+  int* counters = nullptr; // [row_tiles]
+  int64_t bytes = 0;
+  int64_t block_bytes = 0;
+};
+
+namespace {
+
+float* g_dbg_acc = nullptr;     // test hook (bitstack_debug_set), not part of the ABI
+uint32_t* g_dbg_z = nullptr;
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  int cap = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  int used = 0;
+} g_prof;
+
+bitstack_status fail(bitstack_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? BITSTACK_E_OOM : BITSTACK_E_CUDA,     \
+                  "%s failed: %s", #call, cudaGetErrorString(e_));                        \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int dsize(bitstack_dtype d) { return d == BITSTACK_F32 ? 4 : 2; }
+bool valid_dtype(int d) { return d == BITSTACK_F32 || d == BITSTACK_BF16 || d == BITSTACK_F16; }
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+template <int NB, int NDIG>
+bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_t st) {
+  using C = bs::DecodeCfg<NB, NDIG>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(bs::decode_tc_kernel<NB, NDIG>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    attr_done = true;
+  }
+  bs::decode_tc_kernel<NB, NDIG><<<grid, bs::kDecodeThreads, C::kSmemBytes, st>>>(prm);
+  count_launch();
+  CK(cudaGetLastError());
+  return BITSTACK_OK;
+}
+
+template <int NDIG>
+bitstack_status dispatch_decode(int nb, const bs::DecodeParams& prm, int grid, cudaStream_t st) {
+  switch (nb) {
+    case 1: return launch_decode<1, NDIG>(prm, grid, st);
+    case 2: return launch_decode<2, NDIG>(prm, grid, st);
+    case 4: return launch_decode<4, NDIG>(prm, grid, st);
+    case 8: return launch_decode<8, NDIG>(prm, grid, st);
+    default:
+      if constexpr (NDIG == 1) return launch_decode<16, 1>(prm, grid, st);
+      return fail(BITSTACK_E_INVALID_ARG, "internal: batch chunk %d", nb);
+  }
+}
+
+int r_tiles_for(int nb, int ndig) {
+  const int N = 16 * nb * ndig;
+  return std::min(8, 256 / N);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bitstack_last_error(void) { return g_err.c_str(); }
+
+// Test hook (not declared in bitstack.h): device buffers that the decode kernel
+// fills with CTA 0's first on-chip Z tile and raw TMEM accumulators.
+BITSTACK_API void bitstack_debug_set(void* acc, void* z) {
+  g_dbg_acc = reinterpret_cast<float*>(acc);
+  g_dbg_z = reinterpret_cast<uint32_t*>(z);
+}
+
+int64_t bitstack_launch_count(void) { return g_launches.load(); }
+
+int64_t bitstack_block_size_bits(int64_t m, int64_t n, int32_t k, int32_t factor_bits) {
+  return m * n + (int64_t)factor_bits * k * (m + n);
+}
+
+bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t n_capacity,
+                                bitstack_dtype factor_dtype, int64_t row_begin, int64_t row_end,
+                                int32_t device, bitstack_layer* out) {
+  if (!out) return fail(BITSTACK_E_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (d_out < 1 || d_in < 1) return fail(BITSTACK_E_INVALID_ARG, "dims must be positive");
+  if (k < 1 || k > std::min<int64_t>(d_out, d_in) || k > 16)
+    return fail(BITSTACK_E_INVALID_ARG, "k=%d outside [1, min(d_out, d_in, 16)]", k);
+  if (n_capacity < 1) return fail(BITSTACK_E_INVALID_ARG, "n_capacity must be >= 1");
+  if (!valid_dtype(factor_dtype)) return fail(BITSTACK_E_INVALID_ARG, "bad factor dtype");
+  if (row_begin < 0 || row_end > d_out || row_begin >= row_end)
+    return fail(BITSTACK_E_DIM_MISMATCH, "row range [%lld,%lld) outside [0,%lld)",
+                (long long)row_begin, (long long)row_end, (long long)d_out);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(BITSTACK_E_INVALID_ARG, "bad device %d", device);
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(BITSTACK_E_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                device, prop.major, prop.minor);
+  DeviceGuard guard(device);
+
+  auto* L = new bitstack_layer_s();
+  L->d_out = d_out;
+  L->d_in = d_in;
+  L->row_begin = row_begin;
+  L->row_end = row_end;
+  L->rows_local = row_end - row_begin;
+  L->rows_pad = (int)((L->rows_local + 127) / 128 * 128);
+  L->row_tiles = L->rows_pad / 128;
+  L->d_in_pad = (d_in + 127) / 128 * 128;
+  L->nq = (int)(L->d_in_pad / 128);
+  L->k = k;
+  L->n_cap = n_capacity;
+  L->fdt = factor_dtype;
+  L->dev_fdt = factor_dtype == BITSTACK_BF16 ? 1 : 0;
+  L->device = device;
+  L->sm_count = prop.multiProcessorCount;
+
+  const int64_t fs = L->dev_fdt ? 2 : 4;
+  const int64_t sign_bytes = (int64_t)L->nq * L->rows_pad * 16;
+  const int64_t u_bytes = (int64_t)L->rows_pad * 16 * fs;
+  const int64_t v_bytes = L->d_in_pad * 16 * fs;
+  L->block_bytes = sign_bytes + u_bytes + v_bytes;
+  auto alloc = [&](void** p, int64_t bytes) -> cudaError_t {
+    cudaError_t e = cudaMalloc(p, (size_t)bytes);
+    if (e == cudaSuccess) {
+      L->bytes += bytes;
+      e = cudaMemset(*p, 0, (size_t)bytes);
+    }
+    return e;
+  };
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = alloc((void**)&L->signs, sign_bytes * n_capacity);
+  if (e == cudaSuccess) e = alloc(&L->u, u_bytes * n_capacity);
+  if (e == cudaSuccess) e = alloc(&L->v, v_bytes * n_capacity);
+  if (e == cudaSuccess) e = alloc((void**)&L->inv_s, L->d_in_pad * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * 16 * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->y_acc, (int64_t)16 * L->rows_pad * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    bitstack_destroy(L);
+    return fail(e == cudaErrorMemoryAllocation ? BITSTACK_E_OOM : BITSTACK_E_CUDA,
+                "bitstack_create: %s", cudaGetErrorString(e));
+  }
+  *out = L;
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_destroy(bitstack_layer L) {
+  if (!L) return BITSTACK_OK;
+  DeviceGuard guard(L->device);
+  cudaDeviceSynchronize();
+  cudaFree(L->signs);
+  cudaFree(L->u);
+  cudaFree(L->v);
+  cudaFree(L->inv_s);
+  cudaFree(L->zscale);
+  cudaFree(L->y_acc);
+  cudaFree(L->counters);
+  delete L;
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_get_info(bitstack_layer L, bitstack_info* out) {
+  if (!L || !out) return fail(BITSTACK_E_INVALID_ARG, "NULL argument");
+  out->d_out = L->d_out;
+  out->d_in = L->d_in;
+  out->row_begin = L->row_begin;
+  out->row_end = L->row_end;
+  out->k = L->k;
+  out->n_capacity = L->n_cap;
+  out->n_resident = L->n_res;
+  out->n_active = L->n_act;
+  out->factor_dtype = L->fdt;
+  out->device = L->device;
+  out->device_bytes = L->bytes;
+  out->block_bytes_device = L->block_bytes;
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_set_kernel(bitstack_layer L, bitstack_kernel kernel) {
+  if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
+  if (kernel != BITSTACK_KERNEL_AUTO && kernel != BITSTACK_KERNEL_TC && kernel != BITSTACK_KERNEL_SIMT)
+    return fail(BITSTACK_E_INVALID_ARG, "bad kernel selector %d", (int)kernel);
+  L->kernel = kernel;
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_set_num_blocks(bitstack_layer L, int32_t n) {
+  if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
+  if (n < 0 || n > L->n_res)
+    return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "n=%d outside [0, resident=%d]", n, L->n_res);
+  L->n_act = n;
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int32_t count,
+                                     const uint8_t* signs, const void* u, const void* v,
+                                     const float* s, void* stream) {
+  if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
+  if (count < 0) return fail(BITSTACK_E_INVALID_ARG, "count < 0");
+  if (first_block < 0 || first_block > L->n_res)
+    return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "first_block=%d outside [0, resident=%d]",
+                first_block, L->n_res);
+  if ((int64_t)first_block + count > L->n_cap)
+    return fail(BITSTACK_E_CAPACITY, "first_block+count=%d > capacity %d", first_block + count, L->n_cap);
+  if (first_block == 0 && !s) return fail(BITSTACK_E_INVALID_ARG, "s is required when first_block == 0");
+  if (first_block > 0 && s) return fail(BITSTACK_E_INVALID_ARG, "s must be NULL when first_block > 0");
+  if (count > 0 && (!signs || !u || !v)) return fail(BITSTACK_E_INVALID_ARG, "NULL block buffer");
+  DeviceGuard guard(L->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+
+  const int64_t nbits = L->d_out * L->d_in;
+  const int64_t cbytes = (nbits + 7) / 8;
+  const int pad = (int)(cbytes * 8 - nbits);
+  const int fs = dsize(L->fdt);
+
+  // pad-bit validation (SPEC S:203 MalformedBuffer) before touching device state
+  if (count > 0 && pad) {
+    const uint8_t mask = (uint8_t)(0xFFu << (8 - pad));
+    const bool dev = is_device_ptr(signs);
+    for (int b = 0; b < count; ++b) {
+      uint8_t last = 0;
+      if (dev) {
+        CK(cudaMemcpy(&last, signs + (int64_t)b * cbytes + cbytes - 1, 1, cudaMemcpyDeviceToHost));
+      } else {
+        last = signs[(int64_t)b * cbytes + cbytes - 1];
+      }
+      if (last & mask) return fail(BITSTACK_E_MALFORMED_BUFFER, "block %d: non-zero pad bits", first_block + b);
+    }
+  }
+  if (s) {
+    std::vector<float> hs;
+    const float* sp = s;
+    if (is_device_ptr(s)) {
+      hs.resize(L->d_in);
+      CK(cudaMemcpy(hs.data(), s, L->d_in * 4, cudaMemcpyDeviceToHost));
+      sp = hs.data();
+    }
+    for (int64_t c = 0; c < L->d_in; ++c)
+      if (!(sp[c] > 0.f) || !std::isfinite(sp[c]))
+        return fail(BITSTACK_E_INVALID_ARG, "s[%lld] = %g is not a positive finite scale", (long long)c, sp[c]);
+  }
+
+  if (count > 0) {
+    uint8_t* st_signs = nullptr;
+    void* st_u = nullptr;
+    void* st_v = nullptr;
+    const int64_t ub = (int64_t)count * L->d_out * L->k * fs, vb = (int64_t)count * L->d_in * L->k * fs;
+    CK(cudaMalloc(&st_signs, (size_t)(cbytes * count)));
+    CK(cudaMalloc(&st_u, (size_t)ub));
+    CK(cudaMalloc(&st_v, (size_t)vb));
+    CK(cudaMemcpyAsync(st_signs, signs, (size_t)(cbytes * count), cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(st_u, u, (size_t)ub, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(st_v, v, (size_t)vb, cudaMemcpyDefault, st));
+    const int64_t words_per_block = (int64_t)L->nq * L->rows_pad * 4;
+    const int64_t total = words_per_block * count;
+    const int threads = 256;
+    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 65536);
+    bs::repack_signs_kernel<<<blocks, threads, 0, st>>>(
+        st_signs, reinterpret_cast<uint32_t*>(L->signs) + (int64_t)first_block * words_per_block, count,
+        cbytes, L->d_in, L->nq, L->rows_pad, L->rows_local, L->row_begin);
+    count_launch();
+    CK(cudaGetLastError());
+    const int64_t fsd = L->dev_fdt ? 2 : 4;
+    uint8_t* u_dst = reinterpret_cast<uint8_t*>(L->u) + (int64_t)first_block * L->rows_pad * 16 * fsd;
+    uint8_t* v_dst = reinterpret_cast<uint8_t*>(L->v) + (int64_t)first_block * L->d_in_pad * 16 * fsd;
+    const int in_dt = L->fdt == BITSTACK_F32 ? 0 : (L->fdt == BITSTACK_BF16 ? 1 : 2);
+    bs::prep_factors_kernel<<<count, 256, 0, st>>>(st_u, st_v, in_dt, L->k, L->d_out, L->d_in,
+                                                    L->row_begin, L->rows_local, L->rows_pad,
+                                                    L->d_in_pad, u_dst, v_dst, L->dev_fdt ? 1 : 0,
+                                                    L->zscale + (int64_t)first_block * 16);
+    count_launch();
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    cudaFree(st_signs);
+    cudaFree(st_u);
+    cudaFree(st_v);
+  }
+  if (s) {
+    float* st_s = nullptr;
+    CK(cudaMalloc(&st_s, L->d_in * 4));
+    CK(cudaMemcpyAsync(st_s, s, L->d_in * 4, cudaMemcpyDefault, st));
+    bs::inv_s_kernel<<<(int)((L->d_in_pad + 255) / 256), 256, 0, st>>>(st_s, L->inv_s, L->d_in, L->d_in_pad);
+    count_launch();
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    cudaFree(st_s);
+  }
+  L->n_res = first_block + count;
+  L->n_act = std::min(L->n_act, L->n_res);
+  if (first_block == 0 && count > 0 && L->n_act == 0) L->n_act = L->n_res;
+  return BITSTACK_OK;
+}
+
+static bitstack_status record_prof(cudaStream_t st, bool begin, int* slot) {
+  if (!g_prof.on) return BITSTACK_OK;
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  if (begin) {
+    if (g_prof.used >= g_prof.cap) {
+      *slot = -1;
+      return BITSTACK_OK;
+    }
+    *slot = g_prof.used++;
+    CK(cudaEventRecord(g_prof.ev[*slot].first, st));
+  } else if (*slot >= 0) {
+    CK(cudaEventRecord(g_prof.ev[*slot].second, st));
+  }
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype x_dtype, void* y,
+                                bitstack_dtype y_dtype, int64_t batch, void* stream) {
+  if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
+  if (batch < 0) return fail(BITSTACK_E_INVALID_ARG, "batch < 0");
+  if (batch == 0) return BITSTACK_OK;
+  if (!x || !y) return fail(BITSTACK_E_INVALID_ARG, "NULL x or y");
+  if (!valid_dtype(x_dtype)) return fail(BITSTACK_E_INVALID_ARG, "bad x dtype");
+  if (y_dtype != BITSTACK_F32 && y_dtype != BITSTACK_BF16)
+    return fail(BITSTACK_E_INVALID_ARG, "y dtype must be F32 or BF16");
+  if (L->n_res == 0 || L->n_act > L->n_res)
+    return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "no resident blocks (load_blocks first)");
+  DeviceGuard guard(L->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int ysz = y_dtype == BITSTACK_F32 ? 4 : 2;
+  if (L->n_act == 0) {
+    CK(cudaMemsetAsync(y, 0, (size_t)(batch * L->rows_local * ysz), st));
+    return BITSTACK_OK;
+  }
+  const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
+  const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
+  const int xsz = dsize(x_dtype);
+  const bool tc_ok = L->k <= 16;  // k < 16: zero-padded columns of U', V'
+  const bool use_tc = L->kernel == BITSTACK_KERNEL_TC || (L->kernel == BITSTACK_KERNEL_AUTO && tc_ok);
+  if (L->kernel == BITSTACK_KERNEL_TC && !tc_ok)
+    return fail(BITSTACK_E_UNSUPPORTED, "tcgen05 decode kernel needs k <= 16");
+
+  if (!use_tc) {
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+      const int nb = (int)std::min<int64_t>(65535, batch - b0);
+      int slot = -1;
+      bitstack_status ps = record_prof(st, true, &slot);
+      if (ps) return ps;
+      dim3 grid(L->row_tiles, nb);
+      bs::matmul_simt_kernel<<<grid, 128, 0, st>>>(
+          L->signs, L->u, L->v, L->inv_s, reinterpret_cast<const uint8_t*>(x) + b0 * L->d_in * xsz,
+          reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz, L->n_act, L->nq, L->rows_pad,
+          L->rows_local, L->d_in, L->d_in_pad, L->dev_fdt, xdt, ydt, L->d_in, L->rows_local);
+      count_launch();
+      CK(cudaGetLastError());
+      ps = record_prof(st, false, &slot);
+      if (ps) return ps;
+    }
+    return BITSTACK_OK;
+  }
+
+  const int ndig = L->fdt == BITSTACK_F32 ? 2 : 1;
+  const int nbmax = 16 / ndig;
+  for (int64_t b0 = 0; b0 < batch; b0 += nbmax) {
+    const int bc = (int)std::min<int64_t>(nbmax, batch - b0);
+    int nb = 1;
+    while (nb < bc) nb <<= 1;
+    const int R = r_tiles_for(nb, ndig);
+    const int n_groups = (L->row_tiles + R - 1) / R;
+    const int64_t units = (int64_t)L->n_act * L->nq;
+    int cpg = std::max(1, L->sm_count / n_groups);
+    cpg = (int)std::min<int64_t>(cpg, units);
+    bs::DecodeParams prm;
+    prm.signs = L->signs;
+    prm.u = L->u;
+    prm.v = L->v;
+    prm.inv_s = L->inv_s;
+    prm.x = reinterpret_cast<const uint8_t*>(x) + b0 * L->d_in * xsz;
+    prm.y = reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz;
+    prm.y_acc = L->y_acc;
+    prm.counters = L->counters;
+    prm.x_stride = L->d_in;
+    prm.y_stride = L->rows_local;
+    prm.n = L->n_act;
+    prm.nq = L->nq;
+    prm.rows_pad = L->rows_pad;
+    prm.rows_local = (int)L->rows_local;
+    prm.d_in = (int)L->d_in;
+    prm.d_in_pad = (int)L->d_in_pad;
+    prm.row_tiles = L->row_tiles;
+    prm.n_groups = n_groups;
+    prm.ctas_per_group = cpg;
+    prm.batch = bc;
+    prm.x_dtype = xdt;
+    prm.y_dtype = ydt;
+    prm.f_dtype = L->dev_fdt;
+    prm.one2 = 0x3C003C00u;
+    prm.dbg_acc = g_dbg_acc;
+    prm.dbg_z = g_dbg_z;
+    int slot = -1;
+    bitstack_status ps = record_prof(st, true, &slot);
+    if (ps) return ps;
+    const int grid = n_groups * cpg;
+    bitstack_status rs = ndig == 1 ? dispatch_decode<1>(nb, prm, grid, st) : dispatch_decode<2>(nb, prm, grid, st);
+    if (rs) return rs;
+    ps = record_prof(st, false, &slot);
+    if (ps) return ps;
+  }
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_reconstruct(bitstack_layer L, void* w, bitstack_dtype w_dtype, void* stream) {
+  if (!L || !w) return fail(BITSTACK_E_INVALID_ARG, "NULL argument");
+  if (!valid_dtype(w_dtype)) return fail(BITSTACK_E_INVALID_ARG, "bad w dtype");
+  if (L->n_res == 0) return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "no resident blocks");
+  DeviceGuard guard(L->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int wdt = w_dtype == BITSTACK_F32 ? 0 : (w_dtype == BITSTACK_BF16 ? 1 : 2);
+  dim3 grid((unsigned)((L->d_in + 31) / 32), (unsigned)((L->rows_local + 7) / 8));
+  bs::reconstruct_kernel<<<grid, 256, 0, st>>>(L->signs, L->u, L->v, L->inv_s, w, L->n_act, L->nq,
+                                                L->rows_pad, L->rows_local, L->d_in, L->d_in_pad,
+                                                L->dev_fdt, wdt);
+  count_launch();
+  CK(cudaGetLastError());
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_profile_begin(int32_t max_launches) {
+  if (max_launches < 1) return fail(BITSTACK_E_INVALID_ARG, "max_launches < 1");
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  while ((int)g_prof.ev.size() < max_launches) {
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    g_prof.ev.emplace_back(a, b);
+  }
+  g_prof.cap = max_launches;
+  g_prof.used = 0;
+  g_prof.on = true;
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_profile_end(int32_t* launches, double* total_ms) {
+  if (!launches || !total_ms) return fail(BITSTACK_E_INVALID_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = false;
+  double tot = 0.0;
+  for (int i = 0; i < g_prof.used; ++i) {
+    CK(cudaEventSynchronize(g_prof.ev[i].second));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, g_prof.ev[i].first, g_prof.ev[i].second));
+    tot += ms;
+  }
+  *launches = g_prof.used;
+  *total_ms = tot;
+  g_prof.used = 0;
+  return BITSTACK_OK;
+}
+
+}  // extern "C"

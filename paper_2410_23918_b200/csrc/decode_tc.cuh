@@ -1,0 +1,506 @@
+// tcgen05 / TMEM decode kernel for y = W_hat_n x  (BitStack, arXiv 2410.23918).
+//
+// What it computes (Eq.4, Eq.7, Eq.8):
+//     y[b, j] = sum_{i<n} sum_{r<16} U'_i[j, r] * T_i[j, r, b],
+//     T_i[j, r, b] = sum_c S_i[j, c] * Z_i[c, r, b],   Z_i[c, r, b] = V'_i[c, r] * x[b, c] / s[c]
+// with U' = U 2^-e_r, V' = V 2^e_r (exact power-of-two rebalancing done at load
+// time so that max|V'_{:,r}| ~ 2^8 keeps fp16 Z in range; U'V'^T == U V^T exactly).
+//
+// Mapping to the B200:
+//   * the contraction T = S . Z runs on tcgen05.mma kind::f16, M = 128 rows of S,
+//     N = 16 * NDIG * NB (rank x digits x batch), K = 16 per instruction, fp32
+//     accumulators in TMEM -- the "S_i . (V_i (.) X)" contraction of the north star;
+//   * A = S is expanded from packed bits to fp16 +-1 by 8 expander warps
+//     (1 LOP3 + 1 IMAD per 2 elements) and written straight into TMEM with
+//     tcgen05.st (A-from-TMEM "TS" MMA): the expanded operand never touches SMEM/HBM;
+//   * B = Z is formed on chip by 2 builder warps from the TMA-staged V' chunk,
+//     rounded to fp16 (NDIG = 1) or split into two fp16 digits (NDIG = 2, fp32 factors);
+//   * packed signs and V' chunks stream HBM -> SMEM through the bulk-copy (TMA)
+//     engine into a STAGES-deep mbarrier ring, signs with an evict-first L2 policy;
+//   * sum over blocks i and subchunks is a split-K across CTAs: each CTA owns a
+//     contiguous range of (block, 128-column subchunk) units for one group of up to
+//     R row tiles; partial y is folded in with red.global.add.f32 into an fp32
+//     workspace, and the last CTA of each row group converts/writes y and re-zeroes
+//     the workspace (the summation order of those fp32 adds is not
+//     fixed, so y is reproducible to fp32 rounding, not bitwise).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "ptx.cuh"
+
+namespace bs {
+
+constexpr int kDecodeThreads = 384;  // 12 warps
+constexpr int kTileRows = 128;       // M
+constexpr int kSubK = 128;           // columns per unit (one 16-byte sign vector per row)
+
+struct DecodeParams {
+  const uint4* signs;   // [n_cap][nq][rows_pad] : 128 sign bits of one row of one subchunk
+  const void* u;        // [n_cap][rows_pad][16]  U' (bf16 or f32)
+  const void* v;        // [n_cap][d_in_pad][16]  V' (bf16 or f32)
+  const float* inv_s;   // [d_in_pad], 1/s, 0 in the pad
+  const void* x;        // [batch][x_stride]
+  void* y;              // [batch][y_stride]
+  float* y_acc;         // [16][rows_pad] fp32 workspace, zero on entry and on exit
+  int* counters;        // [n_groups], zero on entry and on exit
+  long long x_stride, y_stride;
+  int n, nq, rows_pad, rows_local, d_in, d_in_pad, row_tiles, n_groups, ctas_per_group;
+  int batch;            // valid batch columns in this launch (<= NB)
+  int x_dtype, y_dtype, f_dtype;  // 0 f32, 1 bf16, 2 f16 (f_dtype: 0 f32, 1 bf16)
+  uint32_t one2;                  // 0x3C003C00 (fp16x2 {1, 1}), see expand_f16
+  float* dbg_acc;                 // test hook: raw accumulators of CTA 0's first drain (or null)
+  uint32_t* dbg_z;                // test hook: CTA 0's first Z tile as stored in SMEM (or null)
+};
+
+__device__ __forceinline__ float load_act(const void* p, long long idx, int dt) {
+  if (dt == 0) return __ldg(reinterpret_cast<const float*>(p) + idx);
+  if (dt == 1) return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(p) + idx));
+  return __half2float(__ldg(reinterpret_cast<const __half*>(p) + idx));
+}
+
+__device__ __forceinline__ uint32_t lop3_andnot(uint32_t a, uint32_t b) {  // ~a & b
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, 0, 0x0C;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t lop3_andnot_or(uint32_t a, uint32_t b, uint32_t c) {  // (~a & b) | c
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xAE;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// 32 packed sign bits -> 16 fp16x2 words of +-1.  Device bit p of word w holds
+// column 2*(p & 15) + (p >> 4) of the word's 32-column slice, so pair t' (bits
+// t', t'+16) is K-elements (2t', 2t'+1) = the low/high half of TMEM column t'.
+// Per pair: one LOP3 (alu pipe) isolates the two bits (inverted: bit 0 = -1
+// sets the fp16 sign bit) and one IMAD (fma pipe) shifts them to bit 15/31 and
+// adds 1.0h|1.0h.  `one2` = 0x3C003C00 arrives as a kernel parameter so that
+// ptxas cannot re-associate the pair into shift-then-mask (3 alu ops).
+__device__ __forceinline__ void expand_f16(uint32_t w, uint32_t one2, uint32_t (&o)[16]) {
+#pragma unroll
+  for (int t = 0; t < 15; ++t) o[t] = mad_lo(lop3_andnot(w, 0x00010001u << t), 1u << (15 - t), one2);
+  o[15] = lop3_andnot_or(w, 0x80008000u, one2);
+}
+
+template <int NB, int NDIG>
+struct DecodeCfg {
+  static constexpr int N = 16 * NB * NDIG;                   // MMA N
+  static constexpr int R = (256 / N) < 8 ? (256 / N) : 8;    // row tiles per group
+  static constexpr int kSignBytes = R * kTileRows * 16;      // per stage
+  static constexpr int kVBytes = kSubK * 16 * 4;             // V' chunk, room for f32
+  static constexpr int kZBytes = kSubK * N * 2;              // fp16 B operand
+  static constexpr int kStageBytes = kSignBytes + kVBytes + kZBytes;
+  static constexpr int S0 = (200 * 1024) / kStageBytes;
+  static constexpr int STAGES = S0 > 6 ? 6 : (S0 < 2 ? 2 : S0);
+  static constexpr int kBarBytes = 1024;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes;
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kAccCol = 256;                   // A buffers use [0, 256)
+  static constexpr uint32_t LBO = (N / 8) * 128;             // K-adjacent core matrices
+  static constexpr uint32_t SBO = 128;                       // N-adjacent core matrices
+  static_assert(N <= 256 && N % 16 == 0, "invalid MMA N");
+  static_assert(kAccCol + R * N <= kTmemCols, "TMEM overflow");
+  static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
+};
+
+template <int NB, int NDIG>
+__global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const DecodeParams p) {
+  using C = DecodeCfg<NB, NDIG>;
+  constexpr int N = C::N, R = C::R, STAGES = C::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem[];
+
+  uint8_t* bar_area = smem + STAGES * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bar_area);
+  uint64_t* empty = full + STAGES;
+  uint64_t* zfull = empty + STAGES;
+  uint64_t* a_full = zfull + STAGES;     // [2 wg][2 buf]
+  uint64_t* a_empty = a_full + 4;        // [2 wg][2 buf]
+  uint64_t* acc_full = a_empty + 4;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // ---- work assignment: row group g, contiguous unit range [u0, u1)
+  const int g = blockIdx.x / p.ctas_per_group;
+  const int jc = blockIdx.x % p.ctas_per_group;
+  const long long L = (long long)p.n * p.nq;
+  const long long u0 = L * jc / p.ctas_per_group;
+  const long long u1 = L * (jc + 1) / p.ctas_per_group;
+  const int tiles_left = p.row_tiles - g * R;
+  const int Rg = tiles_left < R ? tiles_left : R;
+  const int row0 = g * R * kTileRows;
+  const int fsz = p.f_dtype == 0 ? 4 : 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8 + 2 + 1);
+      mbar_init(&zfull[s], 2);
+    }
+    for (int b = 0; b < 4; ++b) {
+      mbar_init(&a_full[b], 4);
+      mbar_init(&a_empty[b], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 8);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= producer: bulk copies of sign tiles + V' chunk =================
+    if (lane == 0) {
+      const uint64_t pol_sign = policy_evict_first();
+      const uint64_t pol_v = policy_evict_last();
+      const uint32_t sign_bytes = (uint32_t)Rg * kTileRows * 16;
+      const uint32_t v_bytes = (uint32_t)kSubK * 16 * fsz;
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long u = u0; u < u1; ++u) {
+        const int i = (int)(u / p.nq), q = (int)(u % p.nq);
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * C::kStageBytes;
+        mbar_arrive_expect_tx(&full[s], sign_bytes + v_bytes);
+        const uint4* src_s = p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0;
+        bulk_g2s(st, src_s, sign_bytes, &full[s], pol_sign);
+        const uint8_t* src_v = reinterpret_cast<const uint8_t*>(p.v) +
+                               ((long long)i * p.d_in_pad + (long long)q * kSubK) * 16 * fsz;
+        bulk_g2s(st + C::kSignBytes, src_v, v_bytes, &full[s], pol_v);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (one thread) =================
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_f16_f32(kTileRows, N);
+      int s = 0;
+      uint32_t ph = 0;
+      int ab[2] = {0, 0};
+      uint32_t aph[2] = {0, 0};
+      uint32_t acc_ph = 0;
+      long long piece = 0;
+      for (long long u = u0; u < u1; ++u) {
+        const int q = (int)(u % p.nq);
+        const bool first = (u == u0) || (q == 0);
+        const bool last = (u == u1 - 1) || (q == p.nq - 1);
+        if (first && piece > 0) {  // accumulators drained by the epilogue?
+          mbar_wait(acc_empty, acc_ph);
+          acc_ph ^= 1;
+        }
+        mbar_wait(&zfull[s], ph);
+        tc_fence_after();
+        const uint32_t zaddr = smem_u32(smem + s * C::kStageBytes + C::kSignBytes + C::kVBytes);
+        for (int t = 0; t < Rg; ++t) {
+          const int wg = t & 1;
+          const int slot = wg * 2 + ab[wg];
+          mbar_wait(&a_full[slot], aph[wg]);
+          tc_fence_after();
+          const uint32_t a_col = tbase + (uint32_t)(128 * wg + 64 * ab[wg]);
+          const uint32_t d_col = tbase + C::kAccCol + (uint32_t)(t * N);
+#pragma unroll
+          for (int m = 0; m < kSubK / 16; ++m) {
+            const uint64_t bdesc = smem_desc_kmajor(zaddr + m * 2 * C::LBO, C::LBO, C::SBO);
+            mma_f16_ts(d_col, a_col + 8 * m, bdesc, idesc, (m > 0 || !first) ? 1u : 0u);
+          }
+          mma_commit(&a_empty[slot]);
+          if (++ab[wg] == 2) { ab[wg] = 0; aph[wg] ^= 1; }
+        }
+        mma_commit(&empty[s]);
+        if (last) {
+          mma_commit(acc_full);
+          ++piece;
+        }
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp < 4) {
+    // ================= Z builders: Z = V' (.) x' -> fp16 UMMA B tiles =================
+    const int bt = threadIdx.x - 64;  // 0..63
+    constexpr int kTasks = 16 * (N / 8);  // (k-group, n-group) core matrices
+    int s = 0;
+    uint32_t ph = 0;
+    for (long long u = u0; u < u1; ++u) {
+      const int i = (int)(u / p.nq), q = (int)(u % p.nq);
+      (void)i;
+      mbar_wait(&full[s], ph);
+      uint8_t* st = smem + s * C::kStageBytes;
+      const uint8_t* vs = st + C::kSignBytes;
+      uint8_t* zs = st + C::kSignBytes + C::kVBytes;
+      for (int task = bt; task < kTasks; task += 64) {
+        const int ng = task % (N / 8);
+        const int kg = task / (N / 8);
+        const int n0 = ng * 8;
+        const int r0 = n0 % 16;          // 0 or 8
+        const int bd = n0 / 16;          // b * NDIG + d
+        const int b = bd / NDIG, d = bd % NDIG;
+        const int cbase = q * kSubK + kg * 8;
+        float xs[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const int c = cbase + jj;
+          xs[jj] = (b < p.batch && c < p.d_in)
+                       ? load_act(p.x, (long long)b * p.x_stride + c, p.x_dtype) * __ldg(p.inv_s + c)
+                       : 0.f;
+        }
+        uint32_t out[8][4];  // [rr][k pair]
+#pragma unroll
+        for (int jj = 0; jj < 8; jj += 2) {
+          float z0[8], z1[8];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int kk = kg * 8 + jj + h;
+            float vv[8];
+            if (fsz == 2) {
+              const uint4 raw = *reinterpret_cast<const uint4*>(vs + (kk * 16 + r0) * 2);
+              const __nv_bfloat162* bp = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(bp[e]);
+                vv[2 * e] = f.x;
+                vv[2 * e + 1] = f.y;
+              }
+            } else {
+              const float4 a = *reinterpret_cast<const float4*>(vs + (kk * 16 + r0) * 4);
+              const float4 c4 = *reinterpret_cast<const float4*>(vs + (kk * 16 + r0) * 4 + 16);
+              vv[0] = a.x; vv[1] = a.y; vv[2] = a.z; vv[3] = a.w;
+              vv[4] = c4.x; vv[5] = c4.y; vv[6] = c4.z; vv[7] = c4.w;
+            }
+            float* zz = h == 0 ? z0 : z1;
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) {
+              const float z = vv[rr] * xs[jj + h];
+              if (NDIG == 1 || d == 0) {
+                zz[rr] = z;
+              } else {
+                zz[rr] = z - __half2float(__float2half_rn(z));  // low digit
+              }
+            }
+          }
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const __half2 hp = __floats2half2_rn(z0[rr], z1[rr]);
+            out[rr][jj / 2] = *reinterpret_cast<const uint32_t*>(&hp);
+          }
+        }
+        // Stagger rows across lanes (lane L stores row (e + L) & 7 at step e) so the
+        // 8 lanes of a quarter-warp hit distinct banks; rotate the register array
+        // by L & 7 with compile-time moves instead of dynamic (local-memory) indexing.
+        const int rot = lane & 7;
+#pragma unroll
+        for (int bit = 1; bit < 8; bit <<= 1) {
+          if (rot & bit) {
+            uint32_t tmp[8][4];
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) tmp[rr][e] = out[(rr + bit) & 7][e];
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) out[rr][e] = tmp[rr][e];
+          }
+        }
+        uint8_t* core = zs + (kg * (N / 8) + ng) * 128;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int rr = (e + rot) & 7;
+          *reinterpret_cast<uint4*>(core + rr * 16) = make_uint4(out[e][0], out[e][1], out[e][2], out[e][3]);
+        }
+      }
+      if (p.dbg_z && blockIdx.x == 0 && u == u0) {
+        __syncwarp();
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        for (int e = bt; e < C::kZBytes / 4; e += 64) p.dbg_z[e] = reinterpret_cast<const uint32_t*>(zs)[e];
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&zfull[s]);
+        mbar_arrive(&empty[s]);
+      }
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+    }
+  } else {
+    // ================= expanders + epilogue (8 warps, two warpgroups) =================
+    const int wg = (warp - 4) >> 2;
+    const int qd = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row_in_tile = qd * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
+    constexpr int kMyTiles = (R + 1) / 2;
+    float yacc[kMyTiles][NB];
+#pragma unroll
+    for (int a = 0; a < kMyTiles; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) yacc[a][b] = 0.f;
+    int s = 0;
+    uint32_t ph = 0;
+    int ab = 0;
+    uint32_t aph = 0, acc_ph = 0;
+    for (long long u = u0; u < u1; ++u) {
+      const int i = (int)(u / p.nq), q = (int)(u % p.nq);
+      const bool last = (u == u1 - 1) || (q == p.nq - 1);
+      mbar_wait(&full[s], ph);
+      const uint4* sg = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes);
+      for (int t = wg; t < Rg; t += 2) {
+        const uint4 sw = sg[t * kTileRows + row_in_tile];
+        mbar_wait(&a_empty[wg * 2 + ab], aph ^ 1);
+        tc_fence_after();
+        const uint32_t a_addr = tbase + lane_base + (uint32_t)(128 * wg + 64 * ab);
+        uint32_t o[16];
+        expand_f16(sw.x, p.one2, o);
+        tmem_st16(a_addr + 0, o);
+        expand_f16(sw.y, p.one2, o);
+        tmem_st16(a_addr + 16, o);
+        expand_f16(sw.z, p.one2, o);
+        tmem_st16(a_addr + 32, o);
+        expand_f16(sw.w, p.one2, o);
+        tmem_st16(a_addr + 48, o);
+        tmem_st_wait();
+        if (p.dbg_acc && blockIdx.x == 0 && u == u0 && t == 0) {  // test hook: read A back
+          uint32_t rb[16];
+          tmem_ld16(a_addr, rb);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) p.dbg_acc[8 * 128 * N + row_in_tile * 16 + e] = __uint_as_float(rb[e]);
+          if (threadIdx.x == 128) p.dbg_acc[8 * 128 * N + 128 * 16] = __uint_as_float(tbase);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&a_full[wg * 2 + ab]);
+        if (++ab == 2) { ab = 0; aph ^= 1; }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+
+      if (last) {
+        // ---- epilogue for block i: y += sum_r U'_i[row, r] * T[row, r, b]
+        float uu[kMyTiles][16];
+#pragma unroll
+        for (int a = 0; a < kMyTiles; ++a) {
+          const int t = wg + 2 * a;
+          if (t < Rg) {
+            const long long row = row0 + t * kTileRows + row_in_tile;
+            const long long base = ((long long)i * p.rows_pad + row) * 16;
+            if (p.f_dtype == 1) {
+              const uint4* up = reinterpret_cast<const uint4*>(
+                  reinterpret_cast<const __nv_bfloat16*>(p.u) + base);
+              const uint4 r0v = __ldg(up), r1v = __ldg(up + 1);
+              const __nv_bfloat162* b0 = reinterpret_cast<const __nv_bfloat162*>(&r0v);
+              const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&r1v);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f0 = __bfloat1622float2(b0[e]);
+                const float2 f1 = __bfloat1622float2(b1[e]);
+                uu[a][2 * e] = f0.x; uu[a][2 * e + 1] = f0.y;
+                uu[a][8 + 2 * e] = f1.x; uu[a][8 + 2 * e + 1] = f1.y;
+              }
+            } else {
+              const float4* up = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.u) + base);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float4 f = __ldg(up + e);
+                uu[a][4 * e] = f.x; uu[a][4 * e + 1] = f.y; uu[a][4 * e + 2] = f.z; uu[a][4 * e + 3] = f.w;
+              }
+            }
+          }
+        }
+        mbar_wait(acc_full, acc_ph);
+        acc_ph ^= 1;
+        tc_fence_after();
+#pragma unroll
+        for (int a = 0; a < kMyTiles; ++a) {
+          const int t = wg + 2 * a;
+          if (t < Rg) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              float tsum[16];
+#pragma unroll
+              for (int d = 0; d < NDIG; ++d) {
+                uint32_t v[16];
+                tmem_ld16(tbase + lane_base + C::kAccCol + (uint32_t)(t * N + (b * NDIG + d) * 16), v);
+                tmem_ld_wait();
+                if (p.dbg_acc && blockIdx.x == 0 && u == (long long)(u0 / p.nq * p.nq + p.nq - 1 < u1 - 1 ? u0 / p.nq * p.nq + p.nq - 1 : u1 - 1)) {
+#pragma unroll
+                  for (int r = 0; r < 16; ++r)
+                    p.dbg_acc[(t * kTileRows + row_in_tile) * N + (b * NDIG + d) * 16 + r] = __uint_as_float(v[r]);
+                }
+#pragma unroll
+                for (int r = 0; r < 16; ++r)
+                  tsum[r] = (d == 0) ? __uint_as_float(v[r]) : tsum[r] + __uint_as_float(v[r]);
+              }
+              float acc = 0.f;
+#pragma unroll
+              for (int r = 0; r < 16; ++r) acc = fmaf(uu[a][r], tsum[r], acc);
+              yacc[a][b] += acc;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+      }
+    }
+    // ---- fold this CTA's partial y into the fp32 workspace
+    if (u1 > u0) {
+#pragma unroll
+      for (int a = 0; a < kMyTiles; ++a) {
+        const int t = wg + 2 * a;
+        if (t < Rg) {
+          const int row = row0 + t * kTileRows + row_in_tile;
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            if (b < p.batch) atomicAdd(p.y_acc + (long long)b * p.rows_pad + row, yacc[a][b]);
+        }
+      }
+    }
+  }
+
+  // ---- teardown
+  __threadfence();  // order this thread's red.add's before the group counter update
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<C::kTmemCols>(tbase);
+
+  // ---- last CTA of the row group writes y and re-zeroes the workspace
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(p.counters + g, 1);
+    *last_flag = (prev == p.ctas_per_group - 1);
+  }
+  __syncthreads();
+  if (*last_flag) {
+    __threadfence();
+    const int rows_in_group = Rg * kTileRows;
+    const int total = rows_in_group * p.batch;
+    for (int e = threadIdx.x; e < total; e += kDecodeThreads) {
+      const int b = e / rows_in_group;
+      const int row = row0 + e % rows_in_group;
+      float* src = p.y_acc + (long long)b * p.rows_pad + row;
+      const float val = __ldcg(src);
+      *src = 0.f;
+      if (row < p.rows_local) {
+        const long long o = (long long)b * p.y_stride + row;
+        if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = val;
+        else reinterpret_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(val);
+      }
+    }
+    if (threadIdx.x == 0) p.counters[g] = 0;
+  }
+}
+
+}  // namespace bs

@@ -1,0 +1,81 @@
+"""CPU-side checks of the C-ABI library: it builds for sm_100a, loads, and exports
+every symbol include/bitstack.h declares; host-only entry points behave."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from bitstack_test_helpers import read_golden
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2410_23918_b200 import build as B
+    B.build()
+    from paper_2410_23918_b200 import bitstack as bsmod
+    return bsmod.load_library()
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "bitstack.h")) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"BITSTACK_API\s+[\w\s\*]+?\b(bitstack_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_four_north_star_calls():
+    syms = header_symbols()
+    for name in ("bitstack_load_blocks", "bitstack_set_num_blocks", "bitstack_matmul", "bitstack_reconstruct"):
+        assert name in syms
+
+
+def test_library_exports_every_header_symbol(lib):
+    from paper_2410_23918_b200 import bitstack as bsmod
+    out = subprocess.run(["nm", "-D", "--defined-only", bsmod.LIB_PATH], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\bT (bitstack_\w+)", out))
+    missing = [s for s in header_symbols() if s not in exported]
+    assert not missing, missing
+    assert set(bsmod.EXPORTED_SYMBOLS) == set(header_symbols())
+    for s in header_symbols():
+        assert hasattr(lib, s)
+
+
+def test_library_is_sm100a_with_tcgen05(lib):
+    """The fatbin holds sm_100a SASS with tcgen05 MMA (UTCHMMA), TMEM st/ld and bulk copies."""
+    from paper_2410_23918_b200 import bitstack as bsmod
+    sass = subprocess.run(["cuobjdump", "-sass", bsmod.LIB_PATH], capture_output=True, text=True,
+                          check=True).stdout
+    assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", bsmod.LIB_PATH], capture_output=True,
+                                       text=True).stdout
+    for mnemonic in ("UTCHMMA", "STTM", "LDTM", "UBLKCP"):
+        assert mnemonic in sass, mnemonic
+
+
+def test_block_size_bits_matches_table_a4(lib, golden_dir):
+    """Eq.9 as computed by the library reproduces Table A.4."""
+    from decimal import ROUND_HALF_UP, Decimal
+    for _, _, m, n, printed in read_golden(os.path.join(golden_dir, "table_a4.txt")):
+        bits = lib.bitstack_block_size_bits(int(m), int(n), 16, 16)
+        mib = Decimal(bits) / Decimal(8 * 2 ** 20)
+        assert mib.quantize(Decimal("0.01"), rounding=ROUND_HALF_UP) == Decimal(printed)
+    assert lib.bitstack_block_size_bits(4096, 4096, 16, 32) == 4096 * 4096 + 32 * 16 * 8192
+
+
+def test_create_rejects_bad_arguments_without_gpu(lib):
+    """Argument validation happens before any device call; no GPU here -> clean error."""
+    from paper_2410_23918_b200 import bitstack as bsmod
+    h = ctypes.c_void_p()
+    assert lib.bitstack_create(64, 64, 0, 4, 1, 0, 64, 0, ctypes.byref(h)) == -1       # k < 1
+    assert lib.bitstack_create(64, 64, 17, 4, 1, 0, 64, 0, ctypes.byref(h)) == -1      # k > 16
+    assert lib.bitstack_create(64, 64, 16, 4, 7, 0, 64, 0, ctypes.byref(h)) == -1      # dtype
+    assert lib.bitstack_create(64, 64, 16, 4, 1, 10, 5, 0, ctypes.byref(h)) == -2      # rows
+    assert lib.bitstack_create(64, 64, 16, 4, 1, 0, 65, 0, ctypes.byref(h)) == -2
+    assert b"row range" in lib.bitstack_last_error()
+    assert lib.bitstack_set_num_blocks(None, 0) == -1
+    assert lib.bitstack_matmul(None, None, 0, None, 0, 1, None) == -1
+    with pytest.raises(bsmod.BitStackError):
+        bsmod.Layer(64, 64, k=0)

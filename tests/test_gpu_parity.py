@@ -1,0 +1,298 @@
+"""GPU parity: bitstack_matmul / bitstack_reconstruct (CUDA, through the C ABI)
+against the CPU oracle on the SAME stored blocks and the SAME x.
+
+Tolerances (north star): relative L2 per batch row (reading R16)
+  <= 1e-3 with bf16/f16 factors, <= 1e-5 with fp32 factors, y in fp32;
+  bf16 y adds its own rounding (1.7e-3 measured on the oracle) -> 4e-3.
+Sign unpacking is checked bit-exactly (P15), with no float tolerance.
+"""
+import numpy as np
+import pytest
+
+from bitstack_test_helpers import blocks_from_arrays, stack_blocks
+from oracle import bitstack_oracle as O
+from synthetic import (channel_gains, make_calibration, make_random_blocks, make_weight, make_x,
+                       random_signs_bytes, seed_for)
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def bs():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2410_23918_b200 import build
+    build.build()
+    import paper_2410_23918_b200 as pkg
+    pkg.load_library()
+    return pkg
+
+
+def compress_case(d_out, d_in, n, dtype, seed, method="exact", p=None):
+    g = channel_gains(d_in, seed + 4)
+    w = make_weight(d_out, d_in, seed)
+    x_cal = make_calibration(p or max(256, d_in), g, seed + 1)
+    s, blocks = O.compress(w, x_cal, n, 16, dtype=dtype, method=method, seed=seed)
+    s32 = s.astype(np.float32)
+    return g, s32, blocks
+
+
+def make_layer(bs, d_out, d_in, blocks, s32, dtype, n_capacity=None, row_begin=0, row_end=None):
+    signs, u, v = stack_blocks(blocks, dtype)
+    lay = bs.Layer(d_out, d_in, k=16, n_capacity=n_capacity or len(blocks), factor_dtype=dtype,
+                   row_begin=row_begin, row_end=row_end)
+    lay.load_blocks(0, signs, u, v, s32)
+    torch.cuda.synchronize()
+    return lay
+
+
+def oracle_y(blocks, s32, n, x):
+    return O.matmul_dense(blocks, s32.astype(np.float64), n, x)
+
+
+def gpu_y(lay, x_np, x_dtype=torch.float32, y_dtype=torch.float32):
+    x = torch.from_numpy(np.ascontiguousarray(x_np, dtype=np.float32)).to(x_dtype).cuda()
+    y = lay.matmul(x, y_dtype=y_dtype)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy().astype(np.float64), x.float().cpu().numpy().astype(np.float64)
+
+
+# ------------------------------------------------------------------ P15: bit-exact unpack
+@pytest.mark.parametrize("shape", [(256, 384), (300, 200), (128, 1000)])
+def test_sign_unpack_bit_exact(bs, shape):
+    """U_i[:,0] = 2^i, V_i[:,0] = 1, other columns 0, s = 1  =>  reconstruct in fp32
+    gives sum_i 2^i S_i exactly; decoding it must give back every canonical bit."""
+    d_out, d_in = shape
+    n = 16
+    signs = random_signs_bytes(n, d_out, d_in, seed=7 + d_out)
+    u = np.zeros((n, d_out, 16), np.float32)
+    v = np.zeros((n, d_in, 16), np.float32)
+    for i in range(n):
+        u[i, :, 0] = 2.0 ** i
+        v[i, :, 0] = 1.0
+    lay = bs.Layer(d_out, d_in, k=16, n_capacity=n, factor_dtype="f32")
+    lay.load_blocks(0, signs, u, v, np.ones(d_in, np.float32))
+    w = lay.reconstruct(torch.float32).cpu().numpy().astype(np.int64)
+    # decode: w = sum_i 2^i (2 b_i - 1) = 2 sum_i 2^i b_i - (2^n - 1)
+    code = (w + (2 ** n - 1)) // 2
+    assert np.all((w + (2 ** n - 1)) % 2 == 0)
+    for i in range(n):
+        bits = (code >> i) & 1
+        want = np.unpackbits(signs[i], bitorder="little")[: d_out * d_in].reshape(d_out, d_in)
+        np.testing.assert_array_equal(bits, want)
+
+
+# ------------------------------------------------------------------ C1: fp32 factors, 1e-5
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_c1_parity_fp32(bs, kernel):
+    """Config C1 (256x512, n=4, k=16, fp32 factors, exact LAPACK loop), batch 1."""
+    g, s32, blocks = compress_case(256, 512, 4, "f32", seed_for(1))
+    lay = make_layer(bs, 256, 512, blocks, s32, "f32")
+    lay.set_kernel(kernel)
+    x = make_x(1, g, seed_for(1, 0, "x"))
+    for n in range(0, 5):
+        lay.set_num_blocks(n)
+        y, xr = gpu_y(lay, x)
+        ref = oracle_y(blocks, s32, n, xr)
+        if n == 0:
+            assert not np.any(y)
+        else:
+            assert O.relative_l2(y, ref) <= 1e-5, (n, O.relative_l2(y, ref))
+
+
+# ------------------------------------------------------------------ ragged shapes, batches
+@pytest.mark.parametrize("shape", [(384, 640), (200, 300), (1100, 260)])
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_bf16_parity_ragged(bs, shape, kernel):
+    d_out, d_in = shape
+    g, s32, blocks = compress_case(d_out, d_in, 5, "bf16", 31 + d_out)
+    lay = make_layer(bs, d_out, d_in, blocks, s32, "bf16")
+    lay.set_kernel(kernel)
+    for batch in (1, 2, 3, 5, 8, 16, 17):
+        x = make_x(batch, g, 77 + batch)
+        y, xr = gpu_y(lay, x)
+        ref = oracle_y(blocks, s32, 5, xr)
+        assert O.relative_l2(y, ref) <= 1e-3, (batch, O.relative_l2(y, ref))
+
+
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
+def test_fp32_factor_batches(bs, kernel):
+    """fp32 factors use two fp16 digits of Z on the tensor-core path: 1e-5 at every batch."""
+    g, s32, blocks = compress_case(384, 512, 3, "f32", 91)
+    lay = make_layer(bs, 384, 512, blocks, s32, "f32")
+    lay.set_kernel(kernel)
+    for batch in (1, 2, 4, 7, 8, 9):
+        x = make_x(batch, g, 5 + batch)
+        y, xr = gpu_y(lay, x)
+        assert O.relative_l2(y, oracle_y(blocks, s32, 3, xr)) <= 1e-5
+
+
+def test_f16_factors_and_dtypes(bs):
+    """Paper's own FP16 factors; bf16/f16 activations; bf16 output."""
+    g, s32, blocks = compress_case(256, 384, 4, "f16", 55)
+    lay = make_layer(bs, 256, 384, blocks, s32, "f16")
+    x = make_x(3, g, 8)
+    for xdt in (torch.float32, torch.bfloat16, torch.float16):
+        y, xr = gpu_y(lay, x, x_dtype=xdt)
+        assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 1e-3
+    y, xr = gpu_y(lay, x, y_dtype=torch.bfloat16)
+    assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 4e-3
+
+
+# ------------------------------------------------------------------ C2: every n, full size
+@pytest.fixture(scope="module")
+def c2(bs):
+    g, s32, blocks = compress_case(4096, 4096, 16, "bf16", seed_for(2), method="randomized", p=4096)
+    lay = make_layer(bs, 4096, 4096, blocks, s32, "bf16")
+    return g, s32, blocks, lay
+
+
+def test_c2_parity_every_n(c2):
+    """Config C2 (Llama-3.1-8B q_proj 4096x4096, n=1..16, B=1): <= 1e-3 at every n,
+    in the launch configuration bench.py times (auto kernel = tcgen05)."""
+    g, s32, blocks, lay = c2
+    x = make_x(1, g, seed_for(2, 0, "x"))
+    xt = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).cuda()
+    xr = xt.float().cpu().numpy().astype(np.float64)
+    partial = [O.matmul_dense([b], s32.astype(np.float64), 1, xr) for b in blocks]  # Eq.8 is a sum
+    ref = np.zeros_like(partial[0])
+    for n in range(1, 17):
+        ref = ref + partial[n - 1]
+        lay.set_num_blocks(n)
+        y = lay.matmul(xt).cpu().numpy().astype(np.float64)
+        err = O.relative_l2(y, ref)
+        assert err <= 1e-3, (n, err)
+
+
+def test_c2_reconstruct_matches_oracle(c2):
+    g, s32, blocks, lay = c2
+    lay.set_num_blocks(3)
+    w = lay.reconstruct(torch.float32).cpu().numpy().astype(np.float64)
+    ref = O.reconstruct(blocks, s32.astype(np.float64), 3, 4096, 4096)
+    assert np.linalg.norm(w - ref) / np.linalg.norm(ref) <= 1e-6
+
+
+# ------------------------------------------------------------------ stack semantics
+def test_incremental_load_offload_walk(bs):
+    """Blocks pushed one at a time, random set_num_blocks walk, re-push after offload:
+    y always equals the oracle at the active level."""
+    g, s32, blocks = compress_case(256, 256, 6, "bf16", 123)
+    signs, u, v = stack_blocks(blocks, "bf16")
+    lay = bs.Layer(256, 256, k=16, n_capacity=6, factor_dtype="bf16")
+    x = make_x(2, g, 4)
+    rng = np.random.default_rng(0)
+    lay.load_blocks(0, signs[:1], u[:1], v[:1], s32)
+    resident = 1
+    for step in range(30):
+        if resident < 6 and rng.random() < 0.4:
+            lay.load_blocks(resident, signs[resident:resident + 1], u[resident:resident + 1], v[resident:resident + 1])
+            resident += 1
+        n = int(rng.integers(0, resident + 1))
+        lay.set_num_blocks(n)
+        y, xr = gpu_y(lay, x)
+        ref = oracle_y(blocks, s32, n, xr)
+        if n == 0:
+            assert not np.any(y)
+        else:
+            assert O.relative_l2(y, ref) <= 1e-3
+    # offload to 2 then re-push block 2 (overwrites in place)
+    lay.set_num_blocks(2)
+    lay.load_blocks(2, signs[2:3], u[2:3], v[2:3])
+    assert lay.info()["n_resident"] == 3
+    lay.set_num_blocks(3)
+    y, xr = gpu_y(lay, x)
+    assert O.relative_l2(y, oracle_y(blocks, s32, 3, xr)) <= 1e-3
+
+
+def test_errors_and_edge_cases(bs):
+    g, s32, blocks = compress_case(128, 256, 3, "bf16", 9)
+    signs, u, v = stack_blocks(blocks, "bf16")
+    lay = bs.Layer(128, 256, k=16, n_capacity=3, factor_dtype="bf16")
+    with pytest.raises(bs.BitStackError) as e:
+        lay.set_num_blocks(1)
+    assert e.value.name == "E_LEVEL_OUT_OF_RANGE"
+    with pytest.raises(bs.BitStackError) as e:           # s required for block 0
+        lay.load_blocks(0, signs, u, v, None)
+    assert e.value.name == "E_INVALID_ARG"
+    with pytest.raises(bs.BitStackError) as e:           # first_block > resident
+        lay.load_blocks(1, signs[:1], u[:1], v[:1])
+    assert e.value.name == "E_LEVEL_OUT_OF_RANGE"
+    lay.load_blocks(0, signs, u, v, s32)
+    with pytest.raises(bs.BitStackError) as e:           # capacity
+        lay.load_blocks(3, signs[:1], u[:1], v[:1])
+    assert e.value.name == "E_CAPACITY"
+    bad = np.zeros((1, (127 * 255 + 7) // 8), np.uint8)
+    bad[0, -1] = 0xFF                                      # pad bits set
+    lay2 = bs.Layer(127, 255, k=16, n_capacity=1, factor_dtype="bf16")
+    with pytest.raises(bs.BitStackError) as e:
+        lay2.load_blocks(0, bad, np.zeros((1, 127, 16), np.uint16), np.zeros((1, 255, 16), np.uint16),
+                         np.ones(255, np.float32))
+    assert e.value.name == "E_MALFORMED_BUFFER"
+    s_bad = s32.copy()
+    s_bad[3] = 0.0
+    with pytest.raises(bs.BitStackError):
+        lay.load_blocks(0, signs, u, v, s_bad)
+    # batch 0 is a no-op, n = 0 gives exact zeros
+    x = torch.zeros((0, 256), device="cuda")
+    y = lay.matmul(x)
+    assert y.shape == (0, 128)
+    lay.set_num_blocks(0)
+    y, _ = gpu_y(lay, make_x(4, g, 1))
+    assert not np.any(y)
+
+
+def test_row_shards_concatenate_to_full(bs):
+    """Row sharding: shards [r0, r1) computed independently and
+    concatenated equal the unsharded layer (no collective needed on one GPU)."""
+    g, s32, blocks = compress_case(640, 384, 4, "bf16", 17)
+    x = make_x(3, g, 2)
+    full = make_layer(bs, 640, 384, blocks, s32, "bf16")
+    yf, xr = gpu_y(full, x)
+    cuts = [0, 128, 200, 512, 640]
+    parts = []
+    for a, b in zip(cuts, cuts[1:]):
+        sh = make_layer(bs, 640, 384, blocks, s32, "bf16", row_begin=a, row_end=b)
+        parts.append(gpu_y(sh, x)[0])
+    ys = np.concatenate(parts, axis=1)
+    ref = oracle_y(blocks, s32, 4, xr)
+    assert O.relative_l2(ys, ref) <= 1e-3
+    assert O.relative_l2(ys, yf) <= 1e-5
+
+
+# ------------------------------------------------------------------ full sizes, sampled rows
+def _sampled_reference(signs, u, v, s, n, x, rows, d_out, d_in):
+    """Oracle y on a subset of output rows: slice the stored blocks' rows (oracle unpack
+    / pack) and run the dense oracle on the slice."""
+    sub = []
+    for i in range(n):
+        sm = O.unpack_signs(signs[i], d_out, d_in)[rows]
+        sub.append(O.Block(signs=O.pack_signs(sm), u=np.asarray(u[i][rows], np.float64),
+                           v=np.asarray(v[i], np.float64)))
+    return O.matmul_dense(sub, s.astype(np.float64), n, x)
+
+
+@pytest.mark.parametrize("name,d_out,d_in,n,batch", [
+    ("c5_down_70b", 8192, 28672, 12, 1),
+    ("c5_down_70b_b4", 8192, 28672, 12, 4),
+    ("c3_up", 14336, 4096, 8, 16),
+    ("c4_kproj", 1024, 4096, 3, 1),
+])
+def test_full_size_sampled_rows(bs, name, d_out, d_in, n, batch):
+    """Full BASELINE shapes (random stored-form blocks from synthetic/): the GPU's y on
+    96 sampled rows equals the oracle's, <= 1e-3."""
+    signs, u32, v32, s = make_random_blocks(n, d_out, d_in, 16, seed=seed_for(5, 1, "blocks"))
+    ub = O.bf16_bits(u32)
+    vb = O.bf16_bits(v32)
+    u_val = O.round_to_dtype(u32, "bf16")
+    v_val = O.round_to_dtype(v32, "bf16")
+    lay = bs.Layer(d_out, d_in, k=16, n_capacity=n, factor_dtype="bf16")
+    lay.load_blocks(0, signs, ub, vb, s)
+    g = channel_gains(d_in, seed_for(5, 1, "gains"))
+    x = make_x(batch, g, 3)
+    y, xr = gpu_y(lay, x, x_dtype=torch.bfloat16)
+    rows = np.sort(np.random.default_rng(1).choice(d_out, 96, replace=False))
+    ref = _sampled_reference(signs, u_val, v_val, s, n, xr, rows, d_out, d_in)
+    assert O.relative_l2(y[:, rows], ref) <= 1e-3
+    del lay

@@ -338,3 +338,7 @@ def test_relative_l2_metric():
     assert O.relative_l2([[3.0, 4.0], [1, 0]], [[3.0, 4.0], [2, 0]]) == pytest.approx(0.5)
     assert O.relative_l2([[0.0, 0.0]], [[0.0, 0.0]]) == 0.0
     assert O.relative_l2([[1e-30, 0.0]], [[0.0, 0.0]]) == float("inf")
+    assert O.relative_l2([[np.nan, 1.0]], [[1.0, 1.0]]) == float("inf")   # NaN never passes
+    assert O.relative_l2([[1.0, 1.0]], [[np.inf, 1.0]]) == float("inf")
+    with pytest.raises(ValueError):
+        O.relative_l2([[1.0, 2.0]], [[1.0, 2.0, 3.0]])
