@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""BitStack W_hat_n x on B200: us/layer and HBM GB/s vs peak (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload c2|c5]
+
+One step = one bitstack_matmul of the workload's layer (the whole hot path: the
+fused tcgen05 decode kernel; at N > 1 each rank computes its row shard and the
+output slices are all-gathered over NCCL).  Blocks are synthetic stored-form
+blocks from synthetic/ (kernel time does not depend on values); L2 is defeated
+by rotating over enough layer copies that the working set exceeds 4x L2.
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (oracle/)
+on the host cores on a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synthetic import CONFIGS, channel_gains, make_random_blocks, make_x, seed_for  # noqa: E402
+
+L2_BYTES = 126 * 2 ** 20
+WORKLOADS = {
+    "c2": dict(CONFIGS["c2"], label="c2: Llama-3.1-8B q_proj 4096x4096, n=16 blocks, k=16, bf16 factors, decode"),
+    "c5": dict(CONFIGS["c5"], label="c5: Llama-3.1-70B down_proj 8192x28672, n=12 blocks, k=16, bf16 factors, decode"),
+}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def alg_bytes_per_rank(w, rows, batch, n, x_bytes=2, y_bytes=4):
+    """n (r d_in / 8 + k (r + d_in) f) + B d_in |x| + B r |y| + 4 d_in."""
+    return n * (rows * w["d_in"] / 8 + w["k"] * (rows + w["d_in"]) * 2) + batch * w["d_in"] * x_bytes \
+        + batch * rows * y_bytes + 4 * w["d_in"]
+
+
+class ClockSampler:
+    """Polls NVML (SM clock, max clock, throttle reasons) every ~2 ms while active."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": float(self.max_mhz), "reasons": names, "samples": len(self.samples)}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count()
+
+
+def oracle_sample_time(w, n, batch, rows_sample, steps, warmup, seed):
+    """Time the dense oracle (Eq.8 + Eq.4, fp64) for `rows_sample` output rows of the
+    workload's layer: returns (seconds per step, algorithmic bytes per step)."""
+    from oracle import bitstack_oracle as O
+    d_out, d_in, k = w["d_out"], w["d_in"], w["k"]
+    signs, u, v, s = make_random_blocks(n, d_out, d_in, k, seed=seed)
+    u = O.round_to_dtype(u, "bf16")
+    v = O.round_to_dtype(v, "bf16")
+    rows = np.arange(rows_sample)
+    sub = []
+    for i in range(n):  # stored blocks restricted to the sampled rows (setup, untimed)
+        sm = O.unpack_signs(signs[i], d_out, d_in)[rows]
+        sub.append(O.Block(signs=O.pack_signs(sm), u=u[i][rows], v=v[i]))
+    x = make_x(batch, channel_gains(d_in, seed + 1), seed + 2)
+    for _ in range(warmup):
+        O.matmul_dense(sub, s.astype(np.float64), n, x)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.matmul_dense(sub, s.astype(np.float64), n, x)
+    dt = (time.perf_counter() - t0) / steps
+    return dt, alg_bytes_per_rank(w, rows_sample, batch, n)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--n", type=int, default=None, help="active blocks (default: the config's n)")
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replay")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also report us/layer for n = 1, 2, 4, 8, 16")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = dict(WORKLOADS[args.workload])
+    n = args.n or w["n"]
+    batch = args.batch or w["batch"]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        budget_s = 60.0
+        # bounded row sample: calibrate on 16 rows, then size the sample to the budget
+        t16, _ = oracle_sample_time(w, n, batch, 16, 1, 0, seed_for(2, 0, "blocks"))
+        rows = int(max(16, min(w["d_out"], 16 * budget_s / max(t16, 1e-6) / (args.steps + args.warmup))))
+        dt, by = oracle_sample_time(w, n, batch, rows, args.steps, args.warmup, seed_for(2, 0, "blocks"))
+        val = by / dt / 1e9
+        line = {
+            "impl": "reference", "metric": "bitstack_matmul HBM GB/s (algorithmic bytes / time)",
+            "value": val, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (stored-form random blocks, synthetic/ recipe)",
+            "config": {"workload": w["label"], "d_out": w["d_out"], "d_in": w["d_in"], "n": n, "k": w["k"],
+                       "batch": batch, "parallelism": "cpu", "sample_rows": rows},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": f"dense oracle (fp64 numpy) for {rows} of {w['d_out']} output rows, all {n} blocks"},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2410_23918_b200 import build as B
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2410_23918_b200 as pkg
+    pkg.load_library()
+
+    d_out, d_in, k = w["d_out"], w["d_in"], w["k"]
+    r0 = d_out * rank // world
+    r1 = d_out * (rank + 1) // world
+    rows = r1 - r0
+    # ---- layer copies: working set per rank >= 4 x L2 (inputs larger than L2)
+    per_layer = alg_bytes_per_rank(w, rows, batch, n)
+    copies = max(2, math.ceil(4 * L2_BYTES / per_layer))
+    signs, u32, v32, s = make_random_blocks(w["n"], d_out, d_in, k, seed=seed_for(2, 0, "blocks"))
+    u_bf = torch.from_numpy(u32).to(torch.bfloat16)
+    v_bf = torch.from_numpy(v32).to(torch.bfloat16)
+    layers = []
+    for c in range(copies):
+        lay = pkg.Layer(d_out, d_in, k=k, n_capacity=w["n"], factor_dtype="bf16", row_begin=r0, row_end=r1,
+                        device=local_rank)
+        lay.load_blocks(0, signs, u_bf, v_bf, s)
+        lay.set_num_blocks(n)
+        layers.append(lay)
+    x = torch.from_numpy(make_x(batch, channel_gains(d_in, 5), 6).astype(np.float32)).to(torch.bfloat16).cuda()
+    y = torch.empty((batch, rows), dtype=torch.float32, device="cuda")
+    y_full = torch.empty((world, batch, rows), dtype=torch.float32, device="cuda") if world > 1 else None
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step(i):
+        layers[i % copies].matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, batch, sh)
+        if world > 1:
+            dist.all_gather_into_tensor(y_full, y)
+
+    def timed(nsteps, use_graph):
+        graph = None
+        if use_graph:
+            gs = min(nsteps, copies * max(1, 256 // copies))
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.graph(graph, stream=cap):
+                for i in range(gs):
+                    layers[i % copies].matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, batch,
+                                                  cap.cuda_stream)
+            stream.wait_stream(cap)
+            reps = max(1, nsteps // gs)
+            nsteps = reps * gs
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = pkg.launch_count()
+        e0.record()
+        if graph is not None:
+            for _ in range(reps):
+                graph.replay()
+        else:
+            for i in range(nsteps):
+                step(i)
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        launches = pkg.launch_count() - l0 if graph is None else nsteps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, nsteps, launches
+
+    use_graph = (not args.no_graph) and world == 1
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local_rank)
+    with sampler:
+        ms, ksteps, launches = timed(args.steps, use_graph)
+        # live per-launch kernel time of the decode kernel (CUDA events on its stream)
+        kp = min(max(args.steps, 64), 4096)
+        pkg.profile_begin(kp)
+        for i in range(kp):
+            layers[i % copies].matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, batch, sh)
+        torch.cuda.synchronize()
+        nk, kms = pkg.profile_end()
+    clocks = sampler.summary()
+    ms_step = ms / ksteps
+    total_bytes = alg_bytes_per_rank(w, rows, batch, n)  # this rank
+    if world > 1:
+        tb = torch.tensor([total_bytes], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tb)
+        total_bytes = float(tb.item())
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+    kernel_ms = kms / max(nk, 1)
+    achieved = alg_bytes_per_rank(w, rows, batch, n) / (kernel_ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            traffic = tj.get(f"{args.workload}_n{n}_b{batch}_g{world}")
+        except Exception:  # noqa: BLE001
+            traffic = None
+
+    # ---- e2e: public API with host buffers (pinned), copies inside the timed region
+    x_h = x.cpu().pin_memory()
+    y_h = torch.empty((batch, d_out if world > 1 else rows), dtype=torch.float32).pin_memory()
+    ke = min(args.steps, 2000)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(ke):
+        x.copy_(x_h, non_blocking=True)
+        layers[i % copies].matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, batch, sh)
+        if world > 1:
+            dist.all_gather_into_tensor(y_full, y)
+            y_h.copy_(y_full.permute(1, 0, 2).reshape(batch, d_out), non_blocking=True)
+        else:
+            y_h.copy_(y, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / ke
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+           "h2d_bytes_per_step": int(x_h.numel() * x_h.element_size()),
+           "d2h_bytes_per_step": int(y_h.numel() * y_h.element_size())}
+
+    sweep = None
+    if args.sweep and world == 1:
+        sweep = {}
+        for nn in (1, 2, 4, 8, 16):
+            if nn > w["n"]:
+                continue
+            for lay in layers:
+                lay.set_num_blocks(nn)
+            per = alg_bytes_per_rank(w, rows, batch, nn)
+            cp = max(2, math.ceil(4 * L2_BYTES / per))
+            cp = min(cp, copies)
+            msn, kn, _ = timed(max(2000, 4 * cp), use_graph)
+            us = msn / kn * 1e3
+            sweep[str(nn)] = {"us_per_layer": us, "GBps": per / (us * 1e-6) / 1e9,
+                              "l2_note": "rotation" if cp * per >= 4 * L2_BYTES else "partially L2-resident"}
+        for lay in layers:
+            lay.set_num_blocks(n)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rows_s = 256
+        dt, by = oracle_sample_time(w, n, batch, rows_s, 1, 0, seed_for(2, 0, "blocks"))
+        cpu = {"value": by / dt / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"dense oracle (fp64 numpy, Eq.8+Eq.4) for {rows_s} of {d_out} output rows, "
+                         f"all {n} blocks, 1 call ({dt:.2f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "bitstack_matmul HBM GB/s (algorithmic bytes / time) [us/layer in ms_per_step]",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": ksteps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f16 MMA operands, fp32 accumulate",
+            "data": "synthetic (stored-form random blocks + activations, synthetic/ recipe)",
+            "config": {"workload": w["label"], "d_out": d_out, "d_in": d_in, "n": n, "k": k, "batch": batch,
+                       "factor_dtype": "bf16", "x_dtype": "bf16", "y_dtype": "f32",
+                       "parallelism": f"tp{world} (row shards + NCCL all-gather)" if world > 1 else "tp1",
+                       "l2": f"inputs larger than L2: rotation over {copies} layer copies "
+                             f"({copies * per_layer / 2 ** 20:.0f} MiB/rank > 4x126 MiB)",
+                       "timing": "CUDA-graph replay" if use_graph else "eager launches"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "bs::zq_kernel<1> + bs::decode_f8_kernel<1> (PDL pair)", "kernel_us": kernel_ms * 1e3,
+                         "kernel_launches_timed": nk,
+                         "bytes_per_launch": alg_bytes_per_rank(w, rows, batch, n)},
+            "clocks": clocks,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "cpu_baseline": cpu,
+        }
+        if sweep:
+            line["n_sweep"] = sweep
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

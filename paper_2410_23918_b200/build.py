@@ -11,7 +11,12 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbitstack.so")
 SOURCES = ["bitstack.cu"]
-HEADERS = ["aux_kernels.cuh", "decode_tc.cuh", "ptx.cuh"]
+
+
+def _deps():
+    """Every CUDA source/header under csrc/ plus the public header (content-hashed)."""
+    files = sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".h")))
+    return [os.path.join(CSRC, f) for f in files] + [os.path.join(ROOT, "include", "bitstack.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -30,8 +35,7 @@ def _nvcc() -> str:
 def _digest() -> str:
     """Content hash of every source + the flags (mtimes do not survive a repo snapshot)."""
     h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "bitstack.h")]
-    for d in deps:
+    for d in _deps():
         with open(d, "rb") as f:
             h.update(f.read())
     return h.hexdigest()

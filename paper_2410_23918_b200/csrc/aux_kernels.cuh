@@ -11,17 +11,22 @@
 
 namespace bs {
 
-// Device sign layout: per block, per 128-column subchunk q, per
-// (padded) local row j, one uint4 = 4 words; bit p of word w holds column
-//   c = 128 q + 32 w + 2 (p & 15) + (p >> 4)
-// i.e. fp16 pairs (2t', 2t'+1) sit in bits (t', t'+16) so that one LOP3 + one
-// IMAD expands a pair.  Pad rows/columns hold bit 0 (-1); Z and U are 0 there.
-__device__ __forceinline__ int dev_bit_to_col(int w, int p) { return 32 * w + 2 * (p & 15) + (p >> 4); }
-__host__ __device__ __forceinline__ int col_to_dev_bit(int cl /*0..31*/) { return (cl >> 1) + 16 * (cl & 1); }
+// Device sign layouts: per block, per 128-column subchunk q, per
+// (padded) local row j, one uint4 = 4 words.  Bit p of word w holds column
+//   layout 0 ("F16", fp16 A operand):  c = 128 q + 32 w + 2 (p & 15) + (p >> 4)
+//   layout 1 ("F8",  e4m3 A operand):  c = 128 q + 32 w + 4 (p & 7)  + (p >> 3)
+// so that one LOP3 + one IMAD expands a pair (fp16) or a quad (e4m3) of K-adjacent
+// elements.  Pad rows/columns hold bit 0 (-1); Z and U are 0 there.
+__host__ __device__ __forceinline__ int dev_bit_to_col(int layout, int w, int p) {
+  return layout == 0 ? 32 * w + 2 * (p & 15) + (p >> 4) : 32 * w + 4 * (p & 7) + (p >> 3);
+}
+__host__ __device__ __forceinline__ int col_to_dev_bit(int layout, int cl /*0..31*/) {
+  return layout == 0 ? (cl >> 1) + 16 * (cl & 1) : (cl >> 2) + 8 * (cl & 3);
+}
 
 __global__ void repack_signs_kernel(const uint8_t* __restrict__ canon, uint32_t* __restrict__ dev,
                                     int count, long long canon_bytes, long long d_in, int nq,
-                                    int rows_pad, long long rows_local, long long row_begin) {
+                                    int rows_pad, long long rows_local, long long row_begin, int layout) {
   const long long words_per_block = (long long)nq * rows_pad * 4;
   const long long total = words_per_block * count;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -38,7 +43,7 @@ __global__ void repack_signs_kernel(const uint8_t* __restrict__ canon, uint32_t*
       const uint8_t* src = canon + (long long)blk * canon_bytes;
 #pragma unroll 4
       for (int pb = 0; pb < 32; ++pb) {
-        const long long c = 128LL * q + dev_bit_to_col(w, pb);
+        const long long c = 128LL * q + dev_bit_to_col(layout, w, pb);
         if (c < d_in) {
           const long long bit = rowg * d_in + c;
           word |= (uint32_t)((src[bit >> 3] >> (bit & 7)) & 1u) << pb;
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(128) matmul_simt_kernel(
     const uint4* __restrict__ signs, const void* __restrict__ u, const void* __restrict__ v,
     const float* __restrict__ inv_s, const void* __restrict__ x, void* __restrict__ y, int n,
     int nq, int rows_pad, long long rows_local, long long d_in, long long d_in_pad, int f_dt,
-    int x_dt, int y_dt, long long x_stride, long long y_stride) {
+    int x_dt, int y_dt, long long x_stride, long long y_stride, int layout) {
   __shared__ float zs[128][17];
   const int tile = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int row = tile * 128 + tid;
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(128) matmul_simt_kernel(
       for (int w = 0; w < 4; ++w) {
         for (int pb = 0; pb < 32; ++pb) {
           const float sg = ((words[w] >> pb) & 1u) ? 1.f : -1.f;
-          const int c = 32 * w + 2 * (pb & 15) + (pb >> 4);
+          const int c = dev_bit_to_col(layout, w, pb);
 #pragma unroll
           for (int r = 0; r < 16; ++r) t[r] = fmaf(sg, zs[c][r], t[r]);
         }
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(128) matmul_simt_kernel(
 __global__ void __launch_bounds__(256) reconstruct_kernel(
     const uint4* __restrict__ signs, const void* __restrict__ u, const void* __restrict__ v,
     const float* __restrict__ inv_s, void* __restrict__ w, int n, int nq, int rows_pad,
-    long long rows_local, long long d_in, long long d_in_pad, int f_dt, int w_dt) {
+    long long rows_local, long long d_in, long long d_in_pad, int f_dt, int w_dt, int layout) {
   __shared__ float us[8][16];
   __shared__ float vs[32][17];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(
       const uint4 sw = signs[((long long)i * nq + q) * rows_pad + row];
       const uint32_t words[4] = {sw.x, sw.y, sw.z, sw.w};
       const uint32_t word = words[cl / 32];
-      const int pb = col_to_dev_bit(cl % 32);
+      const int pb = col_to_dev_bit(layout, cl % 32);
       acc += ((word >> pb) & 1u) ? m : -m;
     }
   }

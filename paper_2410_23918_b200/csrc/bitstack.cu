@@ -15,6 +15,7 @@
 
 #include "../../include/bitstack.h"
 #include "aux_kernels.cuh"
+#include "decode_f8.cuh"
 #include "decode_tc.cuh"
 
 struct bitstack_layer_s {
@@ -24,6 +25,7 @@ struct bitstack_layer_s {
   int32_t k = 0, n_cap = 0, n_res = 0, n_act = 0;
   bitstack_dtype fdt = BITSTACK_BF16;
   int dev_fdt = 1;  // device factor storage: 0 f32, 1 bf16
+  int layout = 1;   // device sign layout: 0 = F16 (fp32 factors, fp16 MMA), 1 = F8 (e4m3 MMA)
   int device = 0;
   int sm_count = 148;
   bitstack_kernel kernel = BITSTACK_KERNEL_AUTO;
@@ -33,6 +35,9 @@ struct bitstack_layer_s {
   float* inv_s = nullptr;
   float* zscale = nullptr;
   float* y_acc = nullptr;  // [16][rows_pad]
+  uint8_t* zq = nullptr;   // e4m3 path: Zq units of the current call (grown on demand)
+  int64_t zq_bytes = 0;
+  int* status = nullptr;   // sticky device-side numeric-range flag
   int* counters = nullptr; // [row_tiles]
   int64_t bytes = 0;
   int64_t block_bytes = 0;
@@ -111,6 +116,66 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
   return BITSTACK_OK;
 }
 
+// e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
+template <int NB> struct F8Geom;
+template <> struct F8Geom<1> { static constexpr int R = 4; };
+template <> struct F8Geom<2> { static constexpr int R = 2; };
+template <> struct F8Geom<4> { static constexpr int R = 2; };
+
+template <int NB>
+bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_in, int grid, cudaStream_t st) {
+  using G = F8Geom<NB>;
+  using C = bs::DecodeF8Cfg<NB, G::R>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(bs::decode_f8_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            C::kSmemBytes));
+    attr_done = true;
+  }
+  const int64_t units = (int64_t)prm_in.n * prm_in.nq;
+  const int64_t need = units * C::kZUnit;
+  if (need > L->zq_bytes) {  // grows once per larger batch class; never inside steady state
+    CK(cudaStreamSynchronize(st));
+    cudaFree(L->zq);
+    L->zq = nullptr;
+    const int64_t cap = (int64_t)L->n_cap * L->nq * C::kZUnit;
+    CK(cudaMalloc((void**)&L->zq, (size_t)cap));
+    L->bytes += cap - L->zq_bytes;
+    L->zq_bytes = cap;
+  }
+  bs::ZqParams zp;
+  zp.v = prm_in.v;
+  zp.inv_s = prm_in.inv_s;
+  zp.x = prm_in.x;
+  zp.zq = L->zq;
+  zp.x_stride = prm_in.x_stride;
+  zp.nq = prm_in.nq;
+  zp.d_in = prm_in.d_in;
+  zp.d_in_pad = prm_in.d_in_pad;
+  zp.batch = prm_in.batch;
+  zp.x_dtype = prm_in.x_dtype;
+  zp.f_dtype = prm_in.f_dtype;
+  bs::zq_kernel<NB><<<(unsigned)units, 128, 0, st>>>(zp);
+  count_launch();
+  CK(cudaGetLastError());
+  bs::DecodeParams prm = prm_in;
+  prm.zq = L->zq;
+  prm.status = L->status;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(bs::kF8Threads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8_kernel<NB, G::R>, prm));
+  count_launch();
+  return BITSTACK_OK;
+}
+
 template <int NDIG>
 bitstack_status dispatch_decode(int nb, const bs::DecodeParams& prm, int grid, cudaStream_t st) {
   switch (nb) {
@@ -119,7 +184,6 @@ bitstack_status dispatch_decode(int nb, const bs::DecodeParams& prm, int grid, c
     case 4: return launch_decode<4, NDIG>(prm, grid, st);
     case 8: return launch_decode<8, NDIG>(prm, grid, st);
     default:
-      if constexpr (NDIG == 1) return launch_decode<16, 1>(prm, grid, st);
       return fail(BITSTACK_E_INVALID_ARG, "internal: batch chunk %d", nb);
   }
 }
@@ -185,6 +249,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   L->n_cap = n_capacity;
   L->fdt = factor_dtype;
   L->dev_fdt = factor_dtype == BITSTACK_BF16 ? 1 : 0;
+  L->layout = factor_dtype == BITSTACK_F32 ? 0 : 1;
   L->device = device;
   L->sm_count = prop.multiProcessorCount;
 
@@ -209,6 +274,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * 16 * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->y_acc, (int64_t)16 * L->rows_pad * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->status, 16);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     bitstack_destroy(L);
@@ -230,6 +296,8 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   cudaFree(L->zscale);
   cudaFree(L->y_acc);
   cudaFree(L->counters);
+  cudaFree(L->status);
+  cudaFree(L->zq);
   delete L;
   return BITSTACK_OK;
 }
@@ -332,7 +400,7 @@ bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int3
     const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 65536);
     bs::repack_signs_kernel<<<blocks, threads, 0, st>>>(
         st_signs, reinterpret_cast<uint32_t*>(L->signs) + (int64_t)first_block * words_per_block, count,
-        cbytes, L->d_in, L->nq, L->rows_pad, L->rows_local, L->row_begin);
+        cbytes, L->d_in, L->nq, L->rows_pad, L->rows_local, L->row_begin, L->layout);
     count_launch();
     CK(cudaGetLastError());
     const int64_t fsd = L->dev_fdt ? 2 : 4;
@@ -403,10 +471,12 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
   const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype);
-  const bool tc_ok = L->k <= 16;  // k < 16: zero-padded columns of U', V'
+  // tcgen05 path: k <= 16 (zero-padded columns of U', V'), x rows bulk-copied by the
+  // TMA engine -> 16-byte aligned x and d_in % 8 == 0.
+  const bool tc_ok = L->k <= 16 && L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
   const bool use_tc = L->kernel == BITSTACK_KERNEL_TC || (L->kernel == BITSTACK_KERNEL_AUTO && tc_ok);
   if (L->kernel == BITSTACK_KERNEL_TC && !tc_ok)
-    return fail(BITSTACK_E_UNSUPPORTED, "tcgen05 decode kernel needs k <= 16");
+    return fail(BITSTACK_E_UNSUPPORTED, "tcgen05 decode kernel needs k <= 16, d_in %% 8 == 0 and a 16-byte aligned x");
 
   if (!use_tc) {
     for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
@@ -418,7 +488,7 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
       bs::matmul_simt_kernel<<<grid, 128, 0, st>>>(
           L->signs, L->u, L->v, L->inv_s, reinterpret_cast<const uint8_t*>(x) + b0 * L->d_in * xsz,
           reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz, L->n_act, L->nq, L->rows_pad,
-          L->rows_local, L->d_in, L->d_in_pad, L->dev_fdt, xdt, ydt, L->d_in, L->rows_local);
+          L->rows_local, L->d_in, L->d_in_pad, L->dev_fdt, xdt, ydt, L->d_in, L->rows_local, L->layout);
       count_launch();
       CK(cudaGetLastError());
       ps = record_prof(st, false, &slot);
@@ -427,13 +497,13 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
     return BITSTACK_OK;
   }
 
-  const int ndig = L->fdt == BITSTACK_F32 ? 2 : 1;
-  const int nbmax = 16 / ndig;
+  const bool f8 = L->layout == 1;          // e4m3 kernel (bf16/f16 factors); fp16 kernel for fp32 factors
+  const int nbmax = f8 ? 4 : 8;
   for (int64_t b0 = 0; b0 < batch; b0 += nbmax) {
     const int bc = (int)std::min<int64_t>(nbmax, batch - b0);
     int nb = 1;
     while (nb < bc) nb <<= 1;
-    const int R = r_tiles_for(nb, ndig);
+    const int R = f8 ? (nb == 1 ? F8Geom<1>::R : F8Geom<2>::R) : r_tiles_for(nb, 2);
     const int n_groups = (L->row_tiles + R - 1) / R;
     const int64_t units = (int64_t)L->n_act * L->nq;
     int cpg = std::max(1, L->sm_count / n_groups);
@@ -465,11 +535,19 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
     prm.one2 = 0x3C003C00u;
     prm.dbg_acc = g_dbg_acc;
     prm.dbg_z = g_dbg_z;
+    prm.zq = nullptr;
+    prm.status = nullptr;
     int slot = -1;
     bitstack_status ps = record_prof(st, true, &slot);
     if (ps) return ps;
     const int grid = n_groups * cpg;
-    bitstack_status rs = ndig == 1 ? dispatch_decode<1>(nb, prm, grid, st) : dispatch_decode<2>(nb, prm, grid, st);
+    bitstack_status rs;
+    if (f8) {
+      rs = nb == 1 ? launch_decode_f8<1>(L, prm, grid, st)
+                   : (nb == 2 ? launch_decode_f8<2>(L, prm, grid, st) : launch_decode_f8<4>(L, prm, grid, st));
+    } else {
+      rs = dispatch_decode<2>(nb, prm, grid, st);
+    }
     if (rs) return rs;
     ps = record_prof(st, false, &slot);
     if (ps) return ps;
@@ -487,7 +565,7 @@ bitstack_status bitstack_reconstruct(bitstack_layer L, void* w, bitstack_dtype w
   dim3 grid((unsigned)((L->d_in + 31) / 32), (unsigned)((L->rows_local + 7) / 8));
   bs::reconstruct_kernel<<<grid, 256, 0, st>>>(L->signs, L->u, L->v, L->inv_s, w, L->n_act, L->nq,
                                                 L->rows_pad, L->rows_local, L->d_in, L->d_in_pad,
-                                                L->dev_fdt, wdt);
+                                                L->dev_fdt, wdt, L->layout);
   count_launch();
   CK(cudaGetLastError());
   return BITSTACK_OK;

@@ -1,0 +1,492 @@
+// tcgen05 decode kernel, e4m3 variant: the production decode path for bf16/f16 factors.
+//
+// Same computation as decode_tc.cuh (Eq.4, Eq.7, Eq.8; y = sum_i sum_r U'_i[:,r] *
+// (S_i (V'_i[:,r] * x/s))), mapped differently onto the tensor core because a
+// tcgen05.mma costs ~19 cycles minimum per instruction (scripts/mma_issue_bench.cu):
+// with kind::f16 and N = 16 (rank k at batch 1) that caps the kernel at 128x16 sign
+// elements per 19 cycles.  kind::f8f6f4 has K = 32 per instruction:
+//   * A = S as e4m3 +-2^delta (1 byte per sign, half the tcgen05.st traffic and half the
+//     expansion ALU work of fp16: 8 LOP3 + 7 IMAD per 32 signs),
+//   * B = Z as THREE e4m3 digits (N = 48 per batch column): Z 2^E ~= d0 + d1 + d2 with
+//     d_t = e4m3(residual_t), ~12 significant bits (precision study: 6.4e-5 rel-L2 vs
+//     2.6e-4 for one fp16 digit),
+//   * 24.9 cycles per MMA (N = 48) -> 164 sign elements / clk / SM at the tensor floor.
+// Two kernels:
+//   zq_kernel<NB>      once per call: for every (block i, 128-column subchunk q) unit,
+//                      Z = V'_i (.) x/s, its max, a per-unit exponent e_u putting max|Z 2^e_u|
+//                      in (224, 448], and the three round-to-nearest e4m3 digits, written
+//                      as a ready-to-copy UMMA B tile (+16 B of metadata) -- built ONCE per
+//                      unit instead of once per row group;
+//   decode_f8_kernel<NB>  bulk-copies sign tiles + Zq tiles (TMA engine), expands signs to
+//                      e4m3 +-2^a_u in TMEM, a_u = E - e_u (E = the CTA's first unit's e_u),
+//                      so A*B = +-Z 2^E for every unit; the epilogue multiplies by 2^-E.
+// The decode kernel is launched with programmatic dependent launch: its setup and first
+// sign loads overlap the Zq kernel; only the Zq copies wait (griddepcontrol.wait).
+#pragma once
+#include <cuda_fp8.h>
+
+#include "decode_tc.cuh"
+
+namespace bs {
+
+// Device sign layout for this kernel ("F8 layout"): bit p of word w of a row's 128-column
+// subchunk holds column 32 w + 4 (p & 7) + (p >> 3), so that one LOP3 + one IMAD turn
+// bits (t, t+8, t+16, t+24) into the 4 bytes of TMEM column 8 w + t (K elements 4t..4t+3).
+__device__ __forceinline__ void expand_e4m3(uint32_t w, uint32_t e8, uint32_t* o /*8*/) {
+#pragma unroll
+  for (int t = 0; t < 7; ++t) o[t] = mad_lo(lop3_andnot(w, 0x01010101u << t), 1u << (7 - t), e8);
+  o[7] = lop3_andnot_or(w, 0x80808080u, e8);
+}
+
+// Round-to-nearest to 4 significant bits (the e4m3 significand) by Veltkamp splitting,
+// in plain fp32 arithmetic (no FMA contraction): exact for |z| < 2^100.
+__device__ __forceinline__ float rn4(float z) {
+  const float t = __fmul_rn(z, 1048577.0f);  // 2^20 + 1
+  return __fsub_rn(t, __fsub_rn(t, z));
+}
+
+
+
+constexpr int kF8ExpWarps = 16;          // 4 warpgroups of expanders (TMEM lane quadrant = warp % 4)
+constexpr int kF8WarpProducer = kF8ExpWarps, kF8WarpMma = kF8ExpWarps + 1;
+constexpr int kF8Threads = 32 * (kF8ExpWarps + 2);
+constexpr int kZqSentinel = 127;         // e_u of an all-zero unit
+
+// Zq unit geometry (depends on the batch width only).
+template <int NB>
+struct ZqCfg {
+  static constexpr int N = 48 * NB;                          // 3 digits x 16 ranks x batch
+  static constexpr int kZBytes = kSubK * N;                  // e4m3 B tile of one unit
+  static constexpr int kZUnit = kZBytes + 16;                // + metadata (int32 e_u)
+};
+
+// R row tiles per CTA group.  TMEM (512 columns) = accumulators R x N + NBUF unit
+// buffers of R x 32 columns (the e4m3 A operand of all R tiles of one unit).  One
+// handshake per unit: both warpgroups arrive on the same barrier, the MMA warp waits
+// once and commits once -- barrier/fence latency (~100+ cycles per wait even when the
+// phase is already complete) is paid per unit, not per tile.
+template <int NB, int R_>
+struct DecodeF8Cfg {
+  static constexpr int N = ZqCfg<NB>::N;
+  static constexpr int R = R_;
+  static constexpr int kZBytes = ZqCfg<NB>::kZBytes;
+  static constexpr int kZUnit = ZqCfg<NB>::kZUnit;
+  static constexpr int kSignBytes = R * kTileRows * 16;
+  static constexpr int kOffZ = kSignBytes;
+  static constexpr int kOffMeta = kOffZ + kZBytes;
+  static constexpr int kStageBytes = (kOffZ + kZUnit + 127) / 128 * 128;
+  static constexpr int S0 = (200 * 1024) / kStageBytes;
+  static constexpr int STAGES = S0 > 12 ? 12 : (S0 < 2 ? 2 : S0);
+  static constexpr int kBarBytes = 1024;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes;
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr int kACols = 32;                          // 128 rows x 128 e4m3 per tile
+  static constexpr int kBufCols = R * kACols;                // one unit's A operand
+  static constexpr int NB0 = (512 - R * N) / kBufCols;
+  static constexpr int NBUF = NB0 > 4 ? 4 : NB0;
+  static constexpr uint32_t kAccCol = NBUF * kBufCols;
+  static constexpr uint32_t LBO = (N / 8) * 128;
+  static constexpr uint32_t SBO = 128;
+  static_assert(N <= 256 && N % 16 == 0, "invalid MMA N");
+  static_assert(NBUF >= 2, "need at least double-buffered A");
+  static_assert(kAccCol + R * N <= kTmemCols, "TMEM overflow");
+  static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
+  static_assert(R % (kF8ExpWarps / 4) == 0 || R < kF8ExpWarps / 4, "warpgroups split the R tiles");
+};
+
+struct ZqParams {
+  const void* v;        // [n_cap][d_in_pad][16] V' (bf16 or f32)
+  const float* inv_s;   // [d_in_pad]
+  const void* x;        // [batch][x_stride]
+  uint8_t* zq;          // [n][nq] units of kZUnit bytes
+  long long x_stride;
+  int nq, d_in, d_in_pad, batch, x_dtype, f_dtype;
+};
+
+// One CTA per unit (block i, subchunk q); thread c = column q*128 + c.
+template <int NB>
+__global__ void __launch_bounds__(128) zq_kernel(const ZqParams p) {
+  using C = ZqCfg<NB>;
+  constexpr int N = C::N;
+  __shared__ __align__(16) uint8_t tile[C::kZBytes];
+  __shared__ float red[4];
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int unit = blockIdx.x;
+  const int i = unit / p.nq, q = unit % p.nq;
+  const int c = threadIdx.x;
+  const int col = q * kSubK + c;
+  float vv[16];
+  {
+    const long long base = ((long long)i * p.d_in_pad + col) * 16;
+    if (p.f_dtype == 1) {
+      const uint4* vp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.v) + base);
+      const uint4 a = __ldg(vp), b = __ldg(vp + 1);
+      const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f0 = __bfloat1622float2(h0[e]), f1 = __bfloat1622float2(h1[e]);
+        vv[2 * e] = f0.x; vv[2 * e + 1] = f0.y; vv[8 + 2 * e] = f1.x; vv[8 + 2 * e + 1] = f1.y;
+      }
+    } else {
+      const float4* vp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.v) + base);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 f = __ldg(vp + e);
+        vv[4 * e] = f.x; vv[4 * e + 1] = f.y; vv[4 * e + 2] = f.z; vv[4 * e + 3] = f.w;
+      }
+    }
+  }
+  const float is = col < p.d_in ? __ldg(p.inv_s + col) : 0.f;
+  float z[NB][16];
+  float m = 0.f;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const float xs = (b < p.batch && col < p.d_in) ? load_act(p.x, (long long)b * p.x_stride + col, p.x_dtype) * is : 0.f;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      z[b][r] = vv[r] * xs;
+      m = fmaxf(m, fabsf(z[b][r]));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((c & 31) == 0) red[c >> 5] = m;
+  __syncthreads();
+  m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  int e_u = kZqSentinel;
+  if (m > 0.f && isfinite(m)) {
+    e_u = (int)floorf(log2f(448.0f / m));
+    if (__fmul_rn(m, exp2f((float)e_u)) > 448.0f) e_u -= 1;   // guard log2 rounding
+    e_u = e_u > 100 ? 100 : (e_u < -100 ? -100 : e_u);
+  }
+  const float sc = e_u == kZqSentinel ? 0.f : exp2f((float)e_u);
+  const int kg = c >> 4, kk = c & 15;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const float zz = __fmul_rn(z[b][r], sc);
+      const float d0 = rn4(zz);
+      const float r1 = __fsub_rn(zz, d0);
+      const float d1 = rn4(r1);
+      const float d2 = __fsub_rn(r1, d1);
+      const float dg[3] = {d0, d1, d2};
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int n = (b * 3 + d) * 16 + r;
+        const __nv_fp8_storage_t byte = __nv_cvt_float_to_fp8(dg[d], __NV_SATFINITE, __NV_E4M3);
+        tile[(kg * (N / 8) + n / 8) * 128 + (n % 8) * 16 + kk] = byte;
+      }
+    }
+  }
+  __syncthreads();
+  uint8_t* dst = p.zq + (long long)unit * C::kZUnit;
+  for (int e = c; e < C::kZBytes / 16; e += 128)
+    reinterpret_cast<uint4*>(dst)[e] = reinterpret_cast<const uint4*>(tile)[e];
+  if (c == 0) reinterpret_cast<int4*>(dst + C::kZBytes)[0] = make_int4(e_u, 0, 0, 0);
+}
+
+template <int NB, int R_>
+__global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodeParams p) {
+  using C = DecodeF8Cfg<NB, R_>;
+  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NBUF = C::NBUF;
+  extern __shared__ __align__(1024) uint8_t smem[];
+
+  uint8_t* bar_area = smem + STAGES * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(bar_area);
+  uint64_t* empty = full + STAGES;
+  uint64_t* a_full = empty + STAGES;      // [NBUF] unit buffers
+  uint64_t* a_empty = a_full + NBUF;
+  uint64_t* acc_full = a_empty + NBUF;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int g = blockIdx.x / p.ctas_per_group;
+  const int jc = blockIdx.x % p.ctas_per_group;
+  const long long L = (long long)p.n * p.nq;
+  const long long u0 = L * jc / p.ctas_per_group;
+  const long long u1 = L * (jc + 1) / p.ctas_per_group;
+  const int nunits = (int)(u1 - u0);
+  const int i_start = (int)(u0 / p.nq), q_start = (int)(u0 % p.nq);
+  const int tiles_left = p.row_tiles - g * R;
+  const int Rg = tiles_left < R ? tiles_left : R;
+  const int row0 = g * R * kTileRows;
+  // test hook: CTA 0 timeline (clock64 relative to kernel entry), 8 slots per unit
+  long long* trace = (p.dbg_acc && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
+  const long long tstart = clock64();
+#define BS_TRACE(k_unit, k) do { if (trace && lane == 0) trace[(k_unit) * 8 + (k)] = clock64() - tstart; } while (0)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kF8ExpWarps + 1);
+    }
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(&a_full[b], kF8ExpWarps);
+      mbar_init(&a_empty[b], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kF8ExpWarps);
+    fence_mbar_init();
+  }
+  if (warp == kF8WarpProducer) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+
+  if (warp == kF8WarpProducer) {
+    // ================= producer: sign tiles now, Zq tiles once the Zq kernel is done =================
+    if (lane == 0) {
+      const uint64_t pol_sign = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      const uint32_t sign_bytes = (uint32_t)Rg * kTileRows * 16;
+      const int pre = nunits < STAGES ? nunits : STAGES;
+      int i = i_start, q = q_start;
+      for (int k = 0; k < pre; ++k) {  // first `pre` stages: sign tiles before the dependency wait
+        mbar_arrive_expect_tx(&full[k], sign_bytes + C::kZUnit);
+        bulk_g2s(smem + k * C::kStageBytes, p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0, sign_bytes,
+                 &full[k], pol_sign);
+        if (++q == p.nq) { q = 0; ++i; }
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // Zq of this call is complete and visible
+      for (int k = 0; k < pre; ++k) {
+        bulk_g2s(smem + k * C::kStageBytes + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, C::kZUnit, &full[k], pol_keep);
+        BS_TRACE(k, 0);
+      }
+      int s = pre % STAGES;
+      uint32_t ph = pre == STAGES ? 1u : 0u;
+      for (int k = pre; k < nunits; ++k) {
+        mbar_wait(&empty[s], ph ^ 1);
+        BS_TRACE(k, 0);
+        uint8_t* st = smem + s * C::kStageBytes;
+        mbar_arrive_expect_tx(&full[s], sign_bytes + C::kZUnit);
+        bulk_g2s(st, p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0, sign_bytes, &full[s], pol_sign);
+        bulk_g2s(st + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, C::kZUnit, &full[s], pol_keep);
+        if (++q == p.nq) { q = 0; ++i; }
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == kF8WarpMma) {
+    // ================= MMA issuer (converged warp, elected lane issues) =================
+    // No wait on full[s]: the expanders waited on it before arriving on a_full.
+    constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
+    int s = 0, q = q_start, ab = 0;
+    uint32_t aph = 0, acc_ph = 0;
+    bool have_piece = false;
+    for (int k = 0; k < nunits; ++k) {
+      const bool first = (k == 0) || (q == 0);
+      const bool last = (k == nunits - 1) || (q == p.nq - 1);
+      if (first && have_piece) {
+        mbar_wait(acc_empty, acc_ph);
+        acc_ph ^= 1;
+      }
+      mbar_wait(&a_full[ab], aph);
+      tc_fence_after();
+      BS_TRACE(k, 4);
+      const uint64_t bdesc0 = smem_desc_kmajor(smem_u32(smem + s * C::kStageBytes + C::kOffZ), C::LBO, C::SBO);
+      const uint32_t acc0 = first ? 0u : 1u;
+      const uint32_t abase = tbase + (uint32_t)(C::kBufCols * ab);
+      if (elect_one()) {
+        for (int t = 0; t < Rg; ++t) {
+          const uint32_t d0 = tbase + C::kAccCol + (uint32_t)(t * N);
+          const uint32_t a0 = abase + C::kACols * t;
+#pragma unroll
+          for (int m = 0; m < kSubK / 32; ++m)
+            mma_f8_ts(d0, a0 + 8 * m, bdesc0 + (uint64_t)((m * 2 * C::LBO) >> 4), idesc, m > 0 ? 1u : acc0);
+        }
+        mma_commit(&a_empty[ab]);
+        mma_commit(&empty[s]);
+        if (last) mma_commit(acc_full);
+      }
+      __syncwarp();
+      BS_TRACE(k, 5);
+      if (last) have_piece = true;
+      if (++ab == NBUF) { ab = 0; aph ^= 1; }
+      if (++s == STAGES) { s = 0; }
+      if (++q == p.nq) q = 0;
+    }
+  } else if (warp < kF8ExpWarps) {
+    // ================= expanders + epilogue (4 warpgroups; warpgroup wg owns tiles wg, wg+NWG, ...) =================
+    constexpr int NWG = kF8ExpWarps / 4;
+    const int wg = warp >> 2;
+    const int qd = warp & 3;
+    const int row_in_tile = qd * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
+    constexpr int kMyTiles = (R + NWG - 1) / NWG;
+    float yacc[kMyTiles][NB];
+#pragma unroll
+    for (int a = 0; a < kMyTiles; ++a)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) yacc[a][b] = 0.f;
+    int s = 0, ab = 0, i = i_start, q = q_start;
+    uint32_t ph = 0, aph = 0, acc_ph = 0;
+    int E = 0;
+    bool have_e = false;
+    for (int k = 0; k < nunits; ++k) {
+      const bool last = (k == nunits - 1) || (q == p.nq - 1);
+      mbar_wait(&full[s], ph);
+      if (warp == 0) BS_TRACE(k, 1);
+      const uint8_t* st = smem + s * C::kStageBytes;
+      // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit
+      const int e_u = *reinterpret_cast<const int*>(st + C::kOffMeta);
+      int a_exp = 0;
+      if (e_u != kZqSentinel) {
+        if (!have_e) { E = e_u; have_e = true; }
+        a_exp = E - e_u;
+        if (a_exp < -6 || a_exp > 8) {  // |x/s| range across this CTA's units beyond e4m3 A range
+          if (lane == 0 && p.status) atomicOr(p.status, 1);
+          a_exp = a_exp < -6 ? -6 : 8;
+        }
+      }
+      const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
+      const uint4* sg = reinterpret_cast<const uint4*>(st);
+      uint4 sw[kMyTiles];
+#pragma unroll
+      for (int a = 0; a < kMyTiles; ++a) {
+        const int t = wg + NWG * a;
+        if (t < Rg) sw[a] = sg[t * kTileRows + row_in_tile];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // signs are in registers; the MMA commit covers Zq
+      mbar_wait(&a_empty[ab], aph ^ 1);
+      tc_fence_after();
+      if (warp == 0) BS_TRACE(k, 2);
+      const uint32_t buf = tbase + lane_base + (uint32_t)(C::kBufCols * ab);
+#pragma unroll
+      for (int a = 0; a < kMyTiles; ++a) {
+        const int t = wg + NWG * a;
+        if (t < Rg) {
+          uint32_t o[32];
+          expand_e4m3(sw[a].x, e8, o);
+          expand_e4m3(sw[a].y, e8, o + 8);
+          expand_e4m3(sw[a].z, e8, o + 16);
+          expand_e4m3(sw[a].w, e8, o + 24);
+          tmem_st32(buf + C::kACols * t, o);
+        }
+      }
+      if (warp == 0) BS_TRACE(k, 6);
+      tmem_st_wait();
+      if (warp == 0) BS_TRACE(k, 7);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[ab]);
+      if (warp == 0) BS_TRACE(k, 3);
+      if (++ab == NBUF) { ab = 0; aph ^= 1; }
+      if (++s == STAGES) { s = 0; ph ^= 1; }
+      const int ci = i;
+      if (++q == p.nq) { q = 0; ++i; }
+
+      if (last) {
+        float uu[kMyTiles][16];
+#pragma unroll
+        for (int a = 0; a < kMyTiles; ++a) {
+          const int t = wg + NWG * a;
+          if (t < Rg) {
+            const long long row = row0 + t * kTileRows + row_in_tile;
+            const long long base = ((long long)ci * p.rows_pad + row) * 16;
+            if (p.f_dtype == 1) {
+              const uint4* up = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.u) + base);
+              const uint4 r0v = __ldg(up), r1v = __ldg(up + 1);
+              const __nv_bfloat162* b0 = reinterpret_cast<const __nv_bfloat162*>(&r0v);
+              const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&r1v);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f0 = __bfloat1622float2(b0[e]);
+                const float2 f1 = __bfloat1622float2(b1[e]);
+                uu[a][2 * e] = f0.x; uu[a][2 * e + 1] = f0.y;
+                uu[a][8 + 2 * e] = f1.x; uu[a][8 + 2 * e + 1] = f1.y;
+              }
+            } else {
+              const float4* up = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.u) + base);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float4 f = __ldg(up + e);
+                uu[a][4 * e] = f.x; uu[a][4 * e + 1] = f.y; uu[a][4 * e + 2] = f.z; uu[a][4 * e + 3] = f.w;
+              }
+            }
+          }
+        }
+        mbar_wait(acc_full, acc_ph);
+        acc_ph ^= 1;
+        tc_fence_after();
+        const float esc = exp2f((float)-E);
+#pragma unroll
+        for (int a = 0; a < kMyTiles; ++a) {
+          const int t = wg + NWG * a;
+          if (t < Rg) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              float tsum[16];
+#pragma unroll
+              for (int d = 0; d < 3; ++d) {
+                uint32_t v[16];
+                tmem_ld16(tbase + lane_base + C::kAccCol + (uint32_t)(t * N + (b * 3 + d) * 16), v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int r = 0; r < 16; ++r) tsum[r] = (d == 0) ? __uint_as_float(v[r]) : tsum[r] + __uint_as_float(v[r]);
+              }
+              float acc = 0.f;
+#pragma unroll
+              for (int r = 0; r < 16; ++r) acc = fmaf(uu[a][r], tsum[r], acc);
+              yacc[a][b] = fmaf(acc, esc, yacc[a][b]);
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty);
+      }
+    }
+    if (u1 > u0) {
+#pragma unroll
+      for (int a = 0; a < kMyTiles; ++a) {
+        const int t = wg + NWG * a;
+        if (t < Rg) {
+          const int row = row0 + t * kTileRows + row_in_tile;
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+            if (b < p.batch) atomicAdd(p.y_acc + (long long)b * p.rows_pad + row, yacc[a][b]);
+        }
+      }
+    }
+  }
+
+  // ---- teardown + last-CTA-of-group finalisation
+  __threadfence();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kF8WarpProducer) tmem_dealloc<C::kTmemCols>(tbase);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(p.counters + g, 1);
+    *last_flag = (prev == p.ctas_per_group - 1);
+  }
+  __syncthreads();
+  if (*last_flag) {
+    __threadfence();
+    const int rows_in_group = Rg * kTileRows;
+    const int total = rows_in_group * p.batch;
+    for (int e = threadIdx.x; e < total; e += kF8Threads) {
+      const int b = e / rows_in_group;
+      const int row = row0 + e % rows_in_group;
+      float* src = p.y_acc + (long long)b * p.rows_pad + row;
+      const float val = __ldcg(src);
+      *src = 0.f;
+      if (row < p.rows_local) {
+        const long long o = (long long)b * p.y_stride + row;
+        if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = val;
+        else reinterpret_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(val);
+      }
+    }
+    if (threadIdx.x == 0) p.counters[g] = 0;
+  }
+}
+
+}  // namespace bs

@@ -60,8 +60,9 @@ def gpu_y(lay, x_np, x_dtype=torch.float32, y_dtype=torch.float32):
 
 
 # ------------------------------------------------------------------ P15: bit-exact unpack
+@pytest.mark.parametrize("factor_dtype", ["f32", "bf16"])   # device sign layouts F16 and F8
 @pytest.mark.parametrize("shape", [(256, 384), (300, 200), (128, 1000)])
-def test_sign_unpack_bit_exact(bs, shape):
+def test_sign_unpack_bit_exact(bs, shape, factor_dtype):
     """U_i[:,0] = 2^i, V_i[:,0] = 1, other columns 0, s = 1  =>  reconstruct in fp32
     gives sum_i 2^i S_i exactly; decoding it must give back every canonical bit."""
     d_out, d_in = shape
@@ -72,7 +73,9 @@ def test_sign_unpack_bit_exact(bs, shape):
     for i in range(n):
         u[i, :, 0] = 2.0 ** i
         v[i, :, 0] = 1.0
-    lay = bs.Layer(d_out, d_in, k=16, n_capacity=n, factor_dtype="f32")
+    lay = bs.Layer(d_out, d_in, k=16, n_capacity=n, factor_dtype=factor_dtype)
+    if factor_dtype == "bf16":
+        u, v = O.bf16_bits(u), O.bf16_bits(v)   # powers of two: exact in bf16
     lay.load_blocks(0, signs, u, v, np.ones(d_in, np.float32))
     w = lay.reconstruct(torch.float32).cpu().numpy().astype(np.int64)
     # decode: w = sum_i 2^i (2 b_i - 1) = 2 sum_i 2^i b_i - (2^n - 1)
@@ -103,7 +106,7 @@ def test_c1_parity_fp32(bs, kernel):
 
 
 # ------------------------------------------------------------------ ragged shapes, batches
-@pytest.mark.parametrize("shape", [(384, 640), (200, 300), (1100, 260)])
+@pytest.mark.parametrize("shape", [(384, 640), (200, 296), (1100, 264)])
 @pytest.mark.parametrize("kernel", ["tc", "simt"])
 def test_bf16_parity_ragged(bs, shape, kernel):
     d_out, d_in = shape
@@ -115,6 +118,20 @@ def test_bf16_parity_ragged(bs, shape, kernel):
         y, xr = gpu_y(lay, x)
         ref = oracle_y(blocks, s32, 5, xr)
         assert O.relative_l2(y, ref) <= 1e-3, (batch, O.relative_l2(y, ref))
+
+
+def test_unaligned_d_in_uses_simt(bs):
+    """d_in % 8 != 0: the TMA-fed tcgen05 path is refused (E_UNSUPPORTED when forced) and
+    AUTO runs the SIMT kernel -- still within tolerance."""
+    g, s32, blocks = compress_case(200, 300, 3, "bf16", 44)
+    lay = make_layer(bs, 200, 300, blocks, s32, "bf16")
+    x = make_x(2, g, 1)
+    y, xr = gpu_y(lay, x)
+    assert O.relative_l2(y, oracle_y(blocks, s32, 3, xr)) <= 1e-3
+    lay.set_kernel("tc")
+    with pytest.raises(bs.BitStackError) as e:
+        gpu_y(lay, x)
+    assert e.value.name == "E_UNSUPPORTED"
 
 
 @pytest.mark.parametrize("kernel", ["tc", "simt"])
