@@ -352,7 +352,7 @@ def main():
             "metric": "bitstack_matmul HBM GB/s (algorithmic bytes / time) [us/layer in ms_per_step]",
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": ksteps, "warmup": args.warmup,
             "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f16 MMA operands, fp32 accumulate",
+            "scaling": "strong", "vs_baseline": None, "dtype": "e4m3 MMA operands (S exact, Z as 3 e4m3 digits), fp32 accumulate",
             "data": "synthetic (stored-form random blocks + activations, synthetic/ recipe)",
             "config": {"workload": w["label"], "d_out": d_out, "d_in": d_in, "n": n, "k": k, "batch": batch,
                        "factor_dtype": "bf16", "x_dtype": "bf16", "y_dtype": "f32",

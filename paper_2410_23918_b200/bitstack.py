@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbitstack.so")
+LIB_PATH = os.environ.get("BITSTACK_LIB", os.path.join(HERE, "libbitstack.so"))
 
 F32, BF16, F16 = 0, 1, 2
 KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT = 0, 1, 2
@@ -54,11 +54,13 @@ class Info(ctypes.Structure):
 _lib: Optional[ctypes.CDLL] = None
 
 
-def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libbitstack.so (build it first with paper_2410_23918_b200.build)."""
+def load_library(path: Optional[str] = None) -> ctypes.CDLL:
+    """Load libbitstack.so (build it first with paper_2410_23918_b200.build); the
+    BITSTACK_LIB environment variable, read at first load, selects another build."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("BITSTACK_LIB", LIB_PATH)
     if not os.path.exists(path):
         raise FileNotFoundError(
             f"{path} not found: run `python -m paper_2410_23918_b200.build` (the CUDA "

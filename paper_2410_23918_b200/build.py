@@ -32,34 +32,37 @@ def _nvcc() -> str:
     return "nvcc"
 
 
-def _digest() -> str:
+def _digest(extra=()) -> str:
     """Content hash of every source + the flags (mtimes do not survive a repo snapshot)."""
-    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    h = hashlib.sha256(" ".join(NVCC_FLAGS + list(extra)).encode())
     for d in _deps():
         with open(d, "rb") as f:
             h.update(f.read())
     return h.hexdigest()
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB) or not os.path.exists(LIB + ".sha256"):
+def _stale(out: str, extra=()) -> bool:
+    if not os.path.exists(out) or not os.path.exists(out + ".sha256"):
         return True
-    with open(LIB + ".sha256") as f:
-        return f.read().strip() != _digest()
+    with open(out + ".sha256") as f:
+        return f.read().strip() != _digest(extra)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) -> str:
+    """Compile csrc/bitstack.cu into `out` (default: the in-tree libbitstack.so).
+    `extra` nvcc flags are for debug variants (e.g. -DBS_DECODE_TRACE) written elsewhere."""
+    extra = list(extra)
+    if not force and not _stale(out, extra):
+        return out
+    tmp = out + ".tmp"
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(tmp, LIB)
-    with open(LIB + ".sha256", "w") as f:
-        f.write(_digest())
-    return LIB
+    os.replace(tmp, out)
+    with open(out + ".sha256", "w") as f:
+        f.write(_digest(extra))
+    return out
 
 
 if __name__ == "__main__":

@@ -163,7 +163,7 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
   prm.status = L->status;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(bs::kF8Threads);
+  cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

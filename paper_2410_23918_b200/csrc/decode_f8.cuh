@@ -47,9 +47,6 @@ __device__ __forceinline__ float rn4(float z) {
 
 
 
-constexpr int kF8ExpWarps = 16;          // 4 warpgroups of expanders (TMEM lane quadrant = warp % 4)
-constexpr int kF8WarpProducer = kF8ExpWarps, kF8WarpMma = kF8ExpWarps + 1;
-constexpr int kF8Threads = 32 * (kF8ExpWarps + 2);
 constexpr int kZqSentinel = 127;         // e_u of an all-zero unit
 
 // Zq unit geometry (depends on the batch width only).
@@ -60,15 +57,20 @@ struct ZqCfg {
   static constexpr int kZUnit = kZBytes + 16;                // + metadata (int32 e_u)
 };
 
-// R row tiles per CTA group.  TMEM (512 columns) = accumulators R x N + NBUF unit
-// buffers of R x 32 columns (the e4m3 A operand of all R tiles of one unit).  One
-// handshake per unit: both warpgroups arrive on the same barrier, the MMA warp waits
-// once and commits once -- barrier/fence latency (~100+ cycles per wait even when the
-// phase is already complete) is paid per unit, not per tile.
+// Self-issuing warpgroups.  Warpgroup w (warps 4w..4w+3, TMEM lane
+// quadrant = warp % 4) owns row tile w of the CTA's R tiles: for every unit it expands
+// its 128x128 sign tile into an e4m3 A slot in TMEM, syncs its own 4 warps on a named
+// barrier, and one elected thread of the warpgroup issues the tile's 4 MMAs itself --
+// there is no cross-warp handshake with a separate MMA warp (whose round trip, ~300-500
+// cycles, dwarfed the 100 cycles of MMA work per tile).  Each warpgroup keeps a 2-slot A
+// ring released by its own tcgen05.commit, and its own accumulator (no cross-issuer
+// hazards).  TMEM: R x N accumulator columns + R x NSLOT x 32 A columns <= 512.
 template <int NB, int R_>
 struct DecodeF8Cfg {
   static constexpr int N = ZqCfg<NB>::N;
-  static constexpr int R = R_;
+  static constexpr int R = R_;                               // row tiles = warpgroups
+  static constexpr int kThreads = 32 * (4 * R + 1);          // + producer warp
+  static constexpr int kWarpProducer = 4 * R;
   static constexpr int kZBytes = ZqCfg<NB>::kZBytes;
   static constexpr int kZUnit = ZqCfg<NB>::kZUnit;
   static constexpr int kSignBytes = R * kTileRows * 16;
@@ -81,17 +83,16 @@ struct DecodeF8Cfg {
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr int kACols = 32;                          // 128 rows x 128 e4m3 per tile
-  static constexpr int kBufCols = R * kACols;                // one unit's A operand
-  static constexpr int NB0 = (512 - R * N) / kBufCols;
-  static constexpr int NBUF = NB0 > 4 ? 4 : NB0;
-  static constexpr uint32_t kAccCol = NBUF * kBufCols;
+  static constexpr int NS0 = (512 - R * N) / (R * kACols);
+  static constexpr int NSLOT = NS0 > 4 ? 4 : NS0;            // A slots per warpgroup
+  static constexpr uint32_t kAccCol = R * NSLOT * kACols;
   static constexpr uint32_t LBO = (N / 8) * 128;
   static constexpr uint32_t SBO = 128;
   static_assert(N <= 256 && N % 16 == 0, "invalid MMA N");
-  static_assert(NBUF >= 2, "need at least double-buffered A");
+  static_assert(NSLOT >= 2, "need at least double-buffered A");
   static_assert(kAccCol + R * N <= kTmemCols, "TMEM overflow");
   static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
-  static_assert(R % (kF8ExpWarps / 4) == 0 || R < kF8ExpWarps / 4, "warpgroups split the R tiles");
+  static_assert(R >= 1 && R <= 7, "named barriers 1..R");
 };
 
 struct ZqParams {
@@ -188,19 +189,17 @@ __global__ void __launch_bounds__(128) zq_kernel(const ZqParams p) {
 }
 
 template <int NB, int R_>
-__global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_kernel(const DecodeParams p) {
   using C = DecodeF8Cfg<NB, R_>;
-  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NBUF = C::NBUF;
+  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT;
   extern __shared__ __align__(1024) uint8_t smem[];
 
   uint8_t* bar_area = smem + STAGES * C::kStageBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(bar_area);
   uint64_t* empty = full + STAGES;
-  uint64_t* a_full = empty + STAGES;      // [NBUF] unit buffers
-  uint64_t* a_empty = a_full + NBUF;
-  uint64_t* acc_full = a_empty + NBUF;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* a_empty = empty + STAGES;     // [R warpgroups][NSLOT]
+  uint64_t* acc_full = a_empty + R * NSLOT; // [R]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + R);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -216,31 +215,32 @@ __global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodePa
   const int tiles_left = p.row_tiles - g * R;
   const int Rg = tiles_left < R ? tiles_left : R;
   const int row0 = g * R * kTileRows;
-  // test hook: CTA 0 timeline (clock64 relative to kernel entry), 8 slots per unit
+#ifdef BS_DECODE_TRACE
+  // debug build only (scripts/trace_f8.py): CTA 0 timeline of warpgroup 3, clock64 relative
+  // to kernel entry, 16 slots per unit, written to the bitstack_debug_set buffer
   long long* trace = (p.dbg_acc && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
   const long long tstart = clock64();
-#define BS_TRACE(k_unit, k) do { if (trace && lane == 0) trace[(k_unit) * 8 + (k)] = clock64() - tstart; } while (0)
+#define BS_TRACE(k_unit, k) do { if (warp == 12 && trace && lane == 0) trace[(k_unit) * 16 + (k)] = clock64() - tstart; } while (0)
+#else
+#define BS_TRACE(k_unit, k) do { } while (0)
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kF8ExpWarps + 1);
+      mbar_init(&empty[s], Rg);           // one tcgen05.commit per active warpgroup
     }
-    for (int b = 0; b < NBUF; ++b) {
-      mbar_init(&a_full[b], kF8ExpWarps);
-      mbar_init(&a_empty[b], 1);
-    }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, kF8ExpWarps);
+    for (int b = 0; b < R * NSLOT; ++b) mbar_init(&a_empty[b], 1);
+    for (int w = 0; w < R; ++w) mbar_init(&acc_full[w], 1);
     fence_mbar_init();
   }
-  if (warp == kF8WarpProducer) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == C::kWarpProducer) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
 
-  if (warp == kF8WarpProducer) {
+  if (warp == C::kWarpProducer) {
     // ================= producer: sign tiles now, Zq tiles once the Zq kernel is done =================
     if (lane == 0) {
       const uint64_t pol_sign = policy_evict_first();
@@ -257,13 +257,11 @@ __global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodePa
       asm volatile("griddepcontrol.wait;" ::: "memory");  // Zq of this call is complete and visible
       for (int k = 0; k < pre; ++k) {
         bulk_g2s(smem + k * C::kStageBytes + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, C::kZUnit, &full[k], pol_keep);
-        BS_TRACE(k, 0);
       }
       int s = pre % STAGES;
       uint32_t ph = pre == STAGES ? 1u : 0u;
       for (int k = pre; k < nunits; ++k) {
         mbar_wait(&empty[s], ph ^ 1);
-        BS_TRACE(k, 0);
         uint8_t* st = smem + s * C::kStageBytes;
         mbar_arrive_expect_tx(&full[s], sign_bytes + C::kZUnit);
         bulk_g2s(st, p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0, sign_bytes, &full[s], pol_sign);
@@ -272,66 +270,38 @@ __global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodePa
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp == kF8WarpMma) {
-    // ================= MMA issuer (converged warp, elected lane issues) =================
-    // No wait on full[s]: the expanders waited on it before arriving on a_full.
-    constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
-    int s = 0, q = q_start, ab = 0;
-    uint32_t aph = 0, acc_ph = 0;
-    bool have_piece = false;
-    for (int k = 0; k < nunits; ++k) {
-      const bool first = (k == 0) || (q == 0);
-      const bool last = (k == nunits - 1) || (q == p.nq - 1);
-      if (first && have_piece) {
-        mbar_wait(acc_empty, acc_ph);
-        acc_ph ^= 1;
-      }
-      mbar_wait(&a_full[ab], aph);
-      tc_fence_after();
-      BS_TRACE(k, 4);
-      const uint64_t bdesc0 = smem_desc_kmajor(smem_u32(smem + s * C::kStageBytes + C::kOffZ), C::LBO, C::SBO);
-      const uint32_t acc0 = first ? 0u : 1u;
-      const uint32_t abase = tbase + (uint32_t)(C::kBufCols * ab);
-      if (elect_one()) {
-        for (int t = 0; t < Rg; ++t) {
-          const uint32_t d0 = tbase + C::kAccCol + (uint32_t)(t * N);
-          const uint32_t a0 = abase + C::kACols * t;
-#pragma unroll
-          for (int m = 0; m < kSubK / 32; ++m)
-            mma_f8_ts(d0, a0 + 8 * m, bdesc0 + (uint64_t)((m * 2 * C::LBO) >> 4), idesc, m > 0 ? 1u : acc0);
-        }
-        mma_commit(&a_empty[ab]);
-        mma_commit(&empty[s]);
-        if (last) mma_commit(acc_full);
-      }
-      __syncwarp();
-      BS_TRACE(k, 5);
-      if (last) have_piece = true;
-      if (++ab == NBUF) { ab = 0; aph ^= 1; }
-      if (++s == STAGES) { s = 0; }
-      if (++q == p.nq) q = 0;
-    }
-  } else if (warp < kF8ExpWarps) {
-    // ================= expanders + epilogue (4 warpgroups; warpgroup wg owns tiles wg, wg+NWG, ...) =================
-    constexpr int NWG = kF8ExpWarps / 4;
+  } else {
+    // ================= warpgroup w: expand tile w, issue its MMAs, drain it =================
     const int wg = warp >> 2;
     const int qd = warp & 3;
+    const int t = wg;                      // this warpgroup's row tile
+    const bool active = t < Rg;
+    const bool issuer = qd == 0;           // warp 4w issues the warpgroup's MMAs
     const int row_in_tile = qd * 32 + lane;
     const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
-    constexpr int kMyTiles = (R + NWG - 1) / NWG;
-    float yacc[kMyTiles][NB];
+    constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
+    const uint32_t d_acc = tbase + C::kAccCol + (uint32_t)(t * N);
+    float yacc[NB];
 #pragma unroll
-    for (int a = 0; a < kMyTiles; ++a)
-#pragma unroll
-      for (int b = 0; b < NB; ++b) yacc[a][b] = 0.f;
-    int s = 0, ab = 0, i = i_start, q = q_start;
-    uint32_t ph = 0, aph = 0, acc_ph = 0;
+    for (int b = 0; b < NB; ++b) yacc[b] = 0.f;
+    int s = 0, slot = 0, i = i_start, q = q_start;
+    uint32_t ph = 0, sph = 0, acc_ph = 0;
     int E = 0;
     bool have_e = false;
-    for (int k = 0; k < nunits; ++k) {
+    for (int k = 0; active && k < nunits; ++k) {
+      const bool first = (k == 0) || (q == 0);
       const bool last = (k == nunits - 1) || (q == p.nq - 1);
-      mbar_wait(&full[s], ph);
-      if (warp == 0) BS_TRACE(k, 1);
+      // One warp per warpgroup polls the stage / slot mbarriers; the named barrier below
+      // releases the other three (4x fewer mbarrier waits through the SM's barrier unit).
+      if (qd == 0) {
+        BS_TRACE(k, 7);
+        mbar_wait(&full[s], ph);
+        BS_TRACE(k, 2);
+        mbar_wait(&a_empty[wg * NSLOT + slot], sph ^ 1);
+      }
+      BS_TRACE(k, 0);
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
+      BS_TRACE(k, 1);
       const uint8_t* st = smem + s * C::kStageBytes;
       // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit
       const int e_u = *reinterpret_cast<const int*>(st + C::kOffMeta);
@@ -345,115 +315,103 @@ __global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodePa
         }
       }
       const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
-      const uint4* sg = reinterpret_cast<const uint4*>(st);
-      uint4 sw[kMyTiles];
-#pragma unroll
-      for (int a = 0; a < kMyTiles; ++a) {
-        const int t = wg + NWG * a;
-        if (t < Rg) sw[a] = sg[t * kTileRows + row_in_tile];
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // signs are in registers; the MMA commit covers Zq
-      mbar_wait(&a_empty[ab], aph ^ 1);
+      const uint4 sw = reinterpret_cast<const uint4*>(st)[t * kTileRows + row_in_tile];
       tc_fence_after();
-      if (warp == 0) BS_TRACE(k, 2);
-      const uint32_t buf = tbase + lane_base + (uint32_t)(C::kBufCols * ab);
-#pragma unroll
-      for (int a = 0; a < kMyTiles; ++a) {
-        const int t = wg + NWG * a;
-        if (t < Rg) {
-          uint32_t o[32];
-          expand_e4m3(sw[a].x, e8, o);
-          expand_e4m3(sw[a].y, e8, o + 8);
-          expand_e4m3(sw[a].z, e8, o + 16);
-          expand_e4m3(sw[a].w, e8, o + 24);
-          tmem_st32(buf + C::kACols * t, o);
-        }
+      const uint32_t a_col = tbase + (uint32_t)(C::kACols * (wg * NSLOT + slot));
+      {
+        uint32_t o[32];
+        expand_e4m3(sw.x, e8, o);
+        expand_e4m3(sw.y, e8, o + 8);
+        expand_e4m3(sw.z, e8, o + 16);
+        expand_e4m3(sw.w, e8, o + 24);
+        tmem_st32(a_col + lane_base, o);
       }
-      if (warp == 0) BS_TRACE(k, 6);
+      BS_TRACE(k, 3);
       tmem_st_wait();
-      if (warp == 0) BS_TRACE(k, 7);
+      BS_TRACE(k, 4);
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a_full[ab]);
-      if (warp == 0) BS_TRACE(k, 3);
-      if (++ab == NBUF) { ab = 0; aph ^= 1; }
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");   // the warpgroup's 4 lane quadrants are in TMEM
+      BS_TRACE(k, 5);
+      if (issuer) {
+        tc_fence_after();
+        const uint64_t bdesc0 = smem_desc_kmajor(smem_u32(smem + s * C::kStageBytes + C::kOffZ), C::LBO, C::SBO);
+        if (elect_one()) {
+#pragma unroll
+          for (int m = 0; m < kSubK / 32; ++m) {
+            mma_f8_ts(d_acc, a_col + 8 * m, bdesc0 + (uint64_t)((m * 2 * C::LBO) >> 4), idesc,
+                      (m > 0 || !first) ? 1u : 0u);
+            BS_TRACE(k, 12 + m);
+          }
+          mma_commit(&a_empty[wg * NSLOT + slot]);
+          mma_commit(&empty[s]);
+          if (last) mma_commit(&acc_full[wg]);
+        }
+        __syncwarp();
+      }
+      BS_TRACE(k, 6);
+      if (++slot == NSLOT) { slot = 0; sph ^= 1; }
       if (++s == STAGES) { s = 0; ph ^= 1; }
       const int ci = i;
       if (++q == p.nq) { q = 0; ++i; }
 
       if (last) {
-        float uu[kMyTiles][16];
+        // ---- epilogue for block ci: y += 2^-E sum_r U'_ci[row, r] (T_d0 + T_d1 + T_d2)[row, r]
+        float uu[16];
+        {
+          const long long row = row0 + t * kTileRows + row_in_tile;
+          const long long base = ((long long)ci * p.rows_pad + row) * 16;
+          if (p.f_dtype == 1) {
+            const uint4* up = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.u) + base);
+            const uint4 r0v = __ldg(up), r1v = __ldg(up + 1);
+            const __nv_bfloat162* b0 = reinterpret_cast<const __nv_bfloat162*>(&r0v);
+            const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&r1v);
 #pragma unroll
-        for (int a = 0; a < kMyTiles; ++a) {
-          const int t = wg + NWG * a;
-          if (t < Rg) {
-            const long long row = row0 + t * kTileRows + row_in_tile;
-            const long long base = ((long long)ci * p.rows_pad + row) * 16;
-            if (p.f_dtype == 1) {
-              const uint4* up = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.u) + base);
-              const uint4 r0v = __ldg(up), r1v = __ldg(up + 1);
-              const __nv_bfloat162* b0 = reinterpret_cast<const __nv_bfloat162*>(&r0v);
-              const __nv_bfloat162* b1 = reinterpret_cast<const __nv_bfloat162*>(&r1v);
+            for (int e = 0; e < 4; ++e) {
+              const float2 f0 = __bfloat1622float2(b0[e]);
+              const float2 f1 = __bfloat1622float2(b1[e]);
+              uu[2 * e] = f0.x; uu[2 * e + 1] = f0.y;
+              uu[8 + 2 * e] = f1.x; uu[8 + 2 * e + 1] = f1.y;
+            }
+          } else {
+            const float4* up = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.u) + base);
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f0 = __bfloat1622float2(b0[e]);
-                const float2 f1 = __bfloat1622float2(b1[e]);
-                uu[a][2 * e] = f0.x; uu[a][2 * e + 1] = f0.y;
-                uu[a][8 + 2 * e] = f1.x; uu[a][8 + 2 * e + 1] = f1.y;
-              }
-            } else {
-              const float4* up = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.u) + base);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float4 f = __ldg(up + e);
-                uu[a][4 * e] = f.x; uu[a][4 * e + 1] = f.y; uu[a][4 * e + 2] = f.z; uu[a][4 * e + 3] = f.w;
-              }
+            for (int e = 0; e < 4; ++e) {
+              const float4 f = __ldg(up + e);
+              uu[4 * e] = f.x; uu[4 * e + 1] = f.y; uu[4 * e + 2] = f.z; uu[4 * e + 3] = f.w;
             }
           }
         }
-        mbar_wait(acc_full, acc_ph);
+        mbar_wait(&acc_full[wg], acc_ph);
         acc_ph ^= 1;
         tc_fence_after();
         const float esc = exp2f((float)-E);
 #pragma unroll
-        for (int a = 0; a < kMyTiles; ++a) {
-          const int t = wg + NWG * a;
-          if (t < Rg) {
+        for (int b = 0; b < NB; ++b) {
+          float tsum[16];
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              float tsum[16];
+          for (int d = 0; d < 3; ++d) {
+            uint32_t v[16];
+            tmem_ld16(d_acc + lane_base + (uint32_t)((b * 3 + d) * 16), v);
+            tmem_ld_wait();
 #pragma unroll
-              for (int d = 0; d < 3; ++d) {
-                uint32_t v[16];
-                tmem_ld16(tbase + lane_base + C::kAccCol + (uint32_t)(t * N + (b * 3 + d) * 16), v);
-                tmem_ld_wait();
-#pragma unroll
-                for (int r = 0; r < 16; ++r) tsum[r] = (d == 0) ? __uint_as_float(v[r]) : tsum[r] + __uint_as_float(v[r]);
-              }
-              float acc = 0.f;
-#pragma unroll
-              for (int r = 0; r < 16; ++r) acc = fmaf(uu[a][r], tsum[r], acc);
-              yacc[a][b] = fmaf(acc, esc, yacc[a][b]);
-            }
+            for (int r = 0; r < 16; ++r) tsum[r] = (d == 0) ? __uint_as_float(v[r]) : tsum[r] + __uint_as_float(v[r]);
           }
+          float acc = 0.f;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) acc = fmaf(uu[r], tsum[r], acc);
+          yacc[b] = fmaf(acc, esc, yacc[b]);
         }
+        // the next piece's first MMA (issued after this warpgroup's next bar.sync)
+        // overwrites the accumulator: order these tcgen05.ld before that barrier
         tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(acc_empty);
       }
     }
-    if (u1 > u0) {
+#undef BS_TRACE
+    if (active && nunits > 0) {
+      const int row = row0 + t * kTileRows + row_in_tile;
 #pragma unroll
-      for (int a = 0; a < kMyTiles; ++a) {
-        const int t = wg + NWG * a;
-        if (t < Rg) {
-          const int row = row0 + t * kTileRows + row_in_tile;
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-            if (b < p.batch) atomicAdd(p.y_acc + (long long)b * p.rows_pad + row, yacc[a][b]);
-        }
-      }
+      for (int b = 0; b < NB; ++b)
+        if (b < p.batch) atomicAdd(p.y_acc + (long long)b * p.rows_pad + row, yacc[b]);
     }
   }
 
@@ -462,7 +420,7 @@ __global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodePa
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == kF8WarpProducer) tmem_dealloc<C::kTmemCols>(tbase);
+  if (warp == C::kWarpProducer) tmem_dealloc<C::kTmemCols>(tbase);
   if (threadIdx.x == 0) {
     __threadfence();
     const int prev = atomicAdd(p.counters + g, 1);
@@ -473,7 +431,7 @@ __global__ void __launch_bounds__(kF8Threads, 1) decode_f8_kernel(const DecodePa
     __threadfence();
     const int rows_in_group = Rg * kTileRows;
     const int total = rows_in_group * p.batch;
-    for (int e = threadIdx.x; e < total; e += kF8Threads) {
+    for (int e = threadIdx.x; e < total; e += C::kThreads) {
       const int b = e / rows_in_group;
       const int row = row0 + e % rows_in_group;
       float* src = p.y_acc + (long long)b * p.rows_pad + row;

@@ -1,0 +1,98 @@
+"""Turn a round's ncu outputs (gpurun_out/) into the committed summaries under profiles/.
+
+usage: python scripts/make_profiles.py r01 [workload_key]
+  reads  gpurun_out/launches_<r>.csv   (ncu --metrics gpu__time_duration.sum launch list of bench.py)
+         gpurun_out/decode_<r>.ncu-rep (ncu --set full of zq_kernel + decode_f8_kernel)
+  writes profiles/<r>_launches.txt, profiles/<r>_ncu_full.txt, profiles/traffic.json[workload_key]
+"""
+import csv
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+from collections import OrderedDict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = [
+    "gpu__time_duration.sum", "sm__cycles_elapsed.avg", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum", "launch__registers_per_thread",
+    "launch__grid_size", "launch__block_size", "smsp__inst_executed.sum",
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    i = next(k for k, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[i]
+    agg = OrderedDict()
+    for r in rows[i + 1:]:
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = re.sub(r"\(.*", "", d["Kernel Name"])
+        unit = d["Metric Unit"]
+        v = float(d["Metric Value"]) * {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(unit, 1.0)
+        agg.setdefault(name, []).append(v)
+    return agg
+
+
+def full(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    hdr, units = r[0], r[1]
+    res = []
+    for row in r[2:]:
+        d = dict(zip(hdr, row))
+        u = dict(zip(hdr, units))
+        res.append((re.sub(r"\(.*", "", d["Kernel Name"]), {k: (d.get(k), u.get(k)) for k in KEYS if k in d}))
+    return res
+
+
+def to_bytes(v, unit):
+    return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+def main(r, key="c2_n16_b1_g1"):
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    lp = os.path.join(ROOT, "gpurun_out", f"launches_{r}.csv")
+    lines = [f"# ncu launch list of `python bench.py --steps 40 --warmup 5 --no-cpu-baseline --no-graph`",
+             "# (--metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised: PDL overlap",
+             "#  of zq_kernel with decode_f8_kernel is lost under ncu, so compare SHARES, not absolutes)",
+             f"{'kernel':60s} {'launches':>8s} {'avg_us':>10s} {'total_us':>11s} {'share':>7s}"]
+    agg = launches(lp)
+    tot = sum(sum(v) for v in agg.values())
+    steady = {k: v for k, v in agg.items() if "repack" not in k and "prep_factors" not in k and "inv_s" not in k}
+    tot_steady = sum(sum(v) for v in steady.values())
+    for k, v in agg.items():
+        lines.append(f"{k:60s} {len(v):8d} {sum(v) / len(v):10.2f} {sum(v):11.1f} {sum(v) / tot:7.3f}")
+    lines.append("# per-call share (excluding one-off load_blocks kernels: repack/prep/inv_s):")
+    for k, v in steady.items():
+        lines.append(f"#   {k:56s} {sum(v) / tot_steady:6.3f}")
+    open(os.path.join(ROOT, "profiles", f"{r}_launches.txt"), "w").write("\n".join(lines) + "\n")
+
+    rep = os.path.join(ROOT, "gpurun_out", f"decode_{r}.ncu-rep")
+    out = [f"# ncu --set full --clock-control none --import-source on, one launch of each kernel of the",
+           "# decode pair (C2 4096x4096, n=16, k=16, bf16 factors, B=1), from gpurun_out/decode_" + r + ".ncu-rep"]
+    traffic = 0.0
+    for name, m in full(rep):
+        out.append(name)
+        for k, (v, u) in m.items():
+            out.append(f"    {k:66s} {v} {u or ''}")
+        traffic += to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
+    out.append(f"# pair DRAM traffic per call: {traffic:.0f} bytes")
+    open(os.path.join(ROOT, "profiles", f"{r}_ncu_full.txt"), "w").write("\n".join(out) + "\n")
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    tj = json.load(open(tp)) if os.path.exists(tp) else {}
+    tj[key] = traffic
+    tj["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per call of the zq_kernel + decode_f8_kernel "
+                   "pair from one ncu --set full capture; keys <workload>_n<n>_b<batch>_g<world>")
+    json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
+    print("\n".join(lines + out))
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
