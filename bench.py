@@ -31,19 +31,41 @@ from synthetic import CONFIGS, channel_gains, make_random_blocks, make_x, seed_f
 
 L2_BYTES = 126 * 2 ** 20
 WORKLOADS = {
-    "c2": dict(CONFIGS["c2"], label="c2: Llama-3.1-8B q_proj 4096x4096, n=16 blocks, k=16, bf16 factors, decode"),
-    "c5": dict(CONFIGS["c5"], label="c5: Llama-3.1-70B down_proj 8192x28672, n=12 blocks, k=16, bf16 factors, decode"),
+    "c2": dict(CONFIGS["c2"], kind="decode",
+               label="c2: Llama-3.1-8B q_proj 4096x4096, n=16 blocks, k=16, bf16 factors, decode"),
+    "c5": dict(CONFIGS["c5"], kind="decode",
+               label="c5: Llama-3.1-70B down_proj 8192x28672, n=12 blocks, k=16, bf16 factors, decode"),
+    "c3_up": dict(CONFIGS["c3_up"], kind="prefill",
+                  label="c3: Llama-3.1-8B up/gate_proj 14336x4096, n=8 blocks, k=16, bf16 factors, prefill 2048 tokens"),
+    "c3_down": dict(CONFIGS["c3_down"], kind="prefill",
+                    label="c3: Llama-3.1-8B down_proj 4096x14336, n=8 blocks, k=16, bf16 factors, prefill 2048 tokens"),
 }
 
 
-def peaks():
+def peaks(kind="decode"):
+    """Roofline denominator: HBM copy GB/s (decode), or dense bf16 TFLOP/s sustained (prefill
+    GEMM with fp16 operands: same tensor rate as bf16, nominal ratio 1)."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    key = "hbm_gbs" if kind == "decode" else "bf16_tflops_sustained"
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d[key]), f"measured (MEASURED_PEAKS.json {key})"
     except Exception:
-        return 6650.0, "fallback (B200_PROFILING.md)"
+        return (6650.0, "fallback (B200_PROFILING.md)") if kind == "decode" else \
+            (2250.0, "fallback (nominal dense fp16/bf16)")
+
+
+def alg_flops(w, rows, batch, n):
+    """SURVEY §8(d) prefill: 2 r d_in (B + n k) (restore the tile on tensor cores + GEMM)."""
+    return 2.0 * rows * w["d_in"] * (batch + n * w["k"])
+
+
+def step_units(w, rows, batch, n):
+    """The metric's numerator per step: GB (decode) or TFLOP (prefill)."""
+    if w["kind"] == "decode":
+        return alg_bytes_per_rank(w, rows, batch, n) / 1e9
+    return alg_flops(w, rows, batch, n) / 1e12
 
 
 def alg_bytes_per_rank(w, rows, batch, n, x_bytes=2, y_bytes=4):
@@ -130,7 +152,17 @@ def oracle_sample_time(w, n, batch, rows_sample, steps, warmup, seed):
     for _ in range(steps):
         O.matmul_dense(sub, s.astype(np.float64), n, x)
     dt = (time.perf_counter() - t0) / steps
-    return dt, alg_bytes_per_rank(w, rows_sample, batch, n)
+    return dt, step_units(w, rows_sample, batch, n)
+
+
+def metric_name(w):
+    if w["kind"] == "decode":
+        return "bitstack_matmul HBM GB/s (algorithmic bytes / time) [us/layer in ms_per_step]"
+    return "bitstack_matmul prefill TFLOP/s (algorithmic 2 r d_in (B + n k) / time) [us/layer in ms_per_step]"
+
+
+def unit_name(w):
+    return "GB/s" if w["kind"] == "decode" else "TFLOP/s"
 
 
 def main():
@@ -163,17 +195,16 @@ def main():
         t16, _ = oracle_sample_time(w, n, batch, 16, 1, 0, seed_for(2, 0, "blocks"))
         rows = int(max(16, min(w["d_out"], 16 * budget_s / max(t16, 1e-6) / (args.steps + args.warmup))))
         dt, by = oracle_sample_time(w, n, batch, rows, args.steps, args.warmup, seed_for(2, 0, "blocks"))
-        val = by / dt / 1e9
+        val = by / dt
         line = {
-            "impl": "reference", "metric": "bitstack_matmul HBM GB/s (algorithmic bytes / time)",
-            "value": val, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "impl": "reference", "metric": metric_name(w), "value": val, "unit": unit_name(w), "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (stored-form random blocks, synthetic/ recipe)",
             "config": {"workload": w["label"], "d_out": w["d_out"], "d_in": w["d_in"], "n": n, "k": w["k"],
                        "batch": batch, "parallelism": "cpu", "sample_rows": rows},
-            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": unit_name(w), "cores": cpu_cores(), "kind": "oracle",
                              "sample": f"dense oracle (fp64 numpy) for {rows} of {w['d_out']} output rows, all {n} blocks"},
-            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "e2e": {"value": val, "unit": unit_name(w), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }
         print(json.dumps(line))
         return
@@ -250,7 +281,7 @@ def main():
         if world > 1:
             dist.barrier()
         ms = e0.elapsed_time(e1)
-        launches = pkg.launch_count() - l0 if graph is None else nsteps
+        launches = pkg.launch_count() - l0 if graph is None else nsteps * per_step_launches
         if world > 1:
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -260,6 +291,10 @@ def main():
     use_graph = (not args.no_graph) and world == 1
     for i in range(args.warmup):
         step(i)
+    torch.cuda.synchronize()
+    l0 = pkg.launch_count()
+    step(0)
+    per_step_launches = pkg.launch_count() - l0   # our kernels per bitstack_matmul call
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local_rank)
@@ -274,15 +309,21 @@ def main():
         nk, kms = pkg.profile_end()
     clocks = sampler.summary()
     ms_step = ms / ksteps
-    total_bytes = alg_bytes_per_rank(w, rows, batch, n)  # this rank
+    total_units = step_units(w, rows, batch, n)  # this rank
     if world > 1:
-        tb = torch.tensor([total_bytes], dtype=torch.float64, device="cuda")
+        tb = torch.tensor([total_units], dtype=torch.float64, device="cuda")
         dist.all_reduce(tb)
-        total_bytes = float(tb.item())
-    value = total_bytes / (ms_step * 1e-3) / 1e9
+        total_units = float(tb.item())
+    value = total_units / (ms_step * 1e-3)
     kernel_ms = kms / max(nk, 1)
-    achieved = alg_bytes_per_rank(w, rows, batch, n) / (kernel_ms * 1e-3) / 1e9
-    peak, peak_src = peaks()
+    if w["kind"] == "decode":   # dominant kernel: the zq + decode PDL pair, algorithmic bytes
+        dom_units = alg_bytes_per_rank(w, rows, batch, n) / 1e9
+        dom_name = "bs::zq_kernel<%d> + bs::decode_f8_kernel<%d> (PDL pair)" % (min(batch, 4), min(batch, 4))
+    else:                       # dominant kernel: the GEMM, 2 B r d_in flops
+        dom_units = 2.0 * batch * rows * d_in / 1e12
+        dom_name = "bs::prefill_gemm_kernel<256>"
+    achieved = dom_units / (kernel_ms * 1e-3)
+    peak, peak_src = peaks(w["kind"])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -317,12 +358,12 @@ def main():
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e = {"value": total_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+    e2e = {"value": total_units / (e2e_ms * 1e-3), "unit": unit_name(w), "ms_per_step": e2e_ms,
            "h2d_bytes_per_step": int(x_h.numel() * x_h.element_size()),
            "d2h_bytes_per_step": int(y_h.numel() * y_h.element_size())}
 
     sweep = None
-    if args.sweep and world == 1:
+    if args.sweep and world == 1 and w["kind"] == "decode":
         sweep = {}
         for nn in (1, 2, 4, 8, 16):
             if nn > w["n"]:
@@ -343,16 +384,17 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rows_s = 256
         dt, by = oracle_sample_time(w, n, batch, rows_s, 1, 0, seed_for(2, 0, "blocks"))
-        cpu = {"value": by / dt / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+        cpu = {"value": by / dt, "unit": unit_name(w), "cores": cpu_cores(), "kind": "oracle",
                "sample": f"dense oracle (fp64 numpy, Eq.8+Eq.4) for {rows_s} of {d_out} output rows, "
                          f"all {n} blocks, 1 call ({dt:.2f} s)"}
 
     if rank == 0:
         line = {
-            "metric": "bitstack_matmul HBM GB/s (algorithmic bytes / time) [us/layer in ms_per_step]",
-            "value": value, "unit": "GB/s", "n_gpus": world, "steps": ksteps, "warmup": args.warmup,
+            "metric": metric_name(w),
+            "value": value, "unit": unit_name(w), "n_gpus": world, "steps": ksteps, "warmup": args.warmup,
             "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "e4m3 MMA operands (S exact, Z as 3 e4m3 digits), fp32 accumulate",
+            "scaling": "strong", "vs_baseline": None, "dtype": ("e4m3 MMA operands (S exact, Z as 3 e4m3 digits), fp32 accumulate" if w["kind"] == "decode"
+                      else "bf16 restore MMA + fp16 GEMM operands, fp32 accumulate"),
             "data": "synthetic (stored-form random blocks + activations, synthetic/ recipe)",
             "config": {"workload": w["label"], "d_out": d_out, "d_in": d_in, "n": n, "k": k, "batch": batch,
                        "factor_dtype": "bf16", "x_dtype": "bf16", "y_dtype": "f32",
@@ -360,11 +402,13 @@ def main():
                        "l2": f"inputs larger than L2: rotation over {copies} layer copies "
                              f"({copies * per_layer / 2 ** 20:.0f} MiB/rank > 4x126 MiB)",
                        "timing": "CUDA-graph replay" if use_graph else "eager launches"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "hbm" if w["kind"] == "decode" else "tensor", "achieved": achieved,
+                         "peak": peak, "unit": unit_name(w),
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "bs::zq_kernel<1> + bs::decode_f8_kernel<1> (PDL pair)", "kernel_us": kernel_ms * 1e3,
+                         "kernel": dom_name, "kernel_us": kernel_ms * 1e3,
                          "kernel_launches_timed": nk,
-                         "bytes_per_launch": alg_bytes_per_rank(w, rows, batch, n)},
+                         ("bytes_per_launch" if w["kind"] == "decode" else "flops_per_launch"):
+                             dom_units * (1e9 if w["kind"] == "decode" else 1e12)},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(launches),

@@ -64,9 +64,13 @@ typedef enum {
 
 /* Kernel selection for bitstack_matmul (bitstack_set_kernel). */
 typedef enum {
-  BITSTACK_KERNEL_AUTO = 0,   /* tcgen05 decode kernel when supported, else SIMT */
+  BITSTACK_KERNEL_AUTO = 0,   /* batch >= 16 with bf16 factors: restored-tile GEMM (prefill) path;
+                                 otherwise the tcgen05 decode kernel when supported, else SIMT */
   BITSTACK_KERNEL_TC = 1,     /* force the tcgen05/TMEM decode kernel (E_UNSUPPORTED if not possible) */
-  BITSTACK_KERNEL_SIMT = 2    /* force the CUDA-core FP32 reference kernel (any shape) */
+  BITSTACK_KERNEL_SIMT = 2,   /* force the CUDA-core FP32 reference kernel (any shape) */
+  BITSTACK_KERNEL_PREFILL = 3 /* force the prefill path: W' = sum_i S_i (.) U_i V_i^T restored per
+                                 tile on tcgen05, then Y = (X diag(1/s)) W'^T on tcgen05 with fp16
+                                 operands (E_UNSUPPORTED unless bf16 factors, n <= 16) */
 } bitstack_kernel;
 
 typedef struct {
@@ -82,7 +86,7 @@ typedef struct {
  * [row_begin, row_end) (row sharding); capacity n_capacity blocks,
  * rank k, factors stored as factor_dtype (Q7: the paper stores FP16).
  * Allocates all device memory up front on `device`.
- * Errors: E_INVALID_ARG (k<1, k>min(d_out,d_in), k>32, n_capacity<1, bad dtype, out==NULL),
+ * Errors: E_INVALID_ARG (k<1, k>min(d_out,d_in), k>16, n_capacity<1, bad dtype, out==NULL),
  *         E_DIM_MISMATCH (bad row range), E_UNSUPPORTED (device not sm_100), E_OOM, E_CUDA. */
 BITSTACK_API bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t n_capacity,
                                 bitstack_dtype factor_dtype, int64_t row_begin, int64_t row_end,
@@ -151,7 +155,8 @@ BITSTACK_API int64_t bitstack_block_size_bits(int64_t m, int64_t n, int32_t k, i
 BITSTACK_API const char* bitstack_last_error(void);
 
 /* ---- measurement hooks (used by bench.py; not part of the paper's problem) ----
- * While enabled, every decode-kernel launch made by bitstack_matmul is bracketed
+ * While enabled, the dominant kernel launch of every bitstack_matmul call (decode:
+ * the Zq + decode kernel pair; SIMT: its kernel; prefill: the GEMM) is bracketed
  * by a pair of CUDA events recorded on the launching stream.  profile_end
  * synchronises those events and returns the number of bracketed launches and the
  * sum of their device durations in milliseconds.  Errors: E_INVALID_ARG, E_CUDA. */

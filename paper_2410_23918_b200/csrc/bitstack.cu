@@ -17,6 +17,7 @@
 #include "aux_kernels.cuh"
 #include "decode_f8.cuh"
 #include "decode_tc.cuh"
+#include "prefill.cuh"
 
 struct bitstack_layer_s {
   int64_t d_out = 0, d_in = 0, row_begin = 0, row_end = 0, rows_local = 0;
@@ -39,6 +40,9 @@ struct bitstack_layer_s {
   int64_t zq_bytes = 0;
   int* status = nullptr;   // sticky device-side numeric-range flag
   int* counters = nullptr; // [row_tiles]
+  uint8_t* pf_w = nullptr; // prefill path: W' operand image (transient workspace, grown on demand)
+  uint8_t* pf_x = nullptr; // prefill path: X' operand image
+  int64_t pf_w_bytes = 0, pf_x_bytes = 0;
   int64_t bytes = 0;
   int64_t block_bytes = 0;
 };
@@ -117,6 +121,8 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
 }
 
 // e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
+constexpr int64_t kPrefillMinBatch = 16;   // AUTO: restored-tile GEMM path from this batch on
+
 template <int NB> struct F8Geom;
 template <> struct F8Geom<1> { static constexpr int R = 4; };
 template <> struct F8Geom<2> { static constexpr int R = 2; };
@@ -174,6 +180,106 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
   CK(cudaLaunchKernelEx(&cfg, bs::decode_f8_kernel<NB, G::R>, prm));
   count_launch();
   return BITSTACK_OK;
+}
+
+bitstack_status record_prof(cudaStream_t st, bool begin, int* slot) {
+  if (!g_prof.on) return BITSTACK_OK;
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  if (begin) {
+    if (g_prof.used >= g_prof.cap) {
+      *slot = -1;
+      return BITSTACK_OK;
+    }
+    *slot = g_prof.used++;
+    CK(cudaEventRecord(g_prof.ev[*slot].first, st));
+  } else if (*slot >= 0) {
+    CK(cudaEventRecord(g_prof.ev[*slot].second, st));
+  }
+  return BITSTACK_OK;
+}
+
+constexpr int kPrefillBN = 256;
+
+bitstack_status grow(bitstack_layer L, uint8_t** buf, int64_t* have, int64_t need, cudaStream_t st) {
+  if (need <= *have) return BITSTACK_OK;
+  CK(cudaStreamSynchronize(st));
+  cudaFree(*buf);
+  *buf = nullptr;
+  L->bytes -= *have;
+  *have = 0;
+  cudaError_t e = cudaMalloc((void**)buf, (size_t)need);
+  if (e != cudaSuccess) return fail(BITSTACK_E_OOM, "prefill workspace (%lld bytes): %s", (long long)need, cudaGetErrorString(e));
+  *have = need;
+  L->bytes += need;
+  return BITSTACK_OK;
+}
+
+// Large-batch path (prefill.cuh): X' image, W' image, GEMM -- three launches on `st`.
+bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
+                               cudaStream_t st) {
+  constexpr int BN = kPrefillBN;
+  using GC = bs::GemmCfg<BN>;
+  using WC = bs::WtileCfg<2>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(bs::prefill_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::kSmemBytes));
+    CK(cudaFuncSetAttribute(bs::wtile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, WC::kSmem(16) + 1024));
+    CK(cudaFuncSetAttribute(bs::wtile_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    attr_done = true;
+  }
+  if (L->n_act > 16) return fail(BITSTACK_E_UNSUPPORTED, "prefill path supports n <= 16 active blocks");
+  const int kc = (int)(L->d_in_pad / bs::kPK);
+  const int rt_img = (L->row_tiles + 1) / 2 * 2;
+  const int nt = (int)((batch + BN - 1) / BN);
+  bitstack_status rs = grow(L, &L->pf_w, &L->pf_w_bytes, (int64_t)rt_img * kc * bs::kImgTileA, st);
+  if (rs) return rs;
+  rs = grow(L, &L->pf_x, &L->pf_x_bytes, (int64_t)nt * kc * BN * bs::kPK * 2, st);
+  if (rs) return rs;
+
+  const long long pieces = (long long)nt * kc * BN * 8;
+  const int xgrid = (int)std::min<long long>((pieces + 255) / 256, (long long)L->sm_count * 16);
+  bs::xprep_kernel<<<xgrid, 256, 0, st>>>(x, xdt, L->d_in, L->inv_s, (int)batch, (int)L->d_in, kc, BN, pieces,
+                                          reinterpret_cast<uint4*>(L->pf_x));
+  count_launch();
+  CK(cudaGetLastError());
+
+  bs::WtileParams wp;
+  wp.signs = L->signs;
+  wp.u = reinterpret_cast<const __nv_bfloat16*>(L->u);
+  wp.v = reinterpret_cast<const __nv_bfloat16*>(L->v);
+  wp.img = L->pf_w;
+  wp.n = L->n_act;
+  wp.nq = L->nq;
+  wp.rows_pad = L->rows_pad;
+  wp.row_tiles = L->row_tiles;
+  wp.kc = kc;
+  wp.row_tiles_img = rt_img;
+  // two CTAs per SM (TMEM: 2 x 256 columns; registers 2 x 256 x 120; SMEM <= 2 x 77 KB)
+  const int wgrid = (int)std::min<int64_t>((int64_t)rt_img * kc, (int64_t)L->sm_count * (512 / WC::kTmemCols));
+  bs::wtile_kernel<2><<<wgrid, WC::kThreads, WC::kSmem(L->n_act), st>>>(wp);
+  count_launch();
+  CK(cudaGetLastError());
+
+  bs::GemmParams gp;
+  gp.a_img = L->pf_w;
+  gp.b_img = L->pf_x;
+  gp.y = y;
+  gp.y_dtype = ydt;
+  gp.y_stride = L->rows_local;
+  gp.batch = (int)batch;
+  gp.rows_local = (int)L->rows_local;
+  gp.row_tiles = L->row_tiles;
+  gp.m2_count = rt_img / 2;
+  gp.nt_count = nt;
+  gp.kc = kc;
+  const int tiles = gp.m2_count * nt;
+  int slot = -1;   // measurement hooks bracket the dominant kernel of the path: the GEMM
+  bitstack_status ps = record_prof(st, true, &slot);
+  if (ps) return ps;
+  bs::prefill_gemm_kernel<BN><<<std::min(tiles, L->sm_count), GC::kThreads, GC::kSmemBytes, st>>>(gp);
+  count_launch();
+  CK(cudaGetLastError());
+  return record_prof(st, false, &slot);
 }
 
 template <int NDIG>
@@ -298,6 +404,8 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   cudaFree(L->counters);
   cudaFree(L->status);
   cudaFree(L->zq);
+  cudaFree(L->pf_w);
+  cudaFree(L->pf_x);
   delete L;
   return BITSTACK_OK;
 }
@@ -321,7 +429,8 @@ bitstack_status bitstack_get_info(bitstack_layer L, bitstack_info* out) {
 
 bitstack_status bitstack_set_kernel(bitstack_layer L, bitstack_kernel kernel) {
   if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
-  if (kernel != BITSTACK_KERNEL_AUTO && kernel != BITSTACK_KERNEL_TC && kernel != BITSTACK_KERNEL_SIMT)
+  if (kernel != BITSTACK_KERNEL_AUTO && kernel != BITSTACK_KERNEL_TC && kernel != BITSTACK_KERNEL_SIMT &&
+      kernel != BITSTACK_KERNEL_PREFILL)
     return fail(BITSTACK_E_INVALID_ARG, "bad kernel selector %d", (int)kernel);
   L->kernel = kernel;
   return BITSTACK_OK;
@@ -434,22 +543,6 @@ bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int3
   return BITSTACK_OK;
 }
 
-static bitstack_status record_prof(cudaStream_t st, bool begin, int* slot) {
-  if (!g_prof.on) return BITSTACK_OK;
-  std::lock_guard<std::mutex> lk(g_prof.mu);
-  if (begin) {
-    if (g_prof.used >= g_prof.cap) {
-      *slot = -1;
-      return BITSTACK_OK;
-    }
-    *slot = g_prof.used++;
-    CK(cudaEventRecord(g_prof.ev[*slot].first, st));
-  } else if (*slot >= 0) {
-    CK(cudaEventRecord(g_prof.ev[*slot].second, st));
-  }
-  return BITSTACK_OK;
-}
-
 bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype x_dtype, void* y,
                                 bitstack_dtype y_dtype, int64_t batch, void* stream) {
   if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
@@ -471,6 +564,13 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
   const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype);
+  // large batch: restored-tile GEMM path (bf16 factors); forced with BITSTACK_KERNEL_PREFILL
+  const bool pf_ok = L->dev_fdt == 1 && L->layout == 1 && L->n_act <= 16;
+  if (L->kernel == BITSTACK_KERNEL_PREFILL && !pf_ok)
+    return fail(BITSTACK_E_UNSUPPORTED, "prefill path needs bf16 factors and n <= 16");
+  if (L->kernel == BITSTACK_KERNEL_PREFILL || (L->kernel == BITSTACK_KERNEL_AUTO && pf_ok && batch >= kPrefillMinBatch))
+    return launch_prefill(L, x, xdt, y, ydt, batch, st);
+
   // tcgen05 path: k <= 16 (zero-padded columns of U', V'), x rows bulk-copied by the
   // TMA engine -> 16-byte aligned x and d_in % 8 == 0.
   const bool tc_ok = L->k <= 16 && L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;

@@ -278,6 +278,57 @@ def test_row_shards_concatenate_to_full(bs):
     assert O.relative_l2(ys, yf) <= 1e-5
 
 
+# ------------------------------------------------------------------ H8: large-batch path
+@pytest.mark.parametrize("shape", [(384, 640), (200, 296), (1100, 264), (128, 64)])
+def test_prefill_parity_ragged(bs, shape):
+    """Restored-tile GEMM path (prefill.cuh) forced at every batch: ragged rows (partial
+    and odd row-tile counts), ragged d_in (chunk tails), batches across 256-token tiles,
+    odd n (blocks per MMA step G = 2)."""
+    d_out, d_in = shape
+    g, s32, blocks = compress_case(d_out, d_in, 5, "bf16", 61 + d_out)
+    lay = make_layer(bs, d_out, d_in, blocks, s32, "bf16")
+    lay.set_kernel("prefill")
+    c0 = bs.launch_count()
+    gpu_y(lay, make_x(2, g, 1))
+    assert bs.launch_count() - c0 == 3          # xprep + wtile + gemm: the prefill kernels ran
+    for batch in (1, 17, 256, 300, 600):
+        x = make_x(batch, g, 300 + batch)
+        for n in (1, 2, 5):
+            lay.set_num_blocks(n)
+            y, xr = gpu_y(lay, x, x_dtype=torch.bfloat16)
+            err = O.relative_l2(y, oracle_y(blocks, s32, n, xr))
+            assert err <= 1e-3, (batch, n, err)
+
+
+def test_prefill_dtypes_auto_and_unsupported(bs):
+    """AUTO picks the prefill path from batch 16 on (same y as forcing it); f32/bf16/f16
+    activations; bf16 y (4e-3); fp32 factors refuse a forced prefill (E_UNSUPPORTED)."""
+    g, s32, blocks = compress_case(256, 384, 4, "bf16", 71)
+    lay = make_layer(bs, 256, 384, blocks, s32, "bf16")
+    x = make_x(40, g, 9)
+    c0 = bs.launch_count()
+    y_auto, xr = gpu_y(lay, x)
+    assert bs.launch_count() - c0 == 3
+    assert O.relative_l2(y_auto, oracle_y(blocks, s32, 4, xr)) <= 1e-3
+    lay.set_kernel("prefill")
+    y_pf, _ = gpu_y(lay, x)
+    np.testing.assert_array_equal(y_auto, y_pf)
+    for xdt in (torch.float32, torch.bfloat16, torch.float16):
+        y, xr = gpu_y(lay, x, x_dtype=xdt)
+        assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 1e-3
+    y, xr = gpu_y(lay, x, y_dtype=torch.bfloat16)
+    assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 4e-3
+    g32, s32f, blocks32 = compress_case(128, 256, 2, "f32", 72)
+    lay32 = make_layer(bs, 128, 256, blocks32, s32f, "f32")
+    x32 = make_x(64, g32, 1)
+    y32, xr32 = gpu_y(lay32, x32)          # AUTO keeps the exact fp32-factor decode path
+    assert O.relative_l2(y32, oracle_y(blocks32, s32f, 2, xr32)) <= 1e-5
+    lay32.set_kernel("prefill")
+    with pytest.raises(bs.BitStackError) as e:
+        gpu_y(lay32, x32)
+    assert e.value.name == "E_UNSUPPORTED"
+
+
 # ------------------------------------------------------------------ full sizes, sampled rows
 def _sampled_reference(signs, u, v, s, n, x, rows, d_out, d_in):
     """Oracle y on a subset of output rows: slice the stored blocks' rows (oracle unpack
@@ -294,6 +345,8 @@ def _sampled_reference(signs, u, v, s, n, x, rows, d_out, d_in):
     ("c5_down_70b", 8192, 28672, 12, 1),
     ("c5_down_70b_b4", 8192, 28672, 12, 4),
     ("c3_up", 14336, 4096, 8, 16),
+    ("c3_gate_prefill", 14336, 4096, 8, 2048),
+    ("c3_down_prefill", 4096, 14336, 8, 300),
     ("c4_kproj", 1024, 4096, 3, 1),
 ])
 def test_full_size_sampled_rows(bs, name, d_out, d_in, n, batch):
