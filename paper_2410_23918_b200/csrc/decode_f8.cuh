@@ -65,9 +65,10 @@ struct ZqCfg {
 // cycles, dwarfed the 100 cycles of MMA work per tile).  Each warpgroup keeps a 2-slot A
 // ring released by its own tcgen05.commit, and its own accumulator (no cross-issuer
 // hazards).  TMEM: R x N accumulator columns + R x NSLOT x 32 A columns <= 512.
-template <int NB, int R_>
+template <int NB, int R_, int P_ = 1>
 struct DecodeF8Cfg {
   static constexpr int N = ZqCfg<NB>::N;
+  static constexpr int P = P_;                               // units per warpgroup iteration
   static constexpr int R = R_;                               // row tiles = warpgroups
   static constexpr int kThreads = 32 * (4 * R + 1);          // + producer warp
   static constexpr int kWarpProducer = 4 * R;
@@ -83,13 +84,13 @@ struct DecodeF8Cfg {
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes;
   static constexpr uint32_t kTmemCols = 512;
   static constexpr int kACols = 32;                          // 128 rows x 128 e4m3 per tile
-  static constexpr int NS0 = (512 - R * N) / (R * kACols);
-  static constexpr int NSLOT = NS0 > 4 ? 4 : NS0;            // A slots per warpgroup
-  static constexpr uint32_t kAccCol = R * NSLOT * kACols;
+  static constexpr int NS0 = (512 - R * N) / (R * P * kACols);
+  static constexpr int NSLOT = NS0 > 4 ? 4 : NS0;            // A slots (of P tiles) per warpgroup
+  static constexpr uint32_t kAccCol = R * NSLOT * P * kACols;
   static constexpr uint32_t LBO = (N / 8) * 128;
   static constexpr uint32_t SBO = 128;
   static_assert(N <= 256 && N % 16 == 0, "invalid MMA N");
-  static_assert(NSLOT >= 2, "need at least double-buffered A");
+  static_assert(NSLOT >= (P == 1 ? 2 : 1), "need at least double-buffered A");
   static_assert(kAccCol + R * N <= kTmemCols, "TMEM overflow");
   static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
   static_assert(R >= 1 && R <= 7, "named barriers 1..R");
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(128) zq_kernel(const ZqParams p) {
 template <int NB, int R_>
 __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_kernel(const DecodeParams p) {
   using C = DecodeF8Cfg<NB, R_>;
-  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT;
+  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT, P = C::P;
   extern __shared__ __align__(1024) uint8_t smem[];
 
   uint8_t* bar_area = smem + STAGES * C::kStageBytes;
@@ -217,9 +218,16 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
   const int row0 = g * R * kTileRows;
 #ifdef BS_DECODE_TRACE
   // debug build only (scripts/trace_f8.py): CTA 0 timeline of warpgroup 3, clock64 relative
-  // to kernel entry, 16 slots per unit, written to the bitstack_debug_set buffer
+  // to kernel entry, 16 slots per unit, written to the bitstack_debug_set buffer; every
+  // CTA's entry / exit %globaltimer (ns) at slots 65536 + 4 * blockIdx.x
   long long* trace = (p.dbg_acc && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
   const long long tstart = clock64();
+  if (p.dbg_acc && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x] = (long long)gt;
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x + 2] = nunits;
+  }
 #define BS_TRACE(k_unit, k) do { if (warp == 12 && trace && lane == 0) trace[(k_unit) * 16 + (k)] = clock64() - tstart; } while (0)
 #else
 #define BS_TRACE(k_unit, k) do { } while (0)
@@ -288,43 +296,55 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
     uint32_t ph = 0, sph = 0, acc_ph = 0;
     int E = 0;
     bool have_e = false;
-    for (int k = 0; active && k < nunits; ++k) {
+    int cnt = 1;
+    // Each iteration takes P units (P tiles into one P x 32-column A slot) -- fewer than P
+    // when a block ends, so an iteration never straddles two accumulations.
+    for (int k = 0; active && k < nunits; k += cnt) {
       const bool first = (k == 0) || (q == 0);
-      const bool last = (k == nunits - 1) || (q == p.nq - 1);
+      cnt = 1;
+      while (cnt < P && k + cnt < nunits && q + cnt < p.nq) ++cnt;    // same block, in range
+      const bool last = (k + cnt == nunits) || (q + cnt == p.nq);
       // One warp per warpgroup polls the stage / slot mbarriers; the named barrier below
       // releases the other three (4x fewer mbarrier waits through the SM's barrier unit).
       if (qd == 0) {
         BS_TRACE(k, 7);
-        mbar_wait(&full[s], ph);
+        int sw_ = s;
+        uint32_t pw_ = ph;
+        for (int u = 0; u < cnt; ++u) {
+          mbar_wait(&full[sw_], pw_);
+          if (++sw_ == STAGES) { sw_ = 0; pw_ ^= 1; }
+        }
         BS_TRACE(k, 2);
         mbar_wait(&a_empty[wg * NSLOT + slot], sph ^ 1);
       }
       BS_TRACE(k, 0);
       asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
       BS_TRACE(k, 1);
-      const uint8_t* st = smem + s * C::kStageBytes;
-      // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit
-      const int e_u = *reinterpret_cast<const int*>(st + C::kOffMeta);
-      int a_exp = 0;
-      if (e_u != kZqSentinel) {
-        if (!have_e) { E = e_u; have_e = true; }
-        a_exp = E - e_u;
-        if (a_exp < -6 || a_exp > 8) {  // |x/s| range across this CTA's units beyond e4m3 A range
-          if (lane == 0 && p.status) atomicOr(p.status, 1);
-          a_exp = a_exp < -6 ? -6 : 8;
-        }
-      }
-      const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
-      const uint4 sw = reinterpret_cast<const uint4*>(st)[t * kTileRows + row_in_tile];
       tc_fence_after();
-      const uint32_t a_col = tbase + (uint32_t)(C::kACols * (wg * NSLOT + slot));
-      {
+      const uint32_t a_col = tbase + (uint32_t)(C::kACols * P * (wg * NSLOT + slot));
+      int su = s;
+      for (int u = 0; u < cnt; ++u) {
+        const uint8_t* st = smem + su * C::kStageBytes;
+        // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit
+        const int e_u = *reinterpret_cast<const int*>(st + C::kOffMeta);
+        int a_exp = 0;
+        if (e_u != kZqSentinel) {
+          if (!have_e) { E = e_u; have_e = true; }
+          a_exp = E - e_u;
+          if (a_exp < -6 || a_exp > 8) {  // |x/s| range across this CTA's units beyond e4m3 A range
+            if (lane == 0 && p.status) atomicOr(p.status, 1);
+            a_exp = a_exp < -6 ? -6 : 8;
+          }
+        }
+        const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
+        const uint4 sw = reinterpret_cast<const uint4*>(st)[t * kTileRows + row_in_tile];
         uint32_t o[32];
         expand_e4m3(sw.x, e8, o);
         expand_e4m3(sw.y, e8, o + 8);
         expand_e4m3(sw.z, e8, o + 16);
         expand_e4m3(sw.w, e8, o + 24);
-        tmem_st32(a_col + lane_base, o);
+        tmem_st32(a_col + (uint32_t)(C::kACols * u) + lane_base, o);
+        if (++su == STAGES) su = 0;
       }
       BS_TRACE(k, 3);
       tmem_st_wait();
@@ -334,25 +354,35 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
       BS_TRACE(k, 5);
       if (issuer) {
         tc_fence_after();
-        const uint64_t bdesc0 = smem_desc_kmajor(smem_u32(smem + s * C::kStageBytes + C::kOffZ), C::LBO, C::SBO);
         if (elect_one()) {
+          int sm_ = s;
+          for (int u = 0; u < cnt; ++u) {
+            const uint64_t bdesc0 = smem_desc_kmajor(smem_u32(smem + sm_ * C::kStageBytes + C::kOffZ), C::LBO, C::SBO);
 #pragma unroll
-          for (int m = 0; m < kSubK / 32; ++m) {
-            mma_f8_ts(d_acc, a_col + 8 * m, bdesc0 + (uint64_t)((m * 2 * C::LBO) >> 4), idesc,
-                      (m > 0 || !first) ? 1u : 0u);
-            BS_TRACE(k, 12 + m);
+            for (int m = 0; m < kSubK / 32; ++m) {
+              mma_f8_ts(d_acc, a_col + (uint32_t)(C::kACols * u) + 8 * m, bdesc0 + (uint64_t)((m * 2 * C::LBO) >> 4),
+                        idesc, (m > 0 || u > 0 || !first) ? 1u : 0u);
+              BS_TRACE(k, 12 + m);
+            }
+            if (++sm_ == STAGES) sm_ = 0;
           }
           mma_commit(&a_empty[wg * NSLOT + slot]);
-          mma_commit(&empty[s]);
+          sm_ = s;
+          for (int u = 0; u < cnt; ++u) {
+            mma_commit(&empty[sm_]);
+            if (++sm_ == STAGES) sm_ = 0;
+          }
           if (last) mma_commit(&acc_full[wg]);
         }
         __syncwarp();
       }
       BS_TRACE(k, 6);
       if (++slot == NSLOT) { slot = 0; sph ^= 1; }
-      if (++s == STAGES) { s = 0; ph ^= 1; }
+      s += cnt;
+      if (s >= STAGES) { s -= STAGES; ph ^= 1; }
       const int ci = i;
-      if (++q == p.nq) { q = 0; ++i; }
+      q += cnt;
+      if (q == p.nq) { q = 0; ++i; }
 
       if (last) {
         // ---- epilogue for block ci: y += 2^-E sum_r U'_ci[row, r] (T_d0 + T_d1 + T_d2)[row, r]
@@ -415,6 +445,13 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
     }
   }
 
+#ifdef BS_DECODE_TRACE
+  if (p.dbg_acc && threadIdx.x == 32 * 12) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x + 1] = (long long)gt;
+  }
+#endif
   // ---- teardown + last-CTA-of-group finalisation
   __threadfence();
   tc_fence_before();

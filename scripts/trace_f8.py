@@ -14,11 +14,17 @@ lay.load_blocks(0, signs, torch.from_numpy(u).to(torch.bfloat16), torch.from_num
 x = torch.from_numpy(make_x(1, channel_gains(d, 5), 6).astype(np.float32)).to(torch.bfloat16).cuda()
 for _ in range(3): lay.matmul(x)
 lib = B.load_library(); lib.bitstack_debug_set.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
-tr = torch.zeros(4096 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(65536 + 4 * 1024, dtype=torch.int64, device="cuda")
 lib.bitstack_debug_set(tr.data_ptr(), None)
 lay.matmul(x); torch.cuda.synchronize()
 lib.bitstack_debug_set(None, None)
-t = tr.cpu().numpy().reshape(-1, 16)
+full = tr.cpu().numpy()
+t = full[:65536].reshape(-1, 16)
+cta = full[65536:].reshape(-1, 4)
+cta = cta[cta[:, 0] != 0]
+if len(cta):
+  t0 = cta[:, 0].min()
+  print('CTAs', len(cta), 'entry spread us', (cta[:, 0].max() - t0) / 1e3, 'exit (wg3 done) min/med/max us', (cta[:, 1].min() - t0) / 1e3, (np.median(cta[:, 1]) - t0) / 1e3, (cta[:, 1].max() - t0) / 1e3, 'units min/max', cta[:, 2].min(), cta[:, 2].max())
 print("nonzero", int((t != 0).sum()), "max", int(t.max()), "min", int(t.min()))
 nu = int((t[:, 6] != 0).sum())
 print("units traced:", nu)
