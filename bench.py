@@ -321,7 +321,7 @@ def main():
         dom_name = "bs::zq_kernel<%d> + bs::decode_f8_kernel<%d> (PDL pair)" % (min(batch, 4), min(batch, 4))
     else:                       # dominant kernel: the GEMM, 2 B r d_in flops
         dom_units = 2.0 * batch * rows * d_in / 1e12
-        dom_name = "bs::prefill_gemm_kernel<256>"
+        dom_name = "bs::prefill_gemm_kernel<BN> (BN = 128 or 256 by wave fill)"
     achieved = dom_units / (kernel_ms * 1e-3)
     peak, peak_src = peaks(w["kind"])
     traffic = None

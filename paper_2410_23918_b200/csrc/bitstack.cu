@@ -199,7 +199,15 @@ bitstack_status record_prof(cudaStream_t st, bool begin, int* slot) {
   return BITSTACK_OK;
 }
 
-constexpr int kPrefillBN = 256;
+// GEMM token-tile width: 256 (higher operand reuse) unless 128 fills the SMs' last wave
+// clearly better (persistent grid of sm_count CTAs; tiles = row_tiles/2 x ceil(B/BN)).
+int prefill_bn(int64_t m2, int64_t batch, int sms) {
+  auto eff = [&](int bn) {
+    const int64_t t = m2 * ((batch + bn - 1) / bn);
+    return (double)t / (double)(((t + sms - 1) / sms) * sms);
+  };
+  return eff(128) > eff(256) + 0.05 ? 128 : 256;
+}
 
 bitstack_status grow(bitstack_layer L, uint8_t** buf, int64_t* have, int64_t need, cudaStream_t st) {
   if (need <= *have) return BITSTACK_OK;
@@ -216,9 +224,9 @@ bitstack_status grow(bitstack_layer L, uint8_t** buf, int64_t* have, int64_t nee
 }
 
 // Large-batch path (prefill.cuh): X' image, W' image, GEMM -- three launches on `st`.
+template <int BN>
 bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
                                cudaStream_t st) {
-  constexpr int BN = kPrefillBN;
   using GC = bs::GemmCfg<BN>;
   using WC = bs::WtileCfg<2>;
   static bool attr_done = false;
@@ -239,8 +247,9 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
 
   const long long pieces = (long long)nt * kc * BN * 8;
   const int xgrid = (int)std::min<long long>((pieces + 255) / 256, (long long)L->sm_count * 16);
+  const bool xvec = L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
   bs::xprep_kernel<<<xgrid, 256, 0, st>>>(x, xdt, L->d_in, L->inv_s, (int)batch, (int)L->d_in, kc, BN, pieces,
-                                          reinterpret_cast<uint4*>(L->pf_x));
+                                          reinterpret_cast<uint4*>(L->pf_x), xvec);
   count_launch();
   CK(cudaGetLastError());
 
@@ -281,6 +290,13 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   count_launch();
   CK(cudaGetLastError());
   return record_prof(st, false, &slot);
+}
+
+bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
+                               cudaStream_t st) {
+  const int64_t m2 = (L->row_tiles + 1) / 2;
+  return prefill_bn(m2, batch, L->sm_count) == 128 ? launch_prefill<128>(L, x, xdt, y, ydt, batch, st)
+                                                   : launch_prefill<256>(L, x, xdt, y, ydt, batch, st);
 }
 
 template <int NDIG>

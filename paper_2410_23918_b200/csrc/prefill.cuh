@@ -46,7 +46,7 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 // dense in image order.  Tokens >= batch and columns >= d_in are zero.
 __global__ void __launch_bounds__(256) xprep_kernel(const void* __restrict__ x, int x_dtype, long long x_stride,
                                                    const float* __restrict__ inv_s, int batch, int d_in,
-                                                   int kc, int bn, long long pieces, uint4* __restrict__ img) {
+                                                   int kc, int bn, long long pieces, uint4* __restrict__ img, bool vec) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < pieces;
        e += (long long)gridDim.x * blockDim.x) {
     const long long tile = e / (bn * 8);
@@ -57,10 +57,35 @@ __global__ void __launch_bounds__(256) xprep_kernel(const void* __restrict__ x, 
     const int tok = nt * bn + g * 8 + r8;
     const int col0 = c * kPK + k8 * 8;
     float v[8];
+    if (vec && tok < batch && col0 + 8 <= d_in) {   // 16-byte aligned row segment: vector loads
+      const float4 s0 = __ldg(reinterpret_cast<const float4*>(inv_s + col0));
+      const float4 s1 = __ldg(reinterpret_cast<const float4*>(inv_s + col0) + 1);
+      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const long long o = (long long)tok * x_stride + col0;
+      if (x_dtype == 0) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + o));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + o) + 1);
+        const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int col = col0 + t;
-      v[t] = (tok < batch && col < d_in) ? load_act(x, (long long)tok * x_stride + col, x_dtype) * __ldg(inv_s + col) : 0.f;
+        for (int t = 0; t < 8; ++t) v[t] = xv[t] * sc[t];
+      } else {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + o));
+        const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          float2 f;
+          if (x_dtype == 1) f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[t]));
+          else f = __half22float2(*reinterpret_cast<const __half2*>(&w[t]));
+          v[2 * t] = f.x * sc[2 * t];
+          v[2 * t + 1] = f.y * sc[2 * t + 1];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int col = col0 + t;
+        v[t] = (tok < batch && col < d_in) ? load_act(x, (long long)tok * x_stride + col, x_dtype) * __ldg(inv_s + col) : 0.f;
+      }
     }
     img[e] = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
   }

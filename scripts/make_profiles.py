@@ -56,6 +56,37 @@ def to_bytes(v, unit):
     return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
+def prefill(r, key="c3_up_n8_b2048_g1"):
+    """profiles/<r>_prefill_*.txt from gpurun_out/pf_launches.csv and pf_full.ncu-rep."""
+    lp = os.path.join(ROOT, "gpurun_out", "pf_launches.csv")
+    agg = launches(lp)
+    tot = sum(sum(v) for v in agg.values())
+    lines = ["# ncu launch list of `python bench.py --workload c3_up --steps 20 --warmup 3 --no-cpu-baseline --no-graph`",
+             "# (--metrics gpu__time_duration.sum --clock-control none, kernels xprep|wtile|prefill_gemm; cold-cache,",
+             "#  serialised -- compare shares)",
+             f"{'kernel':60s} {'launches':>8s} {'avg_us':>10s} {'share':>7s}"]
+    for k, v in agg.items():
+        lines.append(f"{k:60s} {len(v):8d} {sum(v) / len(v):10.2f} {sum(v) / tot:7.3f}")
+    open(os.path.join(ROOT, "profiles", f"{r}_prefill_launches.txt"), "w").write("\n".join(lines) + "\n")
+    rep = os.path.join(ROOT, "gpurun_out", "pf_full.ncu-rep")
+    out = ["# ncu --set full --clock-control none --import-source on: one launch each of wtile_kernel and",
+           "# prefill_gemm_kernel (C3 up/gate 14336x4096, n=8, B=2048), from gpurun_out/pf_full.ncu-rep"]
+    gemm_traffic = None
+    for name, m in full(rep):
+        out.append(name)
+        for k, (v, u) in m.items():
+            out.append(f"    {k:66s} {v} {u or ''}")
+        if "prefill_gemm" in name:
+            gemm_traffic = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
+    open(os.path.join(ROOT, "profiles", f"{r}_prefill_ncu_full.txt"), "w").write("\n".join(out) + "\n")
+    if gemm_traffic is not None:
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        tj = json.load(open(tp)) if os.path.exists(tp) else {}
+        tj[key] = gemm_traffic
+        json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
+    print("\n".join(lines + out))
+
+
 def main(r, key="c2_n16_b1_g1"):
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     lp = os.path.join(ROOT, "gpurun_out", f"launches_{r}.csv")
@@ -88,11 +119,15 @@ def main(r, key="c2_n16_b1_g1"):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     tj = json.load(open(tp)) if os.path.exists(tp) else {}
     tj[key] = traffic
-    tj["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per call of the zq_kernel + decode_f8_kernel "
-                   "pair from one ncu --set full capture; keys <workload>_n<n>_b<batch>_g<world>")
+    tj["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per call of the roofline's dominant kernel, "
+                   "from one ncu --set full capture: decode keys = the zq_kernel + decode_f8_kernel pair, "
+                   "prefill (c3_*) keys = prefill_gemm_kernel; keys <workload>_n<n>_b<batch>_g<world>")
     json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
     print("\n".join(lines + out))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    if len(sys.argv) > 2 and sys.argv[2] == "prefill":
+        prefill(sys.argv[1])
+    else:
+        main(*sys.argv[1:])
