@@ -124,7 +124,7 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
 // e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
 constexpr int64_t kPrefillMinBatch = 16;   // AUTO: restored-tile GEMM path from this batch on
 
-template <int NB> struct F8Geom;
+template <int NB> struct F8Geom;   // R: row tiles per CTA
 template <> struct F8Geom<1> { static constexpr int R = 4; };
 template <> struct F8Geom<2> { static constexpr int R = 2; };
 template <> struct F8Geom<4> { static constexpr int R = 2; };
@@ -139,6 +139,7 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
                             C::kSmemBytes));
     attr_done = true;
   }
+
   const int64_t units = (int64_t)prm_in.n * prm_in.nq;
   const int64_t need = units * C::kZUnit;
   if (need > L->zq_bytes) {  // grows once per larger batch class; never inside steady state

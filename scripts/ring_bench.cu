@@ -283,6 +283,105 @@ extern "C" void run_trace() {
   cudaMemcpyToSymbol(g_tr, &z, sizeof(z));
 }
 
+// One elected block of 16 MMAs (4 tiles x 4 K-steps) per iteration, alone or with 16 warps
+// streaming tcgen05.st; DESC = 0: descriptors recomputed per MMA like the decode kernel
+// (slot/stage arithmetic), 1: all 16 (a, b, d) operands precomputed in registers.
+template <int STW, int DESC, int NCOMMIT = 0, int FENCE = 0>
+__global__ void __launch_bounds__(544, 1) mma16(int iters, long long* out) {
+  __shared__ __align__(1024) uint8_t zs[4][128 * 48];
+  __shared__ uint64_t done, cb[4];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32;
+  for (int e = threadIdx.x; e < 4 * 128 * 48 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(zs)[e] = 0x38383838u;
+  if (threadIdx.x == 0) { mbar_init(&done, 1); for (int c = 0; c < 4; ++c) mbar_init(&cb[c], 1); fence_mbar_init(); }
+  if (warp == 16) tmem_alloc<512>(&tslot);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(48 >> 3) << 17) | ((128u >> 4) << 24);
+  long long t0 = clock64();
+  if (warp == 16) {
+    uint64_t bd[4];
+    for (int u = 0; u < 4; ++u) bd[u] = smem_desc_kmajor(smem_u32(zs[u]), (48 / 8) * 128, 128);
+    for (int it = 0; it < iters; ++it) {
+      if (FENCE == 1) tc_fence_after();
+      if (FENCE == 2) { mbar_wait(&cb[3], 1); tc_fence_after(); }   // completed-phase wait + fence
+      if (elect_one()) {
+        if (DESC == 0) {
+          for (int u = 0; u < 4; ++u) {
+            const int st = (it * 4 + u) % 3;
+            const uint64_t b0 = smem_desc_kmajor(smem_u32(zs[st]), (48 / 8) * 128, 128);
+            const uint32_t a_col = tbase + 32 * ((it + u) & 3);
+            const uint32_t d = tbase + 256 + u * 48;
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              mma_f8_ts(d, a_col + 8 * m, b0 + (uint64_t)((m * 2 * (48 / 8) * 128) >> 4), idesc, m > 0 || it > 0);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              mma_f8_ts(tbase + 256 + u * 48, tbase + 32 * u + 8 * m, bd[u] + (uint64_t)((m * 2 * (48 / 8) * 128) >> 4),
+                        idesc, 1u);
+        }
+        for (int c = 0; c < NCOMMIT; ++c) mma_commit(&cb[c]);
+        if (it + 1 >= iters) mma_commit(&done);
+      }
+      __syncwarp();
+    }
+    mbar_wait(&done, 0);
+    long long t1 = clock64();
+    if (threadIdx.x == 512) out[blockIdx.x] = t1 - t0;
+  } else if (STW) {
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t w0 = 0x12345678u * (threadIdx.x + 1), w1 = w0 ^ 0x9e3779b9u, w2 = w0 * 3u, w3 = w1 * 5u;
+    const uint32_t e8 = 0x38383838u ^ (uint32_t)(iters & 0);
+    for (int it = 0; it < iters; ++it) {
+      if (STW == 2) {   // + a 16-byte LDS per thread per iteration from the operand area (signs)
+        const uint4 v = reinterpret_cast<const uint4*>(&zs[0][0])[(threadIdx.x + it * 37) & 1535];
+        w0 ^= v.x; w1 ^= v.y; w2 ^= v.z; w3 ^= v.w;
+      }
+      uint32_t o[32];
+      expand_e4m3(w0, e8, o); expand_e4m3(w1, e8, o + 8); expand_e4m3(w2, e8, o + 16); expand_e4m3(w3, e8, o + 24);
+      tmem_st32(tbase + lane_base + (uint32_t)(128 + 32 * (warp >> 2)), o);
+      tmem_st_wait();
+      w0 = w0 * 1664525u + 1013904223u;
+      w1 ^= w0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 16) tmem_dealloc<512>(tbase);
+}
+
+extern "C" void run_mma16() {
+  const int iters = 1024;
+  auto go = [&](auto k, const char* name) {
+    long long* d; long long h;
+    cudaMalloc(&d, 8);
+    k<<<1, 544>>>(iters, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    printf("%-60s %7.1f cycles per 16-MMA block (%5.1f per MMA) %s\n", name, h / (double)iters, h / (16.0 * iters),
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+  };
+  go(mma16<0, 0>, "16 MMAs/block, per-MMA descriptor math, alone");
+  go(mma16<0, 1>, "16 MMAs/block, precomputed descriptors, alone");
+  go(mma16<1, 0>, "16 MMAs/block, per-MMA descriptor math, + 16 STTM warps");
+  go(mma16<1, 1>, "16 MMAs/block, precomputed descriptors, + 16 STTM warps");
+  go(mma16<1, 1, 1>, "  ... + 1 commit per block");
+  go(mma16<1, 1, 3>, "  ... + 3 commits per block");
+  go(mma16<0, 1, 3>, "16 MMAs/block, precomputed, alone, 3 commits per block");
+  go(mma16<0, 1, 3, 1>, "  alone, 3 commits + fence::after_thread_sync per block");
+  go(mma16<0, 1, 3, 2>, "  alone, 3 commits + completed mbar wait + fence per block");
+  go(mma16<1, 1, 3, 1>, "  + STTM warps, 3 commits + fence per block");
+  go(mma16<2, 1, 3, 1>, "  + STTM warps with LDS.128, 3 commits + fence per block");
+}
+
 extern "C" void run_contention() {
   launch(mma_vs_sttm<0, 4>, "MMA warp alone (4 MMAs/tile)", 544, 1);
   launch(mma_vs_sttm<1, 4>, "MMA warp + 16 warps expand+STTM (no sync)", 544, 1);
