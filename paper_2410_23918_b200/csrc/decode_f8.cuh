@@ -304,19 +304,18 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
       cnt = 1;
       while (cnt < P && k + cnt < nunits && q + cnt < p.nq) ++cnt;    // same block, in range
       const bool last = (k + cnt == nunits) || (q + cnt == p.nq);
-      // One warp per warpgroup polls the stage / slot mbarriers; the named barrier below
-      // releases the other three (4x fewer mbarrier waits through the SM's barrier unit).
-      if (qd == 0) {
-        BS_TRACE(k, 7);
-        int sw_ = s;
-        uint32_t pw_ = ph;
-        for (int u = 0; u < cnt; ++u) {
-          mbar_wait(&full[sw_], pw_);
-          if (++sw_ == STAGES) { sw_ = 0; pw_ ^= 1; }
+      // Warp 1 of the warpgroup polls the stage / slot mbarriers of an iteration (the named
+      // barrier below releases the other three); for iterations after the first it does so
+      // at the end of the PREVIOUS iteration, while warp 0 issues the MMAs, so the ~150-cycle
+      // mbarrier waits leave the warpgroup's critical path.
+      auto waits = [&](int s_, uint32_t ph_, int cnt_, int slot_, uint32_t sph_) {
+        for (int u = 0; u < cnt_; ++u) {
+          mbar_wait(&full[s_], ph_);
+          if (++s_ == STAGES) { s_ = 0; ph_ ^= 1; }
         }
-        BS_TRACE(k, 2);
-        mbar_wait(&a_empty[wg * NSLOT + slot], sph ^ 1);
-      }
+        mbar_wait(&a_empty[wg * NSLOT + slot_], sph_ ^ 1);
+      };
+      if (qd == 1 && k == 0) waits(s, ph, cnt, slot, sph);
       BS_TRACE(k, 0);
       asm volatile("bar.sync %0, 128;" ::"r"(1 + wg) : "memory");
       BS_TRACE(k, 1);
@@ -339,11 +338,20 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
         const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
         const uint4 sw = reinterpret_cast<const uint4*>(st)[t * kTileRows + row_in_tile];
         uint32_t o[32];
+#ifdef BS_EXP_NO_EXPAND   // timing experiments only (scripts/exp_decode.sh): results are wrong
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = e8 ^ sw.x;
+#else
         expand_e4m3(sw.x, e8, o);
         expand_e4m3(sw.y, e8, o + 8);
         expand_e4m3(sw.z, e8, o + 16);
         expand_e4m3(sw.w, e8, o + 24);
+#endif
+#ifndef BS_EXP_NO_STTM
         tmem_st32(a_col + (uint32_t)(C::kACols * u) + lane_base, o);
+#else
+        if (o[0] == 0x12345u && o[31] == 0x777u) p.status[1] = 1;   // keep the expansion alive
+#endif
         if (++su == STAGES) su = 0;
       }
       BS_TRACE(k, 3);
@@ -358,12 +366,16 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
           int sm_ = s;
           for (int u = 0; u < cnt; ++u) {
             const uint64_t bdesc0 = smem_desc_kmajor(smem_u32(smem + sm_ * C::kStageBytes + C::kOffZ), C::LBO, C::SBO);
+#ifndef BS_EXP_NO_MMA
 #pragma unroll
             for (int m = 0; m < kSubK / 32; ++m) {
               mma_f8_ts(d_acc, a_col + (uint32_t)(C::kACols * u) + 8 * m, bdesc0 + (uint64_t)((m * 2 * C::LBO) >> 4),
                         idesc, (m > 0 || u > 0 || !first) ? 1u : 0u);
               BS_TRACE(k, 12 + m);
             }
+#else
+            (void)bdesc0;
+#endif
             if (++sm_ == STAGES) sm_ = 0;
           }
           mma_commit(&a_empty[wg * NSLOT + slot]);
@@ -383,6 +395,11 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
       const int ci = i;
       q += cnt;
       if (q == p.nq) { q = 0; ++i; }
+      if (qd == 1 && k + cnt < nunits) {   // the next iteration's waits (see above)
+        int ncnt = 1;
+        while (ncnt < P && k + cnt + ncnt < nunits && q + ncnt < p.nq) ++ncnt;
+        waits(s, ph, ncnt, slot, sph);
+      }
 
       if (last) {
         // ---- epilogue for block ci: y += 2^-E sum_r U'_ci[row, r] (T_d0 + T_d1 + T_d2)[row, r]
