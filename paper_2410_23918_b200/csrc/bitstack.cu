@@ -141,6 +141,7 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
   }
 
 
+
   const int64_t units = (int64_t)prm_in.n * prm_in.nq;
   const int64_t need = units * C::kZUnit;
   if (need > L->zq_bytes) {  // grows once per larger batch class; never inside steady state

@@ -357,6 +357,75 @@ __global__ void __launch_bounds__(544, 1) mma16(int iters, long long* out) {
   if (warp == 16) tmem_dealloc<512>(tbase);
 }
 
+// Does writing an A slot with tcgen05.st right before the MMAs that read it slow the MMAs?
+// 4 warps (one per lane quadrant) write slot (it % NS) each iteration, sync on a named barrier,
+// warp 0 issues 4 MMAs from that slot (SAME = 1) or from a never-written slot (SAME = 0).
+template <int SAME, int NS>
+__global__ void __launch_bounds__(128, 1) st_then_mma(int iters, long long* out) {
+  __shared__ __align__(1024) uint8_t zs[128 * 48];
+  __shared__ uint64_t done, slot_free[8];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x / 32;
+  for (int e = threadIdx.x; e < 128 * 48 / 4; e += blockDim.x) reinterpret_cast<uint32_t*>(zs)[e] = 0x38383838u;
+  if (threadIdx.x == 0) { mbar_init(&done, 1); for (int i = 0; i < 8; ++i) mbar_init(&slot_free[i], 1); fence_mbar_init(); }
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(48 >> 3) << 17) | ((128u >> 4) << 24);
+  const uint64_t bd = smem_desc_kmajor(smem_u32(zs), (48 / 8) * 128, 128);
+  uint32_t o[32];
+  for (int e = 0; e < 32; ++e) o[e] = 0x38383838u + e;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    const int sl = it % NS;
+    if (it >= NS) mbar_wait(&slot_free[sl], (uint32_t)(((it / NS) - 1) & 1));
+    tc_fence_after();
+    tmem_st32(tbase + 32 * sl + lane_base, o);
+    tmem_st_wait();
+    tc_fence_before();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (warp == 0) {
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a = SAME ? tbase + 32 * sl : tbase + 32 * 7;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+          mma_f8_ts(tbase + 256, a + 8 * m, bd + (uint64_t)((m * 2 * (48 / 8) * 128) >> 4), idesc, 1u);
+        mma_commit(&slot_free[sl]);
+        if (it + 1 >= iters) mma_commit(&done);
+      }
+      __syncwarp();
+    }
+  }
+  if (warp == 0) mbar_wait(&done, 0);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
+extern "C" void run_stmma() {
+  const int iters = 2048;
+  auto go = [&](auto k, const char* name) {
+    long long* d; long long h;
+    cudaMalloc(&d, 8);
+    k<<<1, 128>>>(iters, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    printf("%-58s %7.1f cycles per iteration (4 MMAs) %s\n", name, h / (double)iters, e == cudaSuccess ? "" : cudaGetErrorString(e));
+  };
+  go(st_then_mma<1, 2>, "STTM slot -> MMAs read it (2 slots)");
+  go(st_then_mma<0, 2>, "STTM slot, MMAs read another slot (2 slots)");
+  go(st_then_mma<1, 4>, "STTM slot -> MMAs read it (4 slots)");
+  go(st_then_mma<0, 4>, "STTM slot, MMAs read another slot (4 slots)");
+}
+
 extern "C" void run_mma16() {
   const int iters = 1024;
   auto go = [&](auto k, const char* name) {

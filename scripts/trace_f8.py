@@ -2,7 +2,8 @@
 import ctypes, os, sys
 sys.path.insert(0, ".")
 from paper_2410_23918_b200.build import build
-os.environ["BITSTACK_LIB"] = build(extra=["-DBS_DECODE_TRACE"], out=os.path.abspath("scripts/libbitstack_trace.so"))
+if "BITSTACK_LIB" not in os.environ:
+    os.environ["BITSTACK_LIB"] = build(extra=["-DBS_DECODE_TRACE"], out=os.path.abspath("scripts/libbitstack_trace.so"))
 import numpy as np, torch
 import paper_2410_23918_b200 as pkg
 from paper_2410_23918_b200 import bitstack as B
