@@ -202,6 +202,11 @@ bitstack_status record_prof(cudaStream_t st, bool begin, int* slot) {
   return BITSTACK_OK;
 }
 
+#ifndef BS_WTILE_G
+#define BS_WTILE_G 2
+#endif
+constexpr int kWtileG = BS_WTILE_G;   // blocks per wtile MMA step (2: 2 CTAs/SM; 4: 1 CTA/SM)
+
 // GEMM token-tile width: 256 (higher operand reuse) unless 128 fills the SMs' last wave
 // clearly better (persistent grid of sm_count CTAs; tiles = row_tiles/2 x ceil(B/BN)).
 int prefill_bn(int64_t m2, int64_t batch, int sms) {
@@ -231,12 +236,12 @@ template <int BN>
 bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
                                cudaStream_t st) {
   using GC = bs::GemmCfg<BN>;
-  using WC = bs::WtileCfg<2>;
+  using WC = bs::WtileCfg<kWtileG>;
   static bool attr_done = false;
   if (!attr_done) {
     CK(cudaFuncSetAttribute(bs::prefill_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::kSmemBytes));
-    CK(cudaFuncSetAttribute(bs::wtile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, WC::kSmem(16) + 1024));
-    CK(cudaFuncSetAttribute(bs::wtile_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    CK(cudaFuncSetAttribute(bs::wtile_kernel<kWtileG>, cudaFuncAttributeMaxDynamicSharedMemorySize, WC::kSmem(16) + 1024));
+    CK(cudaFuncSetAttribute(bs::wtile_kernel<kWtileG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_done = true;
   }
   if (L->n_act > 16) return fail(BITSTACK_E_UNSUPPORTED, "prefill path supports n <= 16 active blocks");
@@ -267,9 +272,9 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   wp.row_tiles = L->row_tiles;
   wp.kc = kc;
   wp.row_tiles_img = rt_img;
-  // two CTAs per SM (TMEM: 2 x 256 columns; registers 2 x 256 x 120; SMEM <= 2 x 77 KB)
+  // persistent: 512 / kTmemCols CTAs per SM (G = 2: two CTAs of 256 TMEM columns each)
   const int wgrid = (int)std::min<int64_t>((int64_t)rt_img * kc, (int64_t)L->sm_count * (512 / WC::kTmemCols));
-  bs::wtile_kernel<2><<<wgrid, WC::kThreads, WC::kSmem(L->n_act), st>>>(wp);
+  bs::wtile_kernel<kWtileG><<<wgrid, WC::kThreads, WC::kSmem(L->n_act), st>>>(wp);
   count_launch();
   CK(cudaGetLastError());
 

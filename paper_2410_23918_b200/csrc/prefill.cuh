@@ -118,7 +118,7 @@ struct WtileCfg {
 // step ahead.  Thread (quadrant q, half h) owns row 32q + lane, columns 32h..32h+31.
 // Sign of column l (0..31) of word w of the F8 layout: bit (l & 3) * 8 + (l >> 2).
 template <int G>
-__global__ void __launch_bounds__(256, 2) wtile_kernel(const WtileParams p) {
+__global__ void __launch_bounds__(256, (2 * G * kPK <= 256) ? 2 : 1) wtile_kernel(const WtileParams p) {
   using C = WtileCfg<G>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* su = smem;                                   // [n] U' tiles (core layout)
@@ -171,19 +171,30 @@ __global__ void __launch_bounds__(256, 2) wtile_kernel(const WtileParams p) {
                  p.u + ((long long)i * p.rows_pad + mt * 128 + jj) * 16 + kk * 8);
     }
     cp_async_commit();
-    // Per-thread constant parts of the addresses (G = 2: one V' piece per thread and step).
-    static_assert(G * 128 == C::kThreads, "one 16-byte V' piece per thread and step");
-    const int v_gl = tid >> 7, v_cc = (tid & 127) >> 1, v_kk = tid & 1;
-    const uint8_t* v_src = reinterpret_cast<const uint8_t*>(p.v) + (long long)v_gl * p.kc * kPK * 32 + v_cc * 32 + v_kk * 16;
-    const uint32_t v_dst = smem_u32(sv) + v_gl * C::kVBytes + ((v_cc >> 3) * 2 + v_kk) * 128 + (v_cc & 7) * 16;
+    // Per-thread constant parts of the addresses: G x 128 16-byte V' pieces per step, VP per thread.
+    constexpr int VP = G * 128 / C::kThreads;
+    static_assert(VP * C::kThreads == G * 128, "whole V' pieces per thread");
     const long long v_blk = (long long)p.kc * kPK * 32;                     // bytes per V' block
+    const uint8_t* v_src[VP];
+    uint32_t v_dst[VP];
+    int v_gl[VP];
+#pragma unroll
+    for (int r = 0; r < VP; ++r) {
+      const int x = tid + r * C::kThreads;
+      const int gl = x >> 7, cc = (x & 127) >> 1, kk = x & 1;
+      v_gl[r] = gl;
+      v_src[r] = reinterpret_cast<const uint8_t*>(p.v) + gl * v_blk + cc * 32 + kk * 16;
+      v_dst[r] = smem_u32(sv) + gl * C::kVBytes + ((cc >> 3) * 2 + kk) * 128 + (cc & 7) * 16;
+    }
     const uint8_t* s_src = reinterpret_cast<const uint8_t*>(p.signs) + row * 16 + h * 4;
     const long long s_blk = (long long)p.nq * p.rows_pad * 16;              // bytes per sign block
     auto load_v = [&](int buf, int c, int gi) {   // V' chunk rows of one step -> SMEM buffer buf
-      if (gi * G + v_gl < p.n)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(v_dst + buf * (G * C::kVBytes)),
-                     "l"(v_src + (gi * G) * v_blk + c * (kPK * 32))
-                     : "memory");
+#pragma unroll
+      for (int r = 0; r < VP; ++r)
+        if (gi * G + v_gl[r] < p.n)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(v_dst[r] + buf * (G * C::kVBytes)),
+                       "l"(v_src[r] + (gi * G) * v_blk + c * (kPK * 32))
+                       : "memory");
       cp_async_commit();
     };
     auto issue = [&](int buf, int tb, int gi) {   // one thread: the step's G MMAs into TMEM buffer tb
