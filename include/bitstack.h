@@ -123,8 +123,12 @@ BITSTACK_API bitstack_status bitstack_load_blocks(bitstack_layer layer, int32_t 
 BITSTACK_API bitstack_status bitstack_set_num_blocks(bitstack_layer layer, int32_t n);
 
 /* y[b, :] = W_hat_n[row_begin:row_end, :] x[b, :]  for b < batch.
- *   x : device [batch, d_in] row-major, dtype F32 | BF16 | F16
- *   y : device [batch, row_end-row_begin] row-major, dtype F32 | BF16, overwritten
+ *   x : [batch, d_in] row-major, dtype F32 | BF16 | F16
+ *   y : [batch, row_end-row_begin] row-major, dtype F32 | BF16, overwritten
+ * x and y may be device or host memory.  Small (<= 1 MiB) pinned host buffers are read /
+ * written in place by the decode kernels (their PCIe traffic is the transfer); other host
+ * buffers are staged through device memory with cudaMemcpyAsync on `stream` (pageable host
+ * memory makes those copies synchronous).
  * x and y must not alias.  batch == 0 is a no-op; n == 0 writes y = 0.
  * Asynchronous on `stream`; argument errors are reported synchronously.
  * Numerics: factors and the activation product V (.) (x/s) are

@@ -44,6 +44,9 @@ struct bitstack_layer_s {
   uint8_t* pf_w = nullptr; // prefill path: W' operand image (transient workspace, grown on demand)
   uint8_t* pf_x = nullptr; // prefill path: X' operand image
   int64_t pf_w_bytes = 0, pf_x_bytes = 0;
+  uint8_t* stage_x = nullptr;  // host-buffer calls: device staging of x / y (grown on demand)
+  uint8_t* stage_y = nullptr;
+  int64_t stage_x_bytes = 0, stage_y_bytes = 0;
   int64_t bytes = 0;
   int64_t block_bytes = 0;
 };
@@ -94,6 +97,17 @@ struct DeviceGuard {
 
 int dsize(bitstack_dtype d) { return d == BITSTACK_F32 ? 4 : 2; }
 bool valid_dtype(int d) { return d == BITSTACK_F32 || d == BITSTACK_BF16 || d == BITSTACK_F16; }
+
+enum MemKind { kMemDevice, kMemPinned, kMemPageable };
+MemKind mem_kind(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return kMemPageable;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return kMemDevice;
+  return a.type == cudaMemoryTypeHost ? kMemPinned : kMemPageable;
+}
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
@@ -431,6 +445,8 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   cudaFree(L->zq);
   cudaFree(L->pf_w);
   cudaFree(L->pf_x);
+  cudaFree(L->stage_x);
+  cudaFree(L->stage_y);
   delete L;
   return BITSTACK_OK;
 }
@@ -568,19 +584,10 @@ bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int3
   return BITSTACK_OK;
 }
 
-bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype x_dtype, void* y,
-                                bitstack_dtype y_dtype, int64_t batch, void* stream) {
-  if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
-  if (batch < 0) return fail(BITSTACK_E_INVALID_ARG, "batch < 0");
-  if (batch == 0) return BITSTACK_OK;
-  if (!x || !y) return fail(BITSTACK_E_INVALID_ARG, "NULL x or y");
-  if (!valid_dtype(x_dtype)) return fail(BITSTACK_E_INVALID_ARG, "bad x dtype");
-  if (y_dtype != BITSTACK_F32 && y_dtype != BITSTACK_BF16)
-    return fail(BITSTACK_E_INVALID_ARG, "y dtype must be F32 or BF16");
-  if (L->n_res == 0 || L->n_act > L->n_res)
-    return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "no resident blocks (load_blocks first)");
-  DeviceGuard guard(L->device);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+// bitstack_matmul with device-accessible x / y (device memory, or pinned host memory read /
+// written in place by the kernels); arguments already validated.
+static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_dtype x_dtype, void* y,
+                                     bitstack_dtype y_dtype, int64_t batch, cudaStream_t st) {
   const int ysz = y_dtype == BITSTACK_F32 ? 4 : 2;
   if (L->n_act == 0) {
     CK(cudaMemsetAsync(y, 0, (size_t)(batch * L->rows_local * ysz), st));
@@ -677,6 +684,66 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
     ps = record_prof(st, false, &slot);
     if (ps) return ps;
   }
+  return BITSTACK_OK;
+}
+
+bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype x_dtype, void* y,
+                                bitstack_dtype y_dtype, int64_t batch, void* stream) {
+  if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
+  if (batch < 0) return fail(BITSTACK_E_INVALID_ARG, "batch < 0");
+  if (batch == 0) return BITSTACK_OK;
+  if (!x || !y) return fail(BITSTACK_E_INVALID_ARG, "NULL x or y");
+  if (!valid_dtype(x_dtype)) return fail(BITSTACK_E_INVALID_ARG, "bad x dtype");
+  if (y_dtype != BITSTACK_F32 && y_dtype != BITSTACK_BF16)
+    return fail(BITSTACK_E_INVALID_ARG, "y dtype must be F32 or BF16");
+  if (L->n_res == 0 || L->n_act > L->n_res)
+    return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "no resident blocks (load_blocks first)");
+  DeviceGuard guard(L->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t xbytes = batch * L->d_in * dsize(x_dtype);
+  const int64_t ybytes = batch * L->rows_local * (y_dtype == BITSTACK_F32 ? 4 : 2);
+  const MemKind kx = mem_kind(x), ky = mem_kind(y);
+  if (kx == kMemDevice && ky == kMemDevice) return matmul_device(L, x, x_dtype, y, y_dtype, batch, st);
+
+  // Host buffers (the e2e path).  Small pinned buffers on the decode paths whose kernels read x
+  // and write y with plain loads / stores (e4m3 decode, SIMT) are used in place: the transfer
+  // is the kernels' own PCIe traffic.  Everything else is staged through device memory with
+  // cudaMemcpyAsync on `stream` (synchronous with respect to pageable host memory).
+  const bool pf = L->kernel == BITSTACK_KERNEL_PREFILL ||
+                  (L->kernel == BITSTACK_KERNEL_AUTO && L->dev_fdt == 1 && L->layout == 1 && L->n_act <= 16 &&
+                   batch >= kPrefillMinBatch);
+  const bool plain_io = !pf && (L->layout == 1 || L->kernel == BITSTACK_KERNEL_SIMT) && L->n_act > 0;
+  const bool small = xbytes <= (1 << 20) && ybytes <= (1 << 20);
+  const void* xd = x;
+  void* yd = y;
+  if (kx != kMemDevice) {
+    if (kx == kMemPinned && plain_io && small) {
+      void* dp = nullptr;
+      CK(cudaHostGetDevicePointer(&dp, const_cast<void*>(x), 0));
+      xd = dp;
+    } else {
+      bitstack_status rs = grow(L, &L->stage_x, &L->stage_x_bytes, xbytes, st);
+      if (rs) return rs;
+      CK(cudaMemcpyAsync(L->stage_x, x, (size_t)xbytes, cudaMemcpyHostToDevice, st));
+      xd = L->stage_x;
+    }
+  }
+  bool copy_back = false;
+  if (ky != kMemDevice) {
+    if (ky == kMemPinned && plain_io && small) {
+      void* dp = nullptr;
+      CK(cudaHostGetDevicePointer(&dp, y, 0));
+      yd = dp;
+    } else {
+      bitstack_status rs = grow(L, &L->stage_y, &L->stage_y_bytes, ybytes, st);
+      if (rs) return rs;
+      yd = L->stage_y;
+      copy_back = true;
+    }
+  }
+  bitstack_status rs = matmul_device(L, xd, x_dtype, yd, y_dtype, batch, st);
+  if (rs) return rs;
+  if (copy_back) CK(cudaMemcpyAsync(y, L->stage_y, (size_t)ybytes, cudaMemcpyDeviceToHost, st));
   return BITSTACK_OK;
 }
 

@@ -278,6 +278,27 @@ def test_row_shards_concatenate_to_full(bs):
     assert O.relative_l2(ys, yf) <= 1e-5
 
 
+# ------------------------------------------------------------------ host buffers (e2e path)
+@pytest.mark.parametrize("batch", [1, 3, 40])
+def test_host_buffers(bs, batch):
+    """bitstack_matmul with host x / y: pinned buffers (read / written in place by the decode
+    kernels, or staged for the prefill path) and pageable ones (staged) give the same y as
+    device buffers."""
+    g, s32, blocks = compress_case(256, 384, 3, "bf16", 81)
+    lay = make_layer(bs, 256, 384, blocks, s32, "bf16")
+    x = torch.from_numpy(make_x(batch, g, 5).astype(np.float32)).to(torch.bfloat16)
+    y_dev = lay.matmul(x.cuda()).cpu()
+    for pinned in (True, False):
+        xh = x.pin_memory() if pinned else x.clone()
+        yh = torch.empty((batch, 256), dtype=torch.float32)
+        yh = yh.pin_memory() if pinned else yh
+        lay.matmul_raw(xh.data_ptr(), bs.BF16, yh.data_ptr(), bs.F32, batch, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(yh.numpy(), y_dev.numpy(), rtol=1e-6, atol=1e-6)
+    ref = oracle_y(blocks, s32, 3, x.float().numpy().astype(np.float64))
+    assert O.relative_l2(y_dev.numpy().astype(np.float64), ref) <= 1e-3
+
+
 # ------------------------------------------------------------------ H8: large-batch path
 @pytest.mark.parametrize("shape", [(384, 640), (200, 296), (1100, 264), (128, 64)])
 def test_prefill_parity_ragged(bs, shape):
