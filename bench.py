@@ -318,7 +318,8 @@ def main():
     kernel_ms = kms / max(nk, 1)
     if w["kind"] == "decode":   # dominant kernel: the zq + decode PDL pair, algorithmic bytes
         dom_units = alg_bytes_per_rank(w, rows, batch, n) / 1e9
-        dom_name = "bs::zq_kernel<%d> + bs::decode_f8_kernel<%d> (PDL pair)" % (min(batch, 4), min(batch, 4))
+        nbk = 1 if batch == 1 else (2 if batch == 2 else 4)
+        dom_name = "bs::zq_kernel<%d> + bs::decode_f8i_kernel<%d,%d> (PDL pair)" % (nbk, nbk, 4 if nbk == 1 else 2)
     else:                       # dominant kernel: the GEMM, 2 B r d_in flops
         dom_units = 2.0 * batch * rows * d_in / 1e12
         dom_name = "bs::prefill_gemm_kernel<BN> (BN = 128 or 256 by wave fill)"

@@ -17,6 +17,7 @@
 #include "../../include/bitstack.h"
 #include "aux_kernels.cuh"
 #include "decode_f8.cuh"
+#include "decode_f8i.cuh"
 #include "decode_tc.cuh"
 #include "prefill.cuh"
 
@@ -138,6 +139,13 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
 // e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
 constexpr int64_t kPrefillMinBatch = 16;   // AUTO: restored-tile GEMM path from this batch on
 
+// Decode kernel choice: the per-warpgroup-issuer kernel (decode_f8i.cuh) by default;
+// BS_DECODE_WG=1 selects the previous self-issuing warpgroup kernel (A/B measurements).
+bool decode_issuer() {
+  static const bool v = [] { const char* e = getenv("BS_DECODE_WG"); return !(e && e[0] == '1'); }();
+  return v;
+}
+
 template <int NB> struct F8Geom;   // R: row tiles per CTA
 template <> struct F8Geom<1> { static constexpr int R = 4; };
 template <> struct F8Geom<2> { static constexpr int R = 2; };
@@ -147,12 +155,16 @@ template <int NB>
 bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_in, int grid, cudaStream_t st) {
   using G = F8Geom<NB>;
   using C = bs::DecodeF8Cfg<NB, G::R>;
+  using CI = bs::DecodeF8ICfg<NB, G::R>;
   static bool attr_done = false;
   if (!attr_done) {
     CK(cudaFuncSetAttribute(bs::decode_f8_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             C::kSmemBytes));
+    CK(cudaFuncSetAttribute(bs::decode_f8i_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            CI::kSmemBytes));
     attr_done = true;
   }
+  const bool iss = decode_issuer();
 
 
 
@@ -187,15 +199,16 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
   prm.status = L->status;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(C::kThreads);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.blockDim = dim3(iss ? CI::kThreads : C::kThreads);
+  cfg.dynamicSmemBytes = iss ? CI::kSmemBytes : C::kSmemBytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8_kernel<NB, G::R>, prm));
+  if (iss) CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_kernel<NB, G::R>, prm));
+  else CK(cudaLaunchKernelEx(&cfg, bs::decode_f8_kernel<NB, G::R>, prm));
   count_launch();
   return BITSTACK_OK;
 }
