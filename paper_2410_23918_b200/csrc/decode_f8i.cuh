@@ -41,7 +41,7 @@ struct DecodeF8ICfg {
   static_assert(N <= 256 && N % 16 == 0, "invalid MMA N");
   static_assert(kAccCol + R * N <= kTmemCols, "TMEM overflow");
   static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
-  static_assert(3 * R <= 15, "named barriers 1..3R");
+  static_assert(2 * R <= 15, "named barriers 1..2R");
   static_assert(5 * R + 1 <= 32, "warps");
 };
 
@@ -71,7 +71,17 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
   const int tiles_left = p.row_tiles - g * R;
   const int Rg = tiles_left < R ? tiles_left : R;
   const int row0 = g * R * kTileRows;
-  // named barriers of warpgroup w: go = 1 + 3w, tile-ready (parity) = 2 + 3w + parity
+  // named barriers of warpgroup w: go = 1 + 2w (issuer arrives, expanders sync), tile-ready =
+  // 2 + 2w (expanders arrive, issuer syncs).  Single-buffered is race-free: the issuer
+  // releases unit k+1 only after syncing on unit k's tile, and the expanders arrive on unit
+  // k+1's tile only after that release.
+#ifdef BS_DECODE_TRACE
+  long long* trace = (p.dbg_acc && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
+  const long long tstart = clock64();
+#define BS_ITRACE(k_, c_) do { if (trace && lane == 0) trace[(k_) * 16 + (c_)] = clock64() - tstart; } while (0)
+#else
+#define BS_ITRACE(k_, c_) do { } while (0)
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -117,17 +127,36 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
       }
     }
   } else if (warp % 5 == 4) {
-    // ================= issuer of warpgroup w: the tile's 4 MMAs per unit =================
+    // ================= issuer of warpgroup t =================
+    // Polls the stage / slot mbarriers of unit k+1 while the expanders work on unit k, and
+    // releases them for unit k+1 (bar.arrive "go") as soon as unit k's tile is in TMEM --
+    // before issuing unit k's MMAs, so expansion of k+1 overlaps MMA issue of k.
     const int t = warp / 5;
     if (t < Rg) {
       constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
       const uint64_t bdesc_s0 = smem_desc_kmajor(smem_u32(smem + C::kOffZ), C::LBO, C::SBO);
       const uint32_t d_acc = tbase + C::kAccCol + (uint32_t)(t * N);
+      const int bar_go = 1 + 2 * t, bar_tile = 2 + 2 * t;
       int s = 0, slot = 0, q = q_start;
+      uint32_t ph = 0, sph = 0;
+      int sn = 0, slotn = 0;                 // stage / slot of unit k+1
+      uint32_t phn = 0, sphn = 0;
+      mbar_wait(&full[0], 0);
+      mbar_wait(&a_empty[t * NSLOT], 1);
+      asm volatile("bar.arrive %0, 160;" ::"r"(bar_go) : "memory");
       for (int k = 0; k < nunits; ++k) {
         const bool first = (k == 0) || (q == 0);
         const bool last = (k == nunits - 1) || (q == p.nq - 1);
-        asm volatile("bar.sync %0, 160;" ::"r"(2 + 3 * t + (k & 1)) : "memory");   // tile in TMEM
+        if (++sn == STAGES) { sn = 0; phn ^= 1; }
+        if (++slotn == NSLOT) { slotn = 0; sphn ^= 1; }
+        if (k + 1 < nunits) {
+          mbar_wait(&full[sn], phn);
+          mbar_wait(&a_empty[t * NSLOT + slotn], sphn ^ 1);
+        }
+        if (t == 3) BS_ITRACE(k, 8);
+        asm volatile("bar.sync %0, 160;" ::"r"(bar_tile) : "memory");   // unit k's tile in TMEM
+        if (k + 1 < nunits) asm volatile("bar.arrive %0, 160;" ::"r"(bar_go) : "memory");
+        if (t == 3) BS_ITRACE(k, 9);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t bdesc0 = bdesc_s0 + (uint64_t)((s * C::kStageBytes) >> 4);
@@ -141,37 +170,36 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
           if (last) mma_commit(&acc_full[t]);
         }
         __syncwarp();
-        if (++slot == NSLOT) slot = 0;
-        if (++s == STAGES) s = 0;
+        if (t == 3) BS_ITRACE(k, 10);
+        s = sn; ph = phn;
+        slot = slotn; sph = sphn;
         if (++q == p.nq) q = 0;
       }
+      (void)ph;
+      (void)sph;
     }
   } else {
     // ================= expander warps of warpgroup wg (TMEM lane quadrant = warp % 4) =================
     const int wg = warp / 5;
     const int qd = warp & 3;
-    const bool waiter = (warp % 5) == 0;   // polls the stage / slot mbarriers one unit ahead
     const int t = wg;                      // this warpgroup's row tile
     const bool active = t < Rg;
     const int row_in_tile = qd * 32 + lane;
     const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
     const uint32_t d_acc = tbase + C::kAccCol + (uint32_t)(t * N);
-    const int bar_go = 1 + 3 * wg;
+    const int bar_go = 1 + 2 * wg, bar_tile = 2 + 2 * wg;
     float yacc[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) yacc[b] = 0.f;
     int s = 0, slot = 0, i = i_start, q = q_start;
-    uint32_t ph = 0, sph = 0, acc_ph = 0;
+    uint32_t acc_ph = 0;
     int E = 0;
     bool have_e = false;
-    auto waits = [&](int s_, uint32_t ph_, int slot_, uint32_t sph_) {
-      mbar_wait(&full[s_], ph_);
-      mbar_wait(&a_empty[wg * NSLOT + slot_], sph_ ^ 1);
-    };
     for (int k = 0; active && k < nunits; ++k) {
       const bool last = (k == nunits - 1) || (q == p.nq - 1);
-      if (waiter && k == 0) waits(s, ph, slot, sph);
-      asm volatile("bar.sync %0, 128;" ::"r"(bar_go) : "memory");
+      if (warp == 15) BS_ITRACE(k, 0);
+      asm volatile("bar.sync %0, 160;" ::"r"(bar_go) : "memory");   // stage full, slot free
+      if (warp == 15) BS_ITRACE(k, 1);
       tc_fence_after();
       const uint8_t* st = smem + s * C::kStageBytes;
       // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit
@@ -195,14 +223,16 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
         expand_e4m3(sw.w, e8, o + 24);
         tmem_st32(tbase + (uint32_t)(C::kACols * (t * NSLOT + slot)) + lane_base, o);
       }
+      if (warp == 15) BS_ITRACE(k, 2);
       tmem_st_wait();
+      if (warp == 15) BS_ITRACE(k, 3);
       tc_fence_before();
-      asm volatile("bar.arrive %0, 160;" ::"r"(2 + 3 * wg + (k & 1)) : "memory");   // quarter in TMEM
-      if (++slot == NSLOT) { slot = 0; sph ^= 1; }
-      if (++s == STAGES) { s = 0; ph ^= 1; }
+      asm volatile("bar.arrive %0, 160;" ::"r"(bar_tile) : "memory");   // quarter in TMEM
+      if (++slot == NSLOT) slot = 0;
+      if (++s == STAGES) s = 0;
       const int ci = i;
       if (++q == p.nq) { q = 0; ++i; }
-      if (waiter && k + 1 < nunits) waits(s, ph, slot, sph);
+      if (warp == 15) BS_ITRACE(k, 4);
 
       if (last) {
         // ---- epilogue for block ci: y += 2^-E sum_r U'_ci[row, r] (T_d0 + T_d1 + T_d2)[row, r]
@@ -264,6 +294,7 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
     }
   }
 
+#undef BS_ITRACE
   // ---- teardown + last-CTA-of-group finalisation
   __threadfence();
   tc_fence_before();

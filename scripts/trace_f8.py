@@ -26,6 +26,11 @@ cta = cta[cta[:, 0] != 0]
 if len(cta):
   t0 = cta[:, 0].min()
   print('CTAs', len(cta), 'entry spread us', (cta[:, 0].max() - t0) / 1e3, 'exit (wg3 done) min/med/max us', (cta[:, 1].min() - t0) / 1e3, (np.median(cta[:, 1]) - t0) / 1e3, (cta[:, 1].max() - t0) / 1e3, 'units min/max', cta[:, 2].min(), cta[:, 2].max())
+if os.environ.get("BS_DECODE_WG") != "1":
+    print("unit | warpgroup 3 waiter warp: before_go go_done sttm_issued st_done loop_end | issuer: before_sync synced issued")
+    for k in range(28):
+        print(k, *[f"{x:6d}" for x in t[k, :5]], "|", *[f"{x:6d}" for x in t[k, 8:11]])
+    sys.exit(0)
 print("nonzero", int((t != 0).sum()), "max", int(t.max()), "min", int(t.min()))
 nu = int((t[:, 6] != 0).sum())
 print("units traced:", nu)
