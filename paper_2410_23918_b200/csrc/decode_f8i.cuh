@@ -79,6 +79,12 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
   long long* trace = (p.dbg_acc && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
   const long long tstart = clock64();
 #define BS_ITRACE(k_, c_) do { if (trace && lane == 0) trace[(k_) * 16 + (c_)] = clock64() - tstart; } while (0)
+  if (p.dbg_acc && threadIdx.x == 0) {   // every CTA's entry %globaltimer (ns), unit count
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x] = (long long)gt;
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x + 2] = nunits;
+  }
 #else
 #define BS_ITRACE(k_, c_) do { } while (0)
 #endif
@@ -295,6 +301,13 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
   }
 
 #undef BS_ITRACE
+#ifdef BS_DECODE_TRACE
+  if (p.dbg_acc && threadIdx.x == 0) {   // exit of the main phase (before the teardown barrier)
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x + 1] = (long long)gt;
+  }
+#endif
   // ---- teardown + last-CTA-of-group finalisation
   __threadfence();
   tc_fence_before();
