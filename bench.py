@@ -347,6 +347,9 @@ def main():
         # the same public calls (H2D copy, bitstack_matmul, D2H copy) captured into a CUDA
         # graph, as a serving loop would issue them; every step still moves x in and y out
         gs = min(ke, copies * max(1, 64 // copies))
+        for lay in layers:   # first host-buffer call of each layer outside capture (staging allocation)
+            lay.matmul_raw(x_h.data_ptr(), pkg.BF16, y_h.data_ptr(), pkg.F32, batch, sh)
+        torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)

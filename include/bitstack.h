@@ -128,7 +128,8 @@ BITSTACK_API bitstack_status bitstack_set_num_blocks(bitstack_layer layer, int32
  * x and y may be device or host memory.  Small (<= 1 MiB) pinned host buffers are read /
  * written in place by the decode kernels (their PCIe traffic is the transfer); other host
  * buffers are staged through device memory with cudaMemcpyAsync on `stream` (pageable host
- * memory makes those copies synchronous).
+ * memory makes those copies synchronous).  Staging and prefill workspaces are allocated on
+ * the first call that needs them (which therefore must not be under CUDA-graph capture).
  * x and y must not alias.  batch == 0 is a no-op; n == 0 writes y = 0.
  * Asynchronous on `stream`; argument errors are reported synchronously.
  * Numerics: factors and the activation product V (.) (x/s) are
