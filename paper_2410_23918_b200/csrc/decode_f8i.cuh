@@ -197,44 +197,48 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
     float yacc[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) yacc[b] = 0.f;
-    int s = 0, slot = 0, i = i_start, q = q_start;
+    int s = 0, i = i_start, q = q_start;
     uint32_t acc_ph = 0;
-    int E = 0;
-    bool have_e = false;
+    int E = kZqSentinel;                   // set by the CTA's first non-empty unit
+    // per-thread constant addresses: this row's 16-byte sign vector in stage 0, the two A slots
+    const uint32_t sw_addr0 = smem_u32(smem) + (uint32_t)((t * kTileRows + row_in_tile) * 16);
+    const uint32_t meta_addr0 = smem_u32(smem) + (uint32_t)C::kOffMeta;
+    uint32_t a_addr = tbase + (uint32_t)(C::kACols * t * NSLOT) + lane_base;
+    const uint32_t a_flip = (uint32_t)C::kACols;   // slot 0 <-> slot 1 (NSLOT = 2)
+    static_assert(NSLOT == 2, "slot toggle");
     for (int k = 0; active && k < nunits; ++k) {
       const bool last = (k == nunits - 1) || (q == p.nq - 1);
       if (warp == 15) BS_ITRACE(k, 0);
       asm volatile("bar.sync %0, 160;" ::"r"(bar_go) : "memory");   // stage full, slot free
       if (warp == 15) BS_ITRACE(k, 1);
       tc_fence_after();
-      const uint8_t* st = smem + s * C::kStageBytes;
-      // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit
-      const int e_u = *reinterpret_cast<const int*>(st + C::kOffMeta);
-      int a_exp = 0;
-      if (e_u != kZqSentinel) {
-        if (!have_e) { E = e_u; have_e = true; }
-        a_exp = E - e_u;
-        if (a_exp < -6 || a_exp > 8) {  // |x/s| range across this CTA's units beyond e4m3 A range
-          if (lane == 0 && p.status) atomicOr(p.status, 1);
-          a_exp = a_exp < -6 ? -6 : 8;
-        }
-      }
+      const uint32_t so = (uint32_t)(s * C::kStageBytes);
+      uint4 sw;
+      int e_u;
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(sw.x), "=r"(sw.y), "=r"(sw.z), "=r"(sw.w)
+                   : "r"(sw_addr0 + so));
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(e_u) : "r"(meta_addr0 + so));
+      // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit; E = e_u of
+      // the CTA's first non-empty unit (the same in every warpgroup)
+      if (E == kZqSentinel) E = e_u;
+      const int a_raw = (e_u == kZqSentinel) ? 0 : E - e_u;
+      const int a_exp = min(max(a_raw, -6), 8);
+      if (a_exp != a_raw && lane == 0 && p.status) atomicOr(p.status, 1);   // beyond the e4m3 A range
       const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
-      const uint4 sw = reinterpret_cast<const uint4*>(st)[t * kTileRows + row_in_tile];
       {
         uint32_t o[32];
         expand_e4m3(sw.x, e8, o);
         expand_e4m3(sw.y, e8, o + 8);
         expand_e4m3(sw.z, e8, o + 16);
         expand_e4m3(sw.w, e8, o + 24);
-        tmem_st32(tbase + (uint32_t)(C::kACols * (t * NSLOT + slot)) + lane_base, o);
+        tmem_st32(a_addr, o);
       }
       if (warp == 15) BS_ITRACE(k, 2);
       tmem_st_wait();
       if (warp == 15) BS_ITRACE(k, 3);
       tc_fence_before();
       asm volatile("bar.arrive %0, 160;" ::"r"(bar_tile) : "memory");   // quarter in TMEM
-      if (++slot == NSLOT) slot = 0;
+      a_addr ^= a_flip;
       if (++s == STAGES) s = 0;
       const int ci = i;
       if (++q == p.nq) { q = 0; ++i; }
