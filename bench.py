@@ -316,15 +316,17 @@ def main():
         total_units = float(tb.item())
     value = total_units / (ms_step * 1e-3)
     kernel_ms = kms / max(nk, 1)
-    if w["kind"] == "decode":   # dominant kernel: the zq + decode PDL pair, algorithmic bytes
+    decode_path = batch < 16   # bitstack_matmul AUTO: prefill path from 16 tokens (bf16 factors)
+    if decode_path:   # dominant kernel: the zq + decode PDL pair(s), algorithmic bytes
         dom_units = alg_bytes_per_rank(w, rows, batch, n) / 1e9
         nbk = 1 if batch == 1 else (2 if batch == 2 else 4)
-        dom_name = "bs::zq_kernel<%d> + bs::decode_f8i_kernel<%d,%d> (PDL pair)" % (nbk, nbk, 4 if nbk == 1 else 2)
-    else:                       # dominant kernel: the GEMM, 2 B r d_in flops
+        dom_name = "bs::zq_kernel<%d> + bs::decode_f8i_kernel<%d,%d> (PDL pair%s)" % (
+            nbk, nbk, 4 if nbk == 1 else 2, "" if batch <= 4 else ", %d launches per call" % ((batch + 3) // 4))
+    else:             # dominant kernel: the GEMM, 2 B r d_in flops
         dom_units = 2.0 * batch * rows * d_in / 1e12
         dom_name = "bs::prefill_gemm_kernel<BN> (BN = 128 or 256 by wave fill)"
     achieved = dom_units / (kernel_ms * 1e-3)
-    peak, peak_src = peaks(w["kind"])
+    peak, peak_src = peaks("decode" if decode_path else "prefill")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -429,13 +431,13 @@ def main():
                        "l2": f"inputs larger than L2: rotation over {copies} layer copies "
                              f"({copies * per_layer / 2 ** 20:.0f} MiB/rank > 4x126 MiB)",
                        "timing": "CUDA-graph replay" if use_graph else "eager launches"},
-            "roofline": {"bound": "hbm" if w["kind"] == "decode" else "tensor", "achieved": achieved,
-                         "peak": peak, "unit": unit_name(w),
+            "roofline": {"bound": "hbm" if decode_path else "tensor", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s" if decode_path else "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": dom_name, "kernel_us": kernel_ms * 1e3,
                          "kernel_launches_timed": nk,
-                         ("bytes_per_launch" if w["kind"] == "decode" else "flops_per_launch"):
-                             dom_units * (1e9 if w["kind"] == "decode" else 1e12)},
+                         ("bytes_per_launch" if decode_path else "flops_per_launch"):
+                             dom_units * (1e9 if decode_path else 1e12)},
             "clocks": clocks,
             "e2e": e2e,
             "gpu_launches": int(launches),
