@@ -278,6 +278,23 @@ def test_row_shards_concatenate_to_full(bs):
     assert O.relative_l2(ys, yf) <= 1e-5
 
 
+# ------------------------------------------------------------------ Zq edge cases
+def test_zero_activation_segments(bs):
+    """All-zero 128-column segments of x give all-zero Zq units (sentinel exponent): the
+    decode kernel must skip them when choosing its scale reference and still match the
+    oracle; an all-zero x gives y == 0 exactly."""
+    g, s32, blocks = compress_case(512, 640, 4, "bf16", 91)
+    lay = make_layer(bs, 512, 640, blocks, s32, "bf16")
+    for batch in (1, 2, 4):
+        x = make_x(batch, g, 11 + batch)
+        x[:, :256] = 0.0            # first two subchunks empty: the CTAs' first units are sentinels
+        x[:, 384:512] = 0.0
+        y, xr = gpu_y(lay, x, x_dtype=torch.bfloat16)
+        assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 1e-3, batch
+    y, _ = gpu_y(lay, np.zeros((3, 640)), x_dtype=torch.bfloat16)
+    assert not np.any(y)
+
+
 # ------------------------------------------------------------------ host buffers (e2e path)
 @pytest.mark.parametrize("batch", [1, 3, 40])
 def test_host_buffers(bs, batch):
