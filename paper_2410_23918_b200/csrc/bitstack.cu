@@ -234,14 +234,18 @@ bitstack_status record_prof(cudaStream_t st, bool begin, int* slot) {
 #endif
 constexpr int kWtileG = BS_WTILE_G;   // blocks per wtile MMA step (2: 2 CTAs/SM; 4: 1 CTA/SM)
 
-// GEMM token-tile width: 256 (higher operand reuse) unless 128 fills the SMs' last wave
-// clearly better (persistent grid of sm_count CTAs; tiles = row_tiles/2 x ceil(B/BN)).
-int prefill_bn(int64_t m2, int64_t batch, int sms) {
-  auto eff = [&](int bn) {
-    const int64_t t = m2 * ((batch + bn - 1) / bn);
-    return (double)t / (double)(((t + sms - 1) / sms) * sms);
-  };
-  return eff(128) > eff(256) + 0.05 ? 128 : 256;
+// GEMM tile shape: BN tokens (256, or 128 for small batches) x 128 MH rows.  MH = 2 reuses each
+// X' stage for two MMAs (higher operand reuse, one accumulator set); MH = 1 doubles the tile
+// count (better wave fill on the persistent grid) and double-buffers the accumulators so the
+// epilogue overlaps the next tile.  Measured (C3, B = 2048): up/gate [14336, 4096] MH=1 207 us
+// vs MH=2 231 us; down [4096, 14336] MH=2 182 us vs MH=1 203 us -- modelled as rounds of
+// ceil(tiles / SMs) x per-tile cost (MH=1 tiles cost ~0.56 of MH=2 tiles).
+void prefill_shape(int64_t row_tiles, int64_t batch, int sms, int* bn, int* mh) {
+  *bn = batch <= 128 ? 128 : 256;
+  const int64_t nt = (batch + *bn - 1) / *bn;
+  const int64_t t2 = (row_tiles + 1) / 2 * nt, t1 = row_tiles * nt;
+  const double c2 = (double)((t2 + sms - 1) / sms) * 2.0, c1 = (double)((t1 + sms - 1) / sms) * 1.12;
+  *mh = c1 < c2 ? 1 : 2;
 }
 
 bitstack_status grow(bitstack_layer L, uint8_t** buf, int64_t* have, int64_t need, cudaStream_t st) {
@@ -259,14 +263,14 @@ bitstack_status grow(bitstack_layer L, uint8_t** buf, int64_t* have, int64_t nee
 }
 
 // Large-batch path (prefill.cuh): X' image, W' image, GEMM -- three launches on `st`.
-template <int BN>
+template <int BN, int MH>
 bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
                                cudaStream_t st) {
-  using GC = bs::GemmCfg<BN>;
+  using GC = bs::GemmCfg<BN, MH>;
   using WC = bs::WtileCfg<kWtileG>;
   static bool attr_done = false;
   if (!attr_done) {
-    CK(cudaFuncSetAttribute(bs::prefill_gemm_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::kSmemBytes));
+    CK(cudaFuncSetAttribute(bs::prefill_gemm_kernel<BN, MH>, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::kSmemBytes));
     CK(cudaFuncSetAttribute(bs::wtile_kernel<kWtileG>, cudaFuncAttributeMaxDynamicSharedMemorySize, WC::kSmem(16) + 1024));
     CK(cudaFuncSetAttribute(bs::wtile_kernel<kWtileG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_done = true;
@@ -314,14 +318,14 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   gp.batch = (int)batch;
   gp.rows_local = (int)L->rows_local;
   gp.row_tiles = L->row_tiles;
-  gp.m2_count = rt_img / 2;
+  gp.m2_count = (L->row_tiles + MH - 1) / MH;
   gp.nt_count = nt;
   gp.kc = kc;
   const int tiles = gp.m2_count * nt;
   int slot = -1;   // measurement hooks bracket the dominant kernel of the path: the GEMM
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
-  bs::prefill_gemm_kernel<BN><<<std::min(tiles, L->sm_count), GC::kThreads, GC::kSmemBytes, st>>>(gp);
+  bs::prefill_gemm_kernel<BN, MH><<<std::min(tiles, L->sm_count), GC::kThreads, GC::kSmemBytes, st>>>(gp);
   count_launch();
   CK(cudaGetLastError());
   return record_prof(st, false, &slot);
@@ -329,9 +333,24 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
 
 bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
                                cudaStream_t st) {
-  const int64_t m2 = (L->row_tiles + 1) / 2;
-  return prefill_bn(m2, batch, L->sm_count) == 128 ? launch_prefill<128>(L, x, xdt, y, ydt, batch, st)
-                                                   : launch_prefill<256>(L, x, xdt, y, ydt, batch, st);
+  int bn = 256, mh = 2;
+  prefill_shape(L->row_tiles, batch, L->sm_count, &bn, &mh);
+  static const int bn_env = [] { const char* e = getenv("BS_PREFILL_BN"); return e ? atoi(e) : 0; }();
+  static const int mh_env = [] { const char* e = getenv("BS_PREFILL_MH"); return e ? atoi(e) : 0; }();
+  if (bn_env) bn = bn_env;   // A/B overrides (scripts/exp_bn.sh)
+  if (mh_env) mh = mh_env;
+  if (mh == 1) {
+    switch (bn) {
+      case 128: return launch_prefill<128, 1>(L, x, xdt, y, ydt, batch, st);
+      default: return launch_prefill<256, 1>(L, x, xdt, y, ydt, batch, st);
+    }
+  }
+  switch (bn) {
+    case 128: return launch_prefill<128, 2>(L, x, xdt, y, ydt, batch, st);
+    case 192: return launch_prefill<192, 2>(L, x, xdt, y, ydt, batch, st);
+    case 224: return launch_prefill<224, 2>(L, x, xdt, y, ydt, batch, st);
+    default: return launch_prefill<256, 2>(L, x, xdt, y, ydt, batch, st);
+  }
 }
 
 template <int NDIG>

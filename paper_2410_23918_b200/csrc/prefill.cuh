@@ -302,24 +302,28 @@ struct GemmParams {
   void* y;                // [batch][y_stride]
   int y_dtype;            // 0 f32, 1 bf16
   long long y_stride;
-  int batch, rows_local, row_tiles, m2_count, nt_count, kc;
+  int batch, rows_local, row_tiles, m2_count, nt_count, kc;   // m2_count: row-tile groups of MH
 };
 
-template <int BN>
+template <int BN, int MH>
 struct GemmCfg {
   static constexpr int kThreads = 192;                 // producer, MMA, 4 epilogue warps
   static constexpr int kBBytes = BN * kPK * 2;
-  static constexpr int kStageBytes = 2 * kImgTileA + kBBytes;
+  static constexpr int kOffB = MH * kImgTileA;         // stage: MH A tiles (128 rows each), then B
+  static constexpr int kStageBytes = kOffB + kBBytes;
   static constexpr int STAGES = (220 * 1024) / kStageBytes;
-  static constexpr int NACC = 512 / (2 * BN);          // accumulator sets (256 x BN fp32 each)
+  static constexpr int NACC = 512 / (MH * BN);         // accumulator sets (128 MH x BN fp32 each)
   static constexpr int kSmemBytes = STAGES * kStageBytes + 256;
   static_assert(BN % 32 == 0 && BN <= 256, "BN");
+  static_assert(MH == 1 || MH == 2, "MH");
   static_assert(NACC >= 1, "TMEM");
 };
 
-template <int BN>
+// Output tile = (128 MH rows) x BN tokens; tile t -> (row tile group mt = t / nt_count,
+// token tile nt = t % nt_count); the MH row tiles share each B (X') stage.
+template <int BN, int MH>
 __global__ void __launch_bounds__(192, 1) prefill_gemm_kernel(const GemmParams p) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, MH>;
   constexpr int STAGES = C::STAGES, NACC = C::NACC;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(192, 1) prefill_gemm_kernel(const GemmParams p
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = p.m2_count * p.nt_count;
+  auto halves = [&](int mt) { const int left = p.row_tiles - MH * mt; return left < MH ? left : MH; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -354,18 +359,17 @@ __global__ void __launch_bounds__(192, 1) prefill_gemm_kernel(const GemmParams p
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < T; t += gridDim.x) {
-        const int m2 = t / p.nt_count, nt = t % p.nt_count;
-        const bool h1 = 2 * m2 + 1 < p.row_tiles;
-        const uint32_t bytes = (h1 ? 2 : 1) * kImgTileA + C::kBBytes;
+        const int mt = t / p.nt_count, nt = t % p.nt_count;
+        const int nh = halves(mt);
+        const uint32_t bytes = nh * kImgTileA + C::kBBytes;
         for (int c = 0; c < p.kc; ++c) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * C::kStageBytes;
           mbar_arrive_expect_tx(&full[s], bytes);
-          bulk_g2s(st, p.a_img + ((long long)(2 * m2) * p.kc + c) * kImgTileA, kImgTileA, &full[s], pol_a);
-          if (h1)
-            bulk_g2s(st + kImgTileA, p.a_img + ((long long)(2 * m2 + 1) * p.kc + c) * kImgTileA, kImgTileA,
+          for (int h = 0; h < nh; ++h)
+            bulk_g2s(st + h * kImgTileA, p.a_img + ((long long)(MH * mt + h) * p.kc + c) * kImgTileA, kImgTileA,
                      &full[s], pol_a);
-          bulk_g2s(st + 2 * kImgTileA, p.b_img + ((long long)nt * p.kc + c) * C::kBBytes, C::kBBytes, &full[s], pol_b);
+          bulk_g2s(st + C::kOffB, p.b_img + ((long long)nt * p.kc + c) * C::kBBytes, C::kBBytes, &full[s], pol_b);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -375,12 +379,11 @@ __global__ void __launch_bounds__(192, 1) prefill_gemm_kernel(const GemmParams p
     int s = 0, lt = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x, ++lt) {
-      const int m2 = t / p.nt_count;
-      const bool h1 = 2 * m2 + 1 < p.row_tiles;
+      const int nh = halves(t / p.nt_count);
       const int ab = lt % NACC;
       mbar_wait(&acc_empty[ab], (uint32_t)(((lt / NACC) & 1) ^ 1));
       tc_fence_after();
-      const uint32_t d0 = tbase + (uint32_t)(ab * 2 * BN);
+      const uint32_t d0 = tbase + (uint32_t)(ab * MH * BN);
       for (int c = 0; c < p.kc; ++c) {
         mbar_wait(&full[s], ph);
         tc_fence_after();
@@ -388,10 +391,12 @@ __global__ void __launch_bounds__(192, 1) prefill_gemm_kernel(const GemmParams p
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kPK / 16; ++kk) {
-            const uint64_t bd = smem_desc_kmajor(st + 2 * kImgTileA + kk * 256, 128, 1024);
-            mma_f16_ss(d0, smem_desc_kmajor(st + kk * 256, 128, 1024), bd, idesc, (c | kk) ? 1u : 0u);
-            if (h1) mma_f16_ss(d0 + BN, smem_desc_kmajor(st + kImgTileA + kk * 256, 128, 1024), bd, idesc,
-                               (c | kk) ? 1u : 0u);
+            const uint64_t bd = smem_desc_kmajor(st + C::kOffB + kk * 256, 128, 1024);
+#pragma unroll
+            for (int h = 0; h < MH; ++h)
+              if (h < nh)
+                mma_f16_ss(d0 + (uint32_t)(h * BN), smem_desc_kmajor(st + h * kImgTileA + kk * 256, 128, 1024), bd,
+                           idesc, (c | kk) ? 1u : 0u);
           }
           mma_commit(&empty[s]);
           if (c == p.kc - 1) mma_commit(&acc_full[ab]);
@@ -405,16 +410,16 @@ __global__ void __launch_bounds__(192, 1) prefill_gemm_kernel(const GemmParams p
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     int lt = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x, ++lt) {
-      const int m2 = t / p.nt_count, nt = t % p.nt_count;
-      const bool h1 = 2 * m2 + 1 < p.row_tiles;
+      const int mt = t / p.nt_count, nt = t % p.nt_count;
+      const int nh = halves(mt);
       const int ab = lt % NACC;
       mbar_wait(&acc_full[ab], (uint32_t)((lt / NACC) & 1));
       tc_fence_after();
-      for (int hh = 0; hh < (h1 ? 2 : 1); ++hh) {
-        const int j = m2 * 256 + hh * 128 + q * 32 + lane;
+      for (int hh = 0; hh < nh; ++hh) {
+        const int j = (MH * mt + hh) * 128 + q * 32 + lane;
         for (int cc = 0; cc < BN / 32; ++cc) {
           uint32_t v[32];
-          tmem_ld32(tbase + lane_base + (uint32_t)(ab * 2 * BN + hh * BN + cc * 32), v);
+          tmem_ld32(tbase + lane_base + (uint32_t)(ab * MH * BN + hh * BN + cc * 32), v);
           tmem_ld_wait();
           const int b0 = nt * BN + cc * 32;
           if (j < p.rows_local) {
