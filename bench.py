@@ -27,7 +27,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synthetic import CONFIGS, channel_gains, make_random_blocks, make_x, seed_for  # noqa: E402
+from synthetic import (C4_LEVELS, CONFIGS, LLAMA31_8B_SHAPES, average_levels, channel_gains,  # noqa: E402
+                       make_random_blocks, make_x, seed_for)
 
 L2_BYTES = 126 * 2 ** 20
 WORKLOADS = {
@@ -37,6 +38,10 @@ WORKLOADS = {
                label="c5: Llama-3.1-70B down_proj 8192x28672, n=12 blocks, k=16, bf16 factors, decode"),
     "c3_up": dict(CONFIGS["c3_up"], kind="prefill",
                   label="c3: Llama-3.1-8B up/gate_proj 14336x4096, n=8 blocks, k=16, bf16 factors, prefill 2048 tokens"),
+    "c4": dict(d_out=4096, d_in=4096, n=4, k=16, batch=1, factor_dtype="bf16", kind="stack",
+               label="c4: full Llama-3.1-8B linear stack (32 layers x q,k,v,o,gate,up,down = 224 matrices), "
+                     "5541 MiB budget (average level 3.88: 3-4 blocks per matrix, seeded Average layering), "
+                     "decode, one token-step = 224 bitstack_matmul calls"),
     "c3_down": dict(CONFIGS["c3_down"], kind="prefill",
                     label="c3: Llama-3.1-8B down_proj 4096x14336, n=8 blocks, k=16, bf16 factors, prefill 2048 tokens"),
 }
@@ -165,6 +170,183 @@ def unit_name(w):
     return "GB/s" if w["kind"] == "decode" else "TFLOP/s"
 
 
+
+def run_stack(args, w, world, rank, local_rank):
+    """Config C4: every linear of Llama-3.1-8B held as BitStack blocks at the
+    paper's 5541 MiB memory point; one step = one decode token through all 224 matmuls
+    (32 layers x 7), captured as one CUDA graph.  Row shards at N > 1 (outputs all-gathered)."""
+    level = C4_LEVELS[5541]
+    names = list(LLAMA31_8B_SHAPES)
+    n_of = average_levels(32 * len(names), level, seed_for(4, 0, "blocks")).reshape(32, len(names))
+    batch = args.batch or 1
+    def oracle_stack_sample(reps):
+        """The oracle on a bounded sample: 64 rows of each of layer 0's 7 matrices -> GB/s."""
+        tot_bytes, tot_s = 0.0, 0.0
+        for m, name in enumerate(names):
+            d_out, d_in = LLAMA31_8B_SHAPES[name]
+            ww = dict(d_out=d_out, d_in=d_in, k=16, kind="decode")
+            dt, by = oracle_sample_time(ww, int(n_of[0, m]), batch, 64, reps, 1, seed_for(4, m, "blocks"))
+            tot_bytes += by
+            tot_s += dt
+        return tot_bytes / tot_s, tot_s
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        val, tot_s = oracle_stack_sample(max(1, args.steps // 100))
+        print(json.dumps({
+            "impl": "reference", "metric": metric_name(dict(kind="decode")), "value": val, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (stored-form random blocks, synthetic/ recipe)",
+            "config": {"workload": w["label"], "batch": batch, "parallelism": "cpu", "sample_rows": 64},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": "dense oracle (fp64 numpy) for 64 rows of each of layer 0's 7 matrices"},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2410_23918_b200 import build as B
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2410_23918_b200 as pkg
+    pkg.load_library()
+    # one set of stored-form blocks per matrix type (4 blocks: the maximum level), loaded into
+    # 32 independent handles each (every handle owns its device copy: 3.7 GB of weights)
+    layers, total_bytes = [], 0.0
+    xs = {d: torch.from_numpy(make_x(batch, channel_gains(d, 5), 6).astype(np.float32)).to(torch.bfloat16).cuda()
+          for d in (4096, 14336)}
+    for m, name in enumerate(names):
+        d_out, d_in = LLAMA31_8B_SHAPES[name]
+        signs, u32, v32, s = make_random_blocks(4, d_out, d_in, 16, seed=seed_for(4, m, "blocks"))
+        u_bf = torch.from_numpy(u32).to(torch.bfloat16)
+        v_bf = torch.from_numpy(v32).to(torch.bfloat16)
+        r0, r1 = d_out * rank // world, d_out * (rank + 1) // world
+        for layer in range(32):
+            lay = pkg.Layer(d_out, d_in, k=16, n_capacity=4, factor_dtype="bf16", row_begin=r0, row_end=r1,
+                            device=local_rank)
+            lay.load_blocks(0, signs, u_bf, v_bf, s)
+            nn = int(n_of[layer, m])
+            lay.set_num_blocks(nn)
+            y = torch.empty((batch, r1 - r0), dtype=torch.float32, device="cuda")
+            yf = torch.empty((world * batch, r1 - r0), dtype=torch.float32, device="cuda") if world > 1 else None
+            layers.append((lay, xs[d_in], y, yf))
+            total_bytes += alg_bytes_per_rank(dict(d_in=d_in, k=16), r1 - r0, batch, nn)
+    stream = torch.cuda.current_stream()
+
+    def token_step(sh):
+        for lay, x, y, yf in layers:
+            lay.matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, batch, sh)
+            if world > 1:
+                dist.all_gather_into_tensor(yf, y)
+
+    for _ in range(max(args.warmup, 3)):
+        token_step(stream.cuda_stream)
+    torch.cuda.synchronize()
+    l0 = pkg.launch_count()
+    token_step(stream.cuda_stream)
+    per_step_launches = pkg.launch_count() - l0
+    steps = max(3, min(args.steps, 200))
+    graph = None
+    if world == 1 and not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.graph(graph, stream=cap):
+            token_step(cap.cuda_stream)
+        stream.wait_stream(cap)
+        graph.replay()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            if graph is not None:
+                graph.replay()
+            else:
+                token_step(stream.cuda_stream)
+        e1.record()
+        torch.cuda.synchronize()
+        pkg.profile_begin(4096)
+        token_step(stream.cuda_stream)
+        torch.cuda.synchronize()
+        nk, kms = pkg.profile_end()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        tb = torch.tensor([total_bytes], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tb)
+        all_bytes = float(tb.item())
+    else:
+        all_bytes = total_bytes
+    # e2e: the token's activations in from pinned host memory and every output back
+    x_h = {d: x.cpu().pin_memory() for d, x in xs.items()}
+    y_h = [torch.empty_like(y, device="cpu").pin_memory() for _, _, y, _ in layers]
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ke = max(3, min(steps, 50))
+    f0.record()
+    for _ in range(ke):
+        for d, x in xs.items():
+            x.copy_(x_h[d], non_blocking=True)
+        if graph is not None:
+            graph.replay()
+        else:
+            token_step(stream.cuda_stream)
+        for (_, _, y, _), yh in zip(layers, y_h):
+            yh.copy_(y, non_blocking=True)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / ke
+    clocks = sampler.summary()
+    peak, peak_src = peaks("decode")
+    achieved = total_bytes / 1e9 / (kms * 1e-3) if kms > 0 else None
+    if rank == 0:
+        line = {
+            "metric": metric_name(dict(kind="decode")) + " -- whole 8B linear stack per token",
+            "value": all_bytes / 1e9 / (ms * 1e-3), "unit": "GB/s", "n_gpus": world, "steps": steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "tokens_per_s": batch / (ms * 1e-3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "e4m3 MMA operands (S exact, Z as 3 e4m3 digits), fp32 accumulate",
+            "data": "synthetic (stored-form random blocks + activations, synthetic/ recipe)",
+            "config": {"workload": w["label"], "batch": batch, "matrices": len(layers),
+                       "blocks_per_matrix": {"3": int((n_of == 3).sum()), "4": int((n_of == 4).sum())},
+                       "weight_bytes_per_token": all_bytes,
+                       "parallelism": f"tp{world} (row shards + NCCL all-gather)" if world > 1 else "tp1",
+                       "l2": "inputs larger than L2 (3.7 GB of blocks per token-step)",
+                       "timing": "CUDA-graph replay of the 224 calls" if graph is not None else "eager launches"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None, "peak_source": peak_src,
+                         "kernel": "zq_kernel + decode_f8i_kernel pairs (sum over the 224 calls)",
+                         "kernel_us": kms * 1e3, "kernel_launches_timed": nk},
+            "clocks": clocks,
+            "e2e": {"value": all_bytes / 1e9 / (e2e_ms * 1e-3), "unit": "GB/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in x_h.values())),
+                    "d2h_bytes_per_step": int(sum(y.numel() * y.element_size() for y in y_h))},
+            "gpu_launches": int(per_step_launches * steps),
+            "cpu_baseline": None,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, _ = oracle_stack_sample(1)
+            line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+                                    "sample": "dense oracle (fp64 numpy, Eq.8+Eq.4) for 64 rows of each of "
+                                              "layer 0's 7 matrices, 1 call each"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -186,6 +368,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if w["kind"] == "stack":
+        return run_stack(args, w, world, rank, local_rank)
 
     if args.impl == "reference":
         if rank != 0:

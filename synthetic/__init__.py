@@ -7,8 +7,10 @@ with the shapes and distributions of the paper's workloads (SURVEY.md §8(d),
 (paper_2410_23918_b200/) can be fed identical bytes while sharing no code.
 """
 from .generators import (  # noqa: F401
+    C4_LEVELS,
     CONFIGS,
     LLAMA31_8B_SHAPES,
+    average_levels,
     seed_for,
     channel_gains,
     make_weight,

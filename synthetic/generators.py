@@ -27,6 +27,22 @@ CONFIGS = {
     "c5": dict(d_out=8192, d_in=28672, n=12, k=16, batch=1, factor_dtype="bf16"),
 }
 
+# Config C4: the paper's 8B memory points map to these average block levels per
+# matrix ((budget - 2004.5 MiB embeddings/lm_head) / 912 MiB per level).
+C4_LEVELS = {3674: 1.83, 3877: 2.05, 4506: 2.74, 4709: 2.97, 5338: 3.66, 5541: 3.88}
+
+
+def average_levels(n_matrices: int, level: float, seed: int):
+    """Per-matrix block counts for an average level ("Average" layering S:356):
+    every matrix gets floor(level) blocks, and a seeded random permutation of the matrices
+    receives the next block until round(frac * n_matrices) extra blocks are spent."""
+    base = int(np.floor(level))
+    extra = int(round((level - base) * n_matrices))
+    n = np.full(n_matrices, base, np.int64)
+    n[np.random.default_rng(seed).permutation(n_matrices)[:extra]] += 1
+    return n
+
+
 # Llama-3.1-8B per-layer linear shapes [d_out, d_in] (config C4; P:805 Table A.4 row).
 LLAMA31_8B_SHAPES = {
     "q_proj": (4096, 4096),
