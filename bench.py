@@ -41,7 +41,7 @@ WORKLOADS = {
     "c4": dict(d_out=4096, d_in=4096, n=4, k=16, batch=1, factor_dtype="bf16", kind="stack",
                label="c4: full Llama-3.1-8B linear stack (32 layers x q,k,v,o,gate,up,down = 224 matrices), "
                      "5541 MiB budget (average level 3.88: 3-4 blocks per matrix, seeded Average layering), "
-                     "decode, one token-step = 224 bitstack_matmul calls"),
+                     "decode, one token-step = the 224 matmuls as 128 grouped calls (bitstack_matmul_grouped per shared input)"),
     "c3_down": dict(CONFIGS["c3_down"], kind="prefill",
                     label="c3: Llama-3.1-8B down_proj 4096x14336, n=8 blocks, k=16, bf16 factors, prefill 2048 tokens"),
 }
@@ -238,12 +238,24 @@ def run_stack(args, w, world, rank, local_rank):
             layers.append((lay, xs[d_in], y, yf))
             total_bytes += alg_bytes_per_rank(dict(d_in=d_in, k=16), r1 - r0, batch, nn)
     stream = torch.cuda.current_stream()
+    # matrices of one transformer layer that read the same activation run as one grouped call
+    # (bitstack_matmul_grouped: one Zq + one decode launch): {q,k,v}, {o}, {gate,up}, {down}
+    deps = [["q_proj", "k_proj", "v_proj"], ["o_proj"], ["gate_proj", "up_proj"], ["down_proj"]]
+    if args.no_group:
+        deps = [[nm] for nm in names]
+    groups = []
+    for layer in range(32):
+        for dg in deps:
+            mem = [layers[names.index(nm) * 32 + layer] for nm in dg]
+            groups.append((pkg.Group([m[0] for m in mem], [m[1].data_ptr() for m in mem],
+                                     [m[2].data_ptr() for m in mem]), mem))
 
     def token_step(sh):
-        for lay, x, y, yf in layers:
-            lay.matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, batch, sh)
+        for grp, mem in groups:
+            grp(pkg.BF16, pkg.F32, batch, sh)
             if world > 1:
-                dist.all_gather_into_tensor(yf, y)
+                for _, _, y, yf in mem:
+                    dist.all_gather_into_tensor(yf, y)
 
     for _ in range(max(args.warmup, 3)):
         token_step(stream.cuda_stream)
@@ -325,10 +337,12 @@ def run_stack(args, w, world, rank, local_rank):
                        "weight_bytes_per_token": all_bytes,
                        "parallelism": f"tp{world} (row shards + NCCL all-gather)" if world > 1 else "tp1",
                        "l2": "inputs larger than L2 (3.7 GB of blocks per token-step)",
-                       "timing": "CUDA-graph replay of the 224 calls" if graph is not None else "eager launches"},
+                       "calls_per_token": len(groups),
+                       "grouping": "per matrix" if args.no_group else "grouped per shared input: {q,k,v},{o},{gate,up},{down}",
+                       "timing": "CUDA-graph replay of the token's calls" if graph is not None else "eager launches"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None, "peak_source": peak_src,
-                         "kernel": "zq_kernel + decode_f8i_kernel pairs (sum over the 224 calls)",
+                         "kernel": "zq + decode_f8i kernel pairs (sum over the token's calls)",
                          "kernel_us": kms * 1e3, "kernel_launches_timed": nk},
             "clocks": clocks,
             "e2e": {"value": all_bytes / 1e9 / (e2e_ms * 1e-3), "unit": "GB/s", "ms_per_step": e2e_ms,
@@ -358,6 +372,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-group", action="store_true",
+                    help="c4: one bitstack_matmul per matrix instead of grouped calls per shared input")
     ap.add_argument("--sweep", action="store_true", help="also report us/layer for n = 1, 2, 4, 8, 16")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -139,6 +139,23 @@ BITSTACK_API bitstack_status bitstack_set_num_blocks(bitstack_layer layer, int32
 BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x, bitstack_dtype x_dtype,
                                 void* y, bitstack_dtype y_dtype, int64_t batch, void* stream);
 
+/* Several independent bitstack_matmul calls at one batch size, e.g. the q/k/v or gate/up
+ * projections of a transformer layer that read the same token (Fig.2: every linear
+ * layer of the model is a BitStack stack):  ys[i] = W_hat_{n_i}(layers[i]) xs[i], i < count.
+ * Each member keeps its own level n_i, dtypes of x / y are shared, xs[i] / ys[i] follow
+ * bitstack_matmul's layouts (xs[i] may be the same buffer for several members).
+ * When count <= 8, 1 <= batch <= 4, the members are distinct handles on one device on the
+ * e4m3 decode path (bf16/f16 factors, k <= 16, d_in % 8 == 0, n_i >= 1, AUTO or TC kernel)
+ * and all xs / ys are 16-byte aligned device buffers, the whole group runs as ONE Zq launch
+ * and ONE decode launch whose CTAs are shared out among the members in proportion to their
+ * work; otherwise the members run one after another through bitstack_matmul.  Results are
+ * identical to the individual calls either way.  With profiling enabled the fused pair is
+ * bracketed once.  count == 0 or batch == 0 is a no-op.
+ * Errors: E_INVALID_ARG (NULL arrays) and every error of bitstack_matmul. */
+BITSTACK_API bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t count,
+                                        const void* const* xs, bitstack_dtype x_dtype, void* const* ys,
+                                        bitstack_dtype y_dtype, int64_t batch, void* stream);
+
 /* w = W_hat_n[row_begin:row_end, :] = sum_{i<n} (S_i (.) U_i V_i^T) diag(1/s)
  * (Eq.8 + Eq.4) written densely to device w [row_end-row_begin, d_in] row-major,
  * dtype F32 | BF16 | F16.  A test / export path ("restoration").

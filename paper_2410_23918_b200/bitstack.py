@@ -27,7 +27,7 @@ STATUS = {
 
 EXPORTED_SYMBOLS = (
     "bitstack_create", "bitstack_destroy", "bitstack_load_blocks", "bitstack_set_num_blocks",
-    "bitstack_matmul", "bitstack_reconstruct", "bitstack_get_info", "bitstack_set_kernel",
+    "bitstack_matmul", "bitstack_matmul_grouped", "bitstack_reconstruct", "bitstack_get_info", "bitstack_set_kernel",
     "bitstack_block_size_bits", "bitstack_last_error", "bitstack_profile_begin",
     "bitstack_profile_end", "bitstack_launch_count",
 )
@@ -73,6 +73,7 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
         "bitstack_load_blocks": (I32, [VP, I32, I32, VP, VP, VP, VP, VP]),
         "bitstack_set_num_blocks": (I32, [VP, I32]),
         "bitstack_matmul": (I32, [VP, VP, I32, VP, I32, I64, VP]),
+        "bitstack_matmul_grouped": (I32, [P(VP), I32, P(VP), I32, P(VP), I32, I64, VP]),
         "bitstack_reconstruct": (I32, [VP, VP, I32, VP]),
         "bitstack_get_info": (I32, [VP, P(Info)]),
         "bitstack_set_kernel": (I32, [VP, I32]),
@@ -226,3 +227,43 @@ class Layer:
                         device=f"cuda:{self.device}")
         _check(_lib.bitstack_reconstruct(self._h, _ptr(w), dtype_code(w.dtype), _stream_handle(stream)))
         return w
+
+
+class Group:
+    """Pointer arrays of a fixed bitstack_matmul_grouped call (bench / CUDA-graph capture):
+    members `layers`, inputs `x_ptrs`, outputs `y_ptrs`, built once, called many times."""
+
+    def __init__(self, layers, x_ptrs, y_ptrs):
+        n = len(layers)
+        if not (n == len(x_ptrs) == len(y_ptrs)):
+            raise ValueError("layers, x_ptrs and y_ptrs differ in length")
+        self.count = n
+        self._layers = list(layers)   # keep the handles alive
+        self._h = (ctypes.c_void_p * n)(*[l._h.value for l in layers])
+        self._x = (ctypes.c_void_p * n)(*[int(p) for p in x_ptrs])
+        self._y = (ctypes.c_void_p * n)(*[int(p) for p in y_ptrs])
+
+    def __call__(self, x_dtype: int, y_dtype: int, batch: int, stream: int) -> None:
+        _check(_lib.bitstack_matmul_grouped(self._h, self.count, self._x, int(x_dtype), self._y, int(y_dtype),
+                                            int(batch), int(stream)))
+
+
+def matmul_grouped(layers, xs, y_dtype=None, stream=None):
+    """ys[i] = W_hat(layers[i]) xs[i] in one grouped call (include/bitstack.h
+    bitstack_matmul_grouped); xs: device tensors [batch, d_in_i] of one dtype and batch."""
+    import torch
+    xs = [x.unsqueeze(0) if x.dim() == 1 else x for x in xs]
+    if len(xs) != len(layers):
+        raise ValueError("one input per layer")
+    batch = int(xs[0].shape[0]) if xs else 0
+    ys = [torch.empty((x.shape[0], l.rows), dtype=y_dtype or torch.float32, device=x.device)
+          for l, x in zip(layers, xs)]
+    if not layers:
+        return ys
+    xdt = dtype_code(xs[0].dtype)
+    for x in xs:
+        if int(x.shape[0]) != batch or dtype_code(x.dtype) != xdt:
+            raise ValueError("grouped inputs must share batch size and dtype")
+    Group(layers, [_ptr(x) for x in xs], [_ptr(y) for y in ys])(xdt, dtype_code(ys[0].dtype), batch,
+                                                                    _stream_handle(stream))
+    return ys

@@ -151,6 +151,38 @@ template <> struct F8Geom<1> { static constexpr int R = 4; };
 template <> struct F8Geom<2> { static constexpr int R = 2; };
 template <> struct F8Geom<4> { static constexpr int R = 2; };
 
+// Z workspace of layer L for `units` (block, 128-column chunk) pairs at batch class NB; grows
+// once per larger batch class (a stream sync + cudaMalloc), never inside steady state.
+template <int NB>
+bitstack_status ensure_zq(bitstack_layer L, int64_t units, cudaStream_t st) {
+  using C = bs::DecodeF8Cfg<NB, F8Geom<NB>::R>;
+  if (units * C::kZUnit <= L->zq_bytes) return BITSTACK_OK;
+  CK(cudaStreamSynchronize(st));
+  cudaFree(L->zq);
+  L->zq = nullptr;
+  const int64_t cap = (int64_t)L->n_cap * L->nq * C::kZUnit;
+  CK(cudaMalloc((void**)&L->zq, (size_t)cap));
+  L->bytes += cap - L->zq_bytes;
+  L->zq_bytes = cap;
+  return BITSTACK_OK;
+}
+
+bs::ZqParams zq_params(bitstack_layer L, const bs::DecodeParams& p) {
+  bs::ZqParams zp;
+  zp.v = p.v;
+  zp.inv_s = p.inv_s;
+  zp.x = p.x;
+  zp.zq = L->zq;
+  zp.x_stride = p.x_stride;
+  zp.nq = p.nq;
+  zp.d_in = p.d_in;
+  zp.d_in_pad = p.d_in_pad;
+  zp.batch = p.batch;
+  zp.x_dtype = p.x_dtype;
+  zp.f_dtype = p.f_dtype;
+  return zp;
+}
+
 template <int NB>
 bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_in, int grid, cudaStream_t st) {
   using G = F8Geom<NB>;
@@ -169,28 +201,9 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
 
 
   const int64_t units = (int64_t)prm_in.n * prm_in.nq;
-  const int64_t need = units * C::kZUnit;
-  if (need > L->zq_bytes) {  // grows once per larger batch class; never inside steady state
-    CK(cudaStreamSynchronize(st));
-    cudaFree(L->zq);
-    L->zq = nullptr;
-    const int64_t cap = (int64_t)L->n_cap * L->nq * C::kZUnit;
-    CK(cudaMalloc((void**)&L->zq, (size_t)cap));
-    L->bytes += cap - L->zq_bytes;
-    L->zq_bytes = cap;
-  }
-  bs::ZqParams zp;
-  zp.v = prm_in.v;
-  zp.inv_s = prm_in.inv_s;
-  zp.x = prm_in.x;
-  zp.zq = L->zq;
-  zp.x_stride = prm_in.x_stride;
-  zp.nq = prm_in.nq;
-  zp.d_in = prm_in.d_in;
-  zp.d_in_pad = prm_in.d_in_pad;
-  zp.batch = prm_in.batch;
-  zp.x_dtype = prm_in.x_dtype;
-  zp.f_dtype = prm_in.f_dtype;
+  bitstack_status zs = ensure_zq<NB>(L, units, st);
+  if (zs) return zs;
+  const bs::ZqParams zp = zq_params(L, prm_in);
   bs::zq_kernel<NB><<<(unsigned)units, 128, 0, st>>>(zp);
   count_launch();
   CK(cudaGetLastError());
@@ -368,6 +381,119 @@ bitstack_status dispatch_decode(int nb, const bs::DecodeParams& prm, int grid, c
 int r_tiles_for(int nb, int ndig) {
   const int N = 16 * nb * ndig;
   return std::min(8, 256 / N);
+}
+
+// Kernel parameters of one batch chunk [b0, b0 + bc) of layer L on the tcgen05 decode paths.
+bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz, void* y, int ydt, int ysz,
+                                      int64_t b0, int bc, int n_groups, int cpg) {
+  bs::DecodeParams prm;
+  prm.signs = L->signs;
+  prm.u = L->u;
+  prm.v = L->v;
+  prm.inv_s = L->inv_s;
+  prm.x = reinterpret_cast<const uint8_t*>(x) + b0 * L->d_in * xsz;
+  prm.y = reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz;
+  prm.y_acc = L->y_acc;
+  prm.counters = L->counters;
+  prm.x_stride = L->d_in;
+  prm.y_stride = L->rows_local;
+  prm.n = L->n_act;
+  prm.nq = L->nq;
+  prm.rows_pad = L->rows_pad;
+  prm.rows_local = (int)L->rows_local;
+  prm.d_in = (int)L->d_in;
+  prm.d_in_pad = (int)L->d_in_pad;
+  prm.row_tiles = L->row_tiles;
+  prm.n_groups = n_groups;
+  prm.ctas_per_group = cpg;
+  prm.batch = bc;
+  prm.x_dtype = xdt;
+  prm.y_dtype = ydt;
+  prm.f_dtype = L->dev_fdt;
+  prm.one2 = 0x3C003C00u;
+  prm.dbg_acc = g_dbg_acc;
+  prm.dbg_z = g_dbg_z;
+  prm.zq = nullptr;
+  prm.status = nullptr;
+  return prm;
+}
+
+// One zq_grouped_kernel + one decode_f8i_grouped_kernel (PDL) for `count` layers at batch
+// class NB.  The SMs are shared out in proportion to work: every layer starts at one CTA per
+// row group, then CTAs go one row group's worth at a time to the layer with the most work per
+// CTA while the total stays within one wave (sm_count CTAs, one resident per SM).
+template <int NB>
+bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const void* const* xs, int xdt,
+                                         int xsz, void* const* ys, int ydt, int ysz, int bc, cudaStream_t st) {
+  constexpr int R = F8Geom<NB>::R;
+  using CI = bs::DecodeF8ICfg<NB, R>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(bs::decode_f8i_grouped_kernel<NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            CI::kSmemBytes));
+    attr_done = true;
+  }
+  int n_groups[bs::kMaxGroup], cpg[bs::kMaxGroup];
+  int64_t units[bs::kMaxGroup];
+  double work[bs::kMaxGroup];
+  int total = 0;
+  for (int i = 0; i < count; ++i) {
+    bitstack_layer L = layers[i];
+    n_groups[i] = (L->row_tiles + R - 1) / R;
+    units[i] = (int64_t)L->n_act * L->nq;
+    work[i] = (double)units[i] * L->row_tiles;
+    cpg[i] = 1;
+    total += n_groups[i];
+  }
+  const int budget = layers[0]->sm_count;
+  for (;;) {
+    int best = -1;
+    double best_w = 0.0;
+    for (int i = 0; i < count; ++i) {
+      if (cpg[i] >= units[i] || total + n_groups[i] > budget) continue;
+      const double w = work[i] / ((double)n_groups[i] * cpg[i]);
+      if (w > best_w) { best_w = w; best = i; }
+    }
+    if (best < 0) break;
+    ++cpg[best];
+    total += n_groups[best];
+  }
+  bs::ZqGroup zg;
+  bs::DecodeGroup dg;
+  zg.count = dg.count = count;
+  zg.unit_start[0] = dg.cta_start[0] = 0;
+  for (int i = 0; i < count; ++i) {
+    bitstack_layer L = layers[i];
+    bitstack_status zs = ensure_zq<NB>(L, units[i], st);
+    if (zs) return zs;
+    bs::DecodeParams prm = decode_params(L, xs[i], xdt, xsz, ys[i], ydt, ysz, 0, bc, n_groups[i], cpg[i]);
+    prm.zq = L->zq;
+    prm.status = L->status;
+    zg.prm[i] = zq_params(L, prm);
+    dg.prm[i] = prm;
+    zg.unit_start[i + 1] = zg.unit_start[i] + (int)units[i];
+    dg.cta_start[i + 1] = dg.cta_start[i] + n_groups[i] * cpg[i];
+  }
+  for (int i = count; i < bs::kMaxGroup; ++i) zg.unit_start[i + 1] = dg.cta_start[i + 1] = 0;
+  int slot = -1;
+  bitstack_status ps = record_prof(st, true, &slot);
+  if (ps) return ps;
+  bs::zq_grouped_kernel<NB><<<(unsigned)zg.unit_start[count], 128, 0, st>>>(zg);
+  count_launch();
+  CK(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)dg.cta_start[count]);
+  cfg.blockDim = dim3(CI::kThreads);
+  cfg.dynamicSmemBytes = CI::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_grouped_kernel<NB, R>, dg));
+  count_launch();
+  return record_prof(st, false, &slot);
 }
 
 }  // namespace
@@ -672,35 +798,7 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
     const int64_t units = (int64_t)L->n_act * L->nq;
     int cpg = std::max(1, L->sm_count / n_groups);
     cpg = (int)std::min<int64_t>(cpg, units);
-    bs::DecodeParams prm;
-    prm.signs = L->signs;
-    prm.u = L->u;
-    prm.v = L->v;
-    prm.inv_s = L->inv_s;
-    prm.x = reinterpret_cast<const uint8_t*>(x) + b0 * L->d_in * xsz;
-    prm.y = reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz;
-    prm.y_acc = L->y_acc;
-    prm.counters = L->counters;
-    prm.x_stride = L->d_in;
-    prm.y_stride = L->rows_local;
-    prm.n = L->n_act;
-    prm.nq = L->nq;
-    prm.rows_pad = L->rows_pad;
-    prm.rows_local = (int)L->rows_local;
-    prm.d_in = (int)L->d_in;
-    prm.d_in_pad = (int)L->d_in_pad;
-    prm.row_tiles = L->row_tiles;
-    prm.n_groups = n_groups;
-    prm.ctas_per_group = cpg;
-    prm.batch = bc;
-    prm.x_dtype = xdt;
-    prm.y_dtype = ydt;
-    prm.f_dtype = L->dev_fdt;
-    prm.one2 = 0x3C003C00u;
-    prm.dbg_acc = g_dbg_acc;
-    prm.dbg_z = g_dbg_z;
-    prm.zq = nullptr;
-    prm.status = nullptr;
+    const bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
     int slot = -1;
     bitstack_status ps = record_prof(st, true, &slot);
     if (ps) return ps;
@@ -777,6 +875,42 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
   if (rs) return rs;
   if (copy_back) CK(cudaMemcpyAsync(y, L->stage_y, (size_t)ybytes, cudaMemcpyDeviceToHost, st));
   return BITSTACK_OK;
+}
+
+bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t count, const void* const* xs,
+                                        bitstack_dtype x_dtype, void* const* ys, bitstack_dtype y_dtype,
+                                        int64_t batch, void* stream) {
+  if (count < 0 || (count > 0 && (!layers || !xs || !ys))) return fail(BITSTACK_E_INVALID_ARG, "bad group arrays");
+  if (count == 0 || batch == 0) return BITSTACK_OK;
+  // One launch pair when every member can take the e4m3 decode kernel on device buffers;
+  // otherwise the members run one after another through bitstack_matmul (same results).
+  bool fused = count <= bs::kMaxGroup && batch >= 1 && batch <= 4 && decode_issuer() &&
+               valid_dtype(x_dtype) && (y_dtype == BITSTACK_F32 || y_dtype == BITSTACK_BF16);
+  for (int i = 0; fused && i < count; ++i) {
+    bitstack_layer L = layers[i];
+    fused = L && xs[i] && ys[i] && L->device == layers[0]->device && L->layout == 1 && L->n_res > 0 &&
+            L->n_act > 0 && L->n_act <= L->n_res && L->k <= 16 && L->d_in % 8 == 0 &&
+            (L->kernel == BITSTACK_KERNEL_AUTO || L->kernel == BITSTACK_KERNEL_TC) &&
+            (reinterpret_cast<uintptr_t>(xs[i]) % 16) == 0 && mem_kind(xs[i]) == kMemDevice &&
+            mem_kind(ys[i]) == kMemDevice;
+    for (int j = 0; fused && j < i; ++j) fused = layers[j] != L;   // each member owns its workspaces
+  }
+  if (!fused) {
+    for (int i = 0; i < count; ++i) {
+      bitstack_status rs = bitstack_matmul(layers[i], xs[i], x_dtype, ys[i], y_dtype, batch, stream);
+      if (rs) return rs;
+    }
+    return BITSTACK_OK;
+  }
+  DeviceGuard guard(layers[0]->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
+  const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
+  const int xsz = dsize(x_dtype), ysz = y_dtype == BITSTACK_F32 ? 4 : 2;
+  const int bc = (int)batch;
+  if (bc == 1) return launch_grouped_f8<1>(layers, count, xs, xdt, xsz, ys, ydt, ysz, bc, st);
+  if (bc == 2) return launch_grouped_f8<2>(layers, count, xs, xdt, xsz, ys, ydt, ysz, bc, st);
+  return launch_grouped_f8<4>(layers, count, xs, xdt, xsz, ys, ydt, ysz, bc, st);
 }
 
 bitstack_status bitstack_reconstruct(bitstack_layer L, void* w, bitstack_dtype w_dtype, void* stream) {

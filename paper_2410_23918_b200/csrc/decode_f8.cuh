@@ -107,13 +107,12 @@ struct ZqParams {
 
 // One CTA per unit (block i, subchunk q); thread c = column q*128 + c.
 template <int NB>
-__global__ void __launch_bounds__(128) zq_kernel(const ZqParams p) {
+__device__ __forceinline__ void zq_body(const ZqParams& p, const int unit) {
   using C = ZqCfg<NB>;
   constexpr int N = C::N;
   __shared__ __align__(16) uint8_t tile[C::kZBytes];
   __shared__ float red[4];
   asm volatile("griddepcontrol.launch_dependents;");
-  const int unit = blockIdx.x;
   const int i = unit / p.nq, q = unit % p.nq;
   const int c = threadIdx.x;
   const int col = q * kSubK + c;
@@ -187,6 +186,26 @@ __global__ void __launch_bounds__(128) zq_kernel(const ZqParams p) {
   for (int e = c; e < C::kZBytes / 16; e += 128)
     reinterpret_cast<uint4*>(dst)[e] = reinterpret_cast<const uint4*>(tile)[e];
   if (c == 0) reinterpret_cast<int4*>(dst + C::kZBytes)[0] = make_int4(e_u, 0, 0, 0);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128) zq_kernel(const ZqParams p) {
+  zq_body<NB>(p, (int)blockIdx.x);
+}
+
+// Grouped Zq (bitstack_matmul_grouped): units [unit_start[i], unit_start[i+1]) belong to layer i.
+constexpr int kMaxZqGroup = 8;
+struct ZqGroup {
+  int count;
+  int unit_start[kMaxZqGroup + 1];
+  ZqParams prm[kMaxZqGroup];
+};
+
+template <int NB>
+__global__ void __launch_bounds__(128) zq_grouped_kernel(const __grid_constant__ ZqGroup grp) {
+  int i = 0;
+  while (i + 1 < grp.count && (int)blockIdx.x >= grp.unit_start[i + 1]) ++i;
+  zq_body<NB>(grp.prm[i], (int)blockIdx.x - grp.unit_start[i]);
 }
 
 template <int NB, int R_>

@@ -45,8 +45,10 @@ struct DecodeF8ICfg {
   static_assert(5 * R + 1 <= 32, "warps");
 };
 
+// The kernel body, for CTA `cta` of the launch that computes the layer described by p
+// (decode_f8i_kernel: one layer, cta = cta; decode_f8i_grouped_kernel: several).
 template <int NB, int R_>
-__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_kernel(const DecodeParams p) {
+__device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int cta) {
   using C = DecodeF8ICfg<NB, R_>;
   constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -61,8 +63,8 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int g = blockIdx.x / p.ctas_per_group;
-  const int jc = blockIdx.x % p.ctas_per_group;
+  const int g = cta / p.ctas_per_group;
+  const int jc = cta % p.ctas_per_group;
   const long long L = (long long)p.n * p.nq;
   const long long u0 = L * jc / p.ctas_per_group;
   const long long u1 = L * (jc + 1) / p.ctas_per_group;
@@ -76,14 +78,14 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
   // releases unit k+1 only after syncing on unit k's tile, and the expanders arrive on unit
   // k+1's tile only after that release.
 #ifdef BS_DECODE_TRACE
-  long long* trace = (p.dbg_acc && blockIdx.x == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
+  long long* trace = (p.dbg_acc && cta == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
   const long long tstart = clock64();
 #define BS_ITRACE(k_, c_) do { if (trace && lane == 0) trace[(k_) * 16 + (c_)] = clock64() - tstart; } while (0)
   if (p.dbg_acc && threadIdx.x == 0) {   // every CTA's entry %globaltimer (ns), unit count
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x] = (long long)gt;
-    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x + 2] = nunits;
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * cta] = (long long)gt;
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * cta + 2] = nunits;
   }
 #else
 #define BS_ITRACE(k_, c_) do { } while (0)
@@ -309,7 +311,7 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
   if (p.dbg_acc && threadIdx.x == 0) {   // exit of the main phase (before the teardown barrier)
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * blockIdx.x + 1] = (long long)gt;
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * cta + 1] = (long long)gt;
   }
 #endif
   // ---- teardown + last-CTA-of-group finalisation
@@ -342,6 +344,28 @@ __global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_
     }
     if (threadIdx.x == 0) p.counters[g] = 0;
   }
+}
+
+template <int NB, int R_>
+__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_kernel(const DecodeParams p) {
+  decode_f8i_body<NB, R_>(p, (int)blockIdx.x);
+}
+
+// Grouped launch (bitstack_matmul_grouped): layers [0, count) of one launch, CTAs
+// [cta_start[i], cta_start[i+1]) compute layer i -- several matrices that share a batch
+// (e.g. the q/k/v projections of a token) pay the launch, the Zq dependency and the tail once.
+constexpr int kMaxGroup = 8;
+struct DecodeGroup {
+  int count;
+  int cta_start[kMaxGroup + 1];
+  DecodeParams prm[kMaxGroup];
+};
+
+template <int NB, int R_>
+__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_grouped_kernel(const __grid_constant__ DecodeGroup grp) {
+  int i = 0;
+  while (i + 1 < grp.count && (int)blockIdx.x >= grp.cta_start[i + 1]) ++i;
+  decode_f8i_body<NB, R_>(grp.prm[i], (int)blockIdx.x - grp.cta_start[i]);
 }
 
 }  // namespace bs

@@ -316,6 +316,78 @@ def test_host_buffers(bs, batch):
     assert O.relative_l2(y_dev.numpy().astype(np.float64), ref) <= 1e-3
 
 
+# ------------------------------------------------------------------ grouped decode launches
+def _grouped_case(bs, shapes, seed):
+    out = []
+    for j, (d_out, d_in, n) in enumerate(shapes):
+        g, s32, blocks = compress_case(d_out, d_in, n, "bf16", seed + 7 * j)
+        out.append((g, s32, blocks, make_layer(bs, d_out, d_in, blocks, s32, "bf16")))
+    return out
+
+
+@pytest.mark.parametrize("batch", [1, 2, 3, 4])
+def test_grouped_matches_individual_and_oracle(bs, batch):
+    """bitstack_matmul_grouped: members of different shapes (ragged rows, ragged d_in) and
+    levels run as ONE zq + ONE decode launch and give the individual calls' y (up to the
+    order of the fp32 cross-CTA sums) and the oracle's within the decode tolerance."""
+    case = _grouped_case(bs, [(512, 640, 4), (300, 200, 3), (1100, 264, 5), (128, 1000, 2)], 501)
+    levels = [4, 1, 5, 2]
+    for (_, _, _, lay), n in zip(case, levels):
+        lay.set_num_blocks(n)
+    xs = [torch.from_numpy(make_x(batch, g, 40 + batch).astype(np.float32)).to(torch.bfloat16).cuda()
+          for g, _, _, _ in case]
+    lays = [c[3] for c in case]
+    c0 = bs.launch_count()
+    ys = bs.matmul_grouped(lays, xs)
+    torch.cuda.synchronize()
+    assert bs.launch_count() - c0 == 2           # zq_grouped + decode_f8i_grouped
+    for (g, s32, blocks, lay), n, x, y in zip(case, levels, xs, ys):
+        y1 = lay.matmul(x)
+        torch.cuda.synchronize()
+        yg = y.cpu().numpy().astype(np.float64)
+        assert O.relative_l2(yg, y1.cpu().numpy().astype(np.float64)) <= 1e-5
+        ref = oracle_y(blocks, s32, n, x.float().cpu().numpy().astype(np.float64))
+        assert O.relative_l2(yg, ref) <= 1e-3, (lay.rows, n)
+
+
+def test_grouped_shared_x_more_ctas_than_sms(bs):
+    """q/k/v-style members reading ONE x buffer; 4 members of 5120 rows need 160 row groups,
+    more than one CTA per SM on 148 SMs (the decode kernel does not rely on co-residency)."""
+    case = _grouped_case(bs, [(5120, 256, 2)] * 4, 611)
+    g = case[0][0]
+    x = torch.from_numpy(make_x(2, g, 3).astype(np.float32)).to(torch.bfloat16).cuda()
+    lays = [c[3] for c in case]
+    ys = bs.matmul_grouped(lays, [x] * 4, y_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    xr = x.float().cpu().numpy().astype(np.float64)
+    for (_, s32, blocks, _), y in zip(case, ys):
+        assert O.relative_l2(y.float().cpu().numpy().astype(np.float64), oracle_y(blocks, s32, 2, xr)) <= 4e-3
+
+
+def test_grouped_fallbacks(bs):
+    """Groups the single launch cannot take (fp32 factors, batch > 4, a repeated handle,
+    more than 8 members, n == 0) run member by member with identical results."""
+    case = _grouped_case(bs, [(256, 384, 2), (384, 256, 3)], 701)
+    g32, s32f, blocks32 = compress_case(200, 384, 2, "f32", 721)
+    lay32 = make_layer(bs, 200, 384, blocks32, s32f, "f32")
+    a, b = case[0][3], case[1][3]
+    for batch in (1, 6):
+        xa = torch.from_numpy(make_x(batch, case[0][0], 9).astype(np.float32)).cuda()
+        xb = torch.from_numpy(make_x(batch, case[1][0], 10).astype(np.float32)).cuda()
+        for lays, xs in (([a, lay32, b], [xa, xa, xb]), ([a, a], [xa, xa]), ([b] * 9, [xb] * 9), ([a, b], [xa, xb])):
+            ys = bs.matmul_grouped(lays, xs)
+            torch.cuda.synchronize()
+            for lay, x, y in zip(lays, xs, ys):
+                y1 = lay.matmul(x)
+                torch.cuda.synchronize()
+                assert O.relative_l2(y.cpu().numpy().astype(np.float64), y1.cpu().numpy().astype(np.float64)) <= 1e-5
+    a.set_num_blocks(0)
+    ys = bs.matmul_grouped([a, b], [xa[:1], xb[:1]])
+    torch.cuda.synchronize()
+    assert not torch.any(ys[0])
+    assert bs.matmul_grouped([], []) == []
+
+
 # ------------------------------------------------------------------ H8: large-batch path
 @pytest.mark.parametrize("shape", [(384, 640), (200, 296), (1100, 264), (128, 64)])
 def test_prefill_parity_ragged(bs, shape):
