@@ -42,6 +42,9 @@ WORKLOADS = {
                label="c4: full Llama-3.1-8B linear stack (32 layers x q,k,v,o,gate,up,down = 224 matrices), "
                      "5541 MiB budget (average level 3.88: 3-4 blocks per matrix, seeded Average layering), "
                      "decode, one token-step = the 224 matmuls as 128 grouped calls (bitstack_matmul_grouped per shared input)"),
+    "load": dict(CONFIGS["c5"], kind="load",
+                 label="block streaming: the 12 blocks of Llama-3.1-70B down_proj 8192x28672 (k=16, bf16 "
+                       "factors) pushed from pinned host memory with bitstack_load_blocks_async"),
     "c3_down": dict(CONFIGS["c3_down"], kind="prefill",
                     label="c3: Llama-3.1-8B down_proj 4096x14336, n=8 blocks, k=16, bf16 factors, prefill 2048 tokens"),
 }
@@ -361,6 +364,171 @@ def run_stack(args, w, world, rank, local_rank):
         dist.destroy_process_group()
 
 
+def run_load(args, w, world, rank, local_rank):
+    """Block streaming (Fig.2 "load more weight residuals from
+    storage when available memory increases"): one step = pushing all n blocks of the
+    workload's matrix from pinned host memory into a handle with bitstack_load_blocks_async
+    (DMA of this rank's row shard of S_i and U_i plus V_i into staging, on-device repack into
+    the tile layout), timed with CUDA events on the load stream.  Reported beside it: a plain
+    pinned cudaMemcpyAsync of the same bytes (the PCIe roofline) and the load overlapped with
+    back-to-back decode calls of a resident copy of the same matrix on another stream."""
+    d_out, d_in, k, n = w["d_out"], w["d_in"], w["k"], args.n or w["n"]
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import bitstack_oracle as O
+        signs, _, _, _ = make_random_blocks(1, d_out, d_in, k, seed=seed_for(5, 0, "blocks"))
+        reps = max(1, min(args.steps, 3))
+        O.unpack_signs(signs[0], d_out, d_in)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            O.unpack_signs(signs[0], d_out, d_in)
+        dt = (time.perf_counter() - t0) / reps
+        val = signs[0].nbytes / 1e9 / dt
+        print(json.dumps({
+            "impl": "reference", "metric": "block load GB/s (stored-form bytes made usable per second)", "value": val,
+            "unit": "GB/s", "n_gpus": world, "steps": reps, "warmup": 1, "ms_per_step": dt * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (random stored-form blocks)",
+            "config": {"workload": w["label"], "parallelism": "cpu"},
+            "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": "oracle unpack_signs (canonical bits -> +-1) of one block"},
+            "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2410_23918_b200 import build as B
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2410_23918_b200 as pkg
+    pkg.load_library()
+    signs, u32, v32, s = make_random_blocks(n, d_out, d_in, k, seed=seed_for(5, 0, "blocks"))
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    ps = pin(signs)
+    pu = torch.from_numpy(u32).to(torch.bfloat16).pin_memory()
+    pv = torch.from_numpy(v32).to(torch.bfloat16).pin_memory()
+    pss = pin(s)
+    r0, r1 = d_out * rank // world, d_out * (rank + 1) // world
+    rows = r1 - r0
+    step_bytes = n * (rows * d_in / 8 + k * (rows + d_in) * 2) + 4 * d_in
+    lay = pkg.Layer(d_out, d_in, k=k, n_capacity=n, factor_dtype="bf16", row_begin=r0, row_end=r1, device=local_rank)
+    busy = pkg.Layer(d_out, d_in, k=k, n_capacity=n, factor_dtype="bf16", row_begin=r0, row_end=r1, device=local_rank)
+    busy.load_blocks(0, ps, pu, pv, pss)
+    side = torch.cuda.Stream()
+    l0 = pkg.launch_count()
+
+    def load_step():
+        lay.load_blocks_async(0, ps, pu, pv, pss, stream=side)
+
+    for _ in range(args.warmup):
+        load_step()
+    torch.cuda.synchronize()
+    launches_per_step = (pkg.launch_count() - l0) // args.warmup
+    steps = max(3, min(args.steps, 20))
+    sampler = ClockSampler(local_rank)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(side)
+        for _ in range(steps):
+            load_step()
+        e1.record(side)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    # PCIe roofline: one plain pinned host->device copy of the same bytes
+    flat = torch.empty(int(step_bytes), dtype=torch.uint8).pin_memory()
+    dflat = torch.empty_like(flat, device="cuda")
+    best = float("inf")
+    for _ in range(5):
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        dflat.copy_(flat, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        best = min(best, c0.elapsed_time(c1))
+    pcie_gbs = step_bytes / 1e9 / (best * 1e-3)
+    # overlap: decode of the resident copy on the main stream while the load runs on `side`
+    x = torch.from_numpy(make_x(1, channel_gains(d_in, 5), 6).astype(np.float32)).to(torch.bfloat16).cuda()
+    y = torch.empty((1, rows), dtype=torch.float32, device="cuda")
+    main = torch.cuda.current_stream()
+    calls = 40
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(5):
+        busy.matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, 1, main.cuda_stream)
+    torch.cuda.synchronize()
+    d0.record(main)
+    for _ in range(calls):
+        busy.matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, 1, main.cuda_stream)
+    d1.record(main)
+    torch.cuda.synchronize()
+    dec_alone = d0.elapsed_time(d1) / calls
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(main)
+    g0.record(side)
+    load_step()
+    g1.record(side)
+    ov_calls = 0
+    while not g1.query() or ov_calls < 5:
+        busy.matmul_raw(x.data_ptr(), pkg.BF16, y.data_ptr(), pkg.F32, 1, main.cuda_stream)
+        ov_calls += 1
+        if ov_calls % 20 == 0:
+            main.synchronize()
+        if ov_calls > 20000:
+            break
+    d1.record(main)
+    torch.cuda.synchronize()
+    ov_load_ms = g0.elapsed_time(g1)
+    dec_ov = d0.elapsed_time(d1) / ov_calls
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_bytes = step_bytes * world
+    if rank == 0:
+        peak_src = "measured in-run: pinned host->device cudaMemcpyAsync of the same bytes (best of 5)"
+        line = {
+            "metric": "block load GB/s (stored-form bytes of the rank's shard moved from pinned host memory into the "
+                      "device block store per second)",
+            "value": total_bytes / 1e9 / (ms * 1e-3), "unit": "GB/s", "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms, "ms_per_block": ms / n, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8 signs + bf16 factors",
+            "data": "synthetic (random stored-form blocks in pinned host memory)",
+            "config": {"workload": w["label"], "d_out": d_out, "d_in": d_in, "n": n, "k": k,
+                       "bytes_per_step": total_bytes, "parallelism": f"tp{world} (row shards)" if world > 1 else "tp1",
+                       "l2": "inputs larger than L2 (host memory, 355 MB per step)"},
+            "roofline": {"bound": "pcie", "achieved": step_bytes / 1e9 / (ms * 1e-3), "peak": pcie_gbs, "unit": "GB/s",
+                         "frac": (step_bytes / 1e9 / (ms * 1e-3)) / pcie_gbs, "traffic": None, "peak_source": peak_src,
+                         "kernel": "cudaMemcpyAsync DMA (overlapped) + repack_rows_kernel + factor_max_kernel + factor_scale_kernel per block"},
+            "overlap": {"decode_us_alone": dec_alone * 1e3, "decode_us_during_load": dec_ov * 1e3,
+                        "decode_calls_during_load": ov_calls, "load_ms_during_decode": ov_load_ms,
+                        "load_gbs_during_decode": step_bytes / 1e9 / (ov_load_ms * 1e-3)},
+            "clocks": sampler.summary(),
+            "e2e": {"value": total_bytes / 1e9 / (ms * 1e-3), "unit": "GB/s",
+                    "h2d_bytes_per_step": int(step_bytes), "d2h_bytes_per_step": 0,
+                    "note": "the step itself is the host->device transfer"},
+            "gpu_launches": int(launches_per_step * steps),
+            "cpu_baseline": None,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            from oracle import bitstack_oracle as O
+            O.unpack_signs(signs[0], d_out, d_in)
+            t0 = time.perf_counter()
+            O.unpack_signs(signs[0], d_out, d_in)
+            dt = time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": signs[0].nbytes / 1e9 / dt, "unit": "GB/s", "cores": cpu_cores(),
+                                    "kind": "oracle", "sample": "oracle unpack_signs of one block (canonical bits -> +-1)"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -387,6 +555,8 @@ def main():
 
     if w["kind"] == "stack":
         return run_stack(args, w, world, rank, local_rank)
+    if w["kind"] == "load":
+        return run_load(args, w, world, rank, local_rank)
 
     if args.impl == "reference":
         if rank != 0:

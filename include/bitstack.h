@@ -116,6 +116,24 @@ BITSTACK_API bitstack_status bitstack_load_blocks(bitstack_layer layer, int32_t 
                                      const uint8_t* signs, const void* u, const void* v,
                                      const float* s, void* stream);
 
+/* bitstack_load_blocks without the host synchronisation: block streaming, "load more weight
+ * residuals from storage when available memory increases" (Fig.2) overlapped with
+ * compute on other streams.  Same arguments, layouts, validation and errors.  Per block, the
+ * canonical sign bytes of this handle's rows (only the shard when d_in % 8 == 0), its U rows
+ * and V are copied with cudaMemcpyAsync on `stream` into a per-device staging area (two slots,
+ * grown once to the largest block seen; each slot is reused only after an event says its last
+ * reader finished), then repacked and rebalanced on `stream`.  The call returns once this is
+ * enqueued: from PINNED host memory or device memory the copies are asynchronous and the caller
+ * must keep the buffers unchanged until `stream` passes this point (e.g. an event recorded
+ * after the call); from pageable host memory cudaMemcpyAsync returns after the data is staged,
+ * so the call is effectively synchronous.  The resident/active counts change immediately:
+ * matmul calls enqueued later on `stream` see the new blocks; calls on other streams must wait
+ * for an event recorded on `stream` after this call.  Not capturable into a CUDA graph.
+ * bitstack_load_blocks is this call followed by a synchronisation of `stream`. */
+BITSTACK_API bitstack_status bitstack_load_blocks_async(bitstack_layer layer, int32_t first_block, int32_t count,
+                                           const uint8_t* signs, const void* u, const void* v,
+                                           const float* s, void* stream);
+
 /* Select how many resident blocks take part in matmul/reconstruct: 0 <= n <= resident.
  * Host-side O(1) ("dynamically load or offload"); affects calls enqueued
  * after it.  Blocks >= n stay resident until overwritten ("offload ... in

@@ -26,7 +26,8 @@ STATUS = {
 }
 
 EXPORTED_SYMBOLS = (
-    "bitstack_create", "bitstack_destroy", "bitstack_load_blocks", "bitstack_set_num_blocks",
+    "bitstack_create", "bitstack_destroy", "bitstack_load_blocks", "bitstack_load_blocks_async",
+    "bitstack_set_num_blocks",
     "bitstack_matmul", "bitstack_matmul_grouped", "bitstack_reconstruct", "bitstack_get_info", "bitstack_set_kernel",
     "bitstack_block_size_bits", "bitstack_last_error", "bitstack_profile_begin",
     "bitstack_profile_end", "bitstack_launch_count",
@@ -71,6 +72,7 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
         "bitstack_create": (I32, [I64, I64, I32, I32, I32, I64, I64, I32, P(VP)]),
         "bitstack_destroy": (I32, [VP]),
         "bitstack_load_blocks": (I32, [VP, I32, I32, VP, VP, VP, VP, VP]),
+        "bitstack_load_blocks_async": (I32, [VP, I32, I32, VP, VP, VP, VP, VP]),
         "bitstack_set_num_blocks": (I32, [VP, I32]),
         "bitstack_matmul": (I32, [VP, VP, I32, VP, I32, I64, VP]),
         "bitstack_matmul_grouped": (I32, [P(VP), I32, P(VP), I32, P(VP), I32, I64, VP]),
@@ -192,6 +194,13 @@ class Layer:
         count = int(signs.shape[0]) if signs is not None else 0
         _check(_lib.bitstack_load_blocks(self._h, int(first_block), count, _ptr(signs), _ptr(u),
                                          _ptr(v), _ptr(s), _stream_handle(stream)))
+
+    def load_blocks_async(self, first_block: int, signs, u, v, s=None, stream=None) -> None:
+        """bitstack_load_blocks_async: enqueue the load on `stream` and return; keep the (pinned
+        host or device) buffers alive and unchanged until the stream has passed this call."""
+        count = int(signs.shape[0]) if signs is not None else 0
+        _check(_lib.bitstack_load_blocks_async(self._h, int(first_block), count, _ptr(signs), _ptr(u),
+                                               _ptr(v), _ptr(s), _stream_handle(stream)))
 
     def set_num_blocks(self, n: int) -> None:
         _check(_lib.bitstack_set_num_blocks(self._h, int(n)))

@@ -54,6 +54,60 @@ __global__ void repack_signs_kernel(const uint8_t* __restrict__ canon, uint32_t*
   }
 }
 
+// Fast repack for byte-aligned rows (d_in % 8 == 0), used by the block loads: one thread per
+// (block, local row, 128-column subchunk) with the subchunk index fastest, so a warp reads
+// consecutive 16-byte pieces of one canonical row (coalesced), and stores the row's 16
+// device-layout bytes as one uint4.  Columns >= d_in and rows >= rows_local become 0 bits,
+// as in repack_signs_kernel.  `canon` points at local row 0 of block 0 (the caller copies
+// just the shard's rows); consecutive blocks are `canon_stride` bytes apart.
+// The bit permutation inside a 32-bit word maps the 5-bit column index (layout 1:
+// cl = 4a + b -> 8b + a; layout 0: cl = 2a + b -> 16b + a) and is applied per canonical byte
+// through a 256-entry table: byte k holds columns 8k..8k+7, whose device positions are the
+// table entry of that byte shifted by 2k (layout 1) or 4k (layout 0).
+__global__ void repack_rows_kernel(const uint8_t* __restrict__ canon, long long canon_stride, uint4* __restrict__ dev,
+                                   int count, long long d_in, int nq, int rows_pad, long long rows_local, int layout) {
+  __shared__ uint32_t lut[256];
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    uint32_t o = 0;
+    for (int bit = 0; bit < 8; ++bit)
+      if ((v >> bit) & 1) o |= 1u << col_to_dev_bit(layout, bit);   // column bit of byte 0
+    lut[v] = o;
+  }
+  __syncthreads();
+  const int sh = layout == 1 ? 2 : 4;   // device-position shift per canonical byte
+  const long long per_block = (long long)rows_pad * nq;
+  const long long total = per_block * count;
+  const long long row_bytes = d_in / 8;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int blk = (int)(e / per_block);
+    const long long rem = e % per_block;
+    const int j = (int)(rem / nq);
+    const int q = (int)(rem % nq);
+    uint32_t in[4] = {0u, 0u, 0u, 0u};
+    if (j < rows_local) {
+      const uint8_t* src = canon + blk * canon_stride + j * row_bytes + 16LL * q;
+      const long long nb = row_bytes - 16LL * q;
+      if (nb >= 16 && (reinterpret_cast<uintptr_t>(src) & 3) == 0) {
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(src);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) in[w] = __ldg(s4 + w);
+      } else {
+        for (int b = 0; b < 16 && b < nb; ++b) in[b >> 2] |= (uint32_t)__ldg(src + b) << (8 * (b & 3));
+      }
+    }
+    uint32_t out[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      uint32_t o = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o |= lut[(in[w] >> (8 * k)) & 0xFFu] << (sh * k);
+      out[w] = o;
+    }
+    dev[((long long)blk * nq + q) * rows_pad + j] = make_uint4(out[0], out[1], out[2], out[3]);
+  }
+}
+
 __device__ __forceinline__ float ld_factor(const void* p, long long idx, int dt) {
   if (dt == 0) return reinterpret_cast<const float*>(p)[idx];
   if (dt == 1) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
@@ -110,6 +164,71 @@ __global__ void prep_factors_kernel(const void* __restrict__ u_in, const void* _
     if (c < d_in && r < k) val = ld_factor(v_in, vb + c * k + r, in_dt) * scale[r];
     if (out_dt == 0) reinterpret_cast<float*>(v_out)[ov + e] = val;
     else reinterpret_cast<__nv_bfloat16*>(v_out)[ov + e] = __float2bfloat16_rn(val);
+  }
+}
+
+// Parallel form of prep_factors_kernel for one block (the block loads): factor_max_kernel
+// reduces max_c |V[c, r]| into vmax[16] (float bits as uint: |v| >= 0 orders like its bits;
+// vmax zeroed before), factor_scale_kernel derives the same power-of-two e_r and writes
+// U' = U 2^-e_r, V' = V 2^e_r (rows_pad x 16 and d_in_pad x 16, zero padded) and zscale.
+__global__ void factor_max_kernel(const void* __restrict__ v_in, int in_dt, int k, long long d_in,
+                                  unsigned int* __restrict__ vmax) {
+  __shared__ float red[16];
+  if (threadIdx.x < 16) red[threadIdx.x] = 0.f;
+  __syncthreads();
+  float m[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) m[r] = 0.f;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d_in; c += (long long)gridDim.x * blockDim.x)
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (r < k) m[r] = fmaxf(m[r], fabsf(ld_factor(v_in, c * k + r, in_dt)));
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    float x = m[r];
+    for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<unsigned int*>(&red[r]), __float_as_uint(x));
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) atomicMax(vmax + threadIdx.x, __float_as_uint(red[threadIdx.x]));
+}
+
+__device__ __forceinline__ float factor_scale(const unsigned int* vmax, int r) {
+  const float m = __uint_as_float(vmax[r]);
+  int e = 0;
+  if (m > 0.f && isfinite(m)) {
+    e = (int)floorf(log2f(256.0f / m));
+    e = e > 60 ? 60 : (e < -60 ? -60 : e);
+  }
+  return ldexpf(1.0f, e);
+}
+
+__global__ void factor_scale_kernel(const void* __restrict__ u_in, const void* __restrict__ v_in, int in_dt, int k,
+                                    long long rows_local, int rows_pad, long long d_in, long long d_in_pad,
+                                    const unsigned int* __restrict__ vmax, void* u_out, void* v_out, int out_dt,
+                                    float* zscale_out) {
+  __shared__ float scale[16];
+  if (threadIdx.x < 16) scale[threadIdx.x] = factor_scale(vmax, threadIdx.x);
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < 16 && zscale_out) zscale_out[threadIdx.x] = scale[threadIdx.x];
+  const long long nu = (long long)rows_pad * 16, nv = d_in_pad * 16;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nu + nv;
+       e += (long long)gridDim.x * blockDim.x) {
+    float val = 0.f;
+    if (e < nu) {
+      const long long j = e / 16;
+      const int r = (int)(e % 16);
+      if (j < rows_local && r < k) val = ld_factor(u_in, j * k + r, in_dt) / scale[r];
+      if (out_dt == 0) reinterpret_cast<float*>(u_out)[e] = val;
+      else reinterpret_cast<__nv_bfloat16*>(u_out)[e] = __float2bfloat16_rn(val);
+    } else {
+      const long long ev = e - nu;
+      const long long c = ev / 16;
+      const int r = (int)(ev % 16);
+      if (c < d_in && r < k) val = ld_factor(v_in, c * k + r, in_dt) * scale[r];
+      if (out_dt == 0) reinterpret_cast<float*>(v_out)[ev] = val;
+      else reinterpret_cast<__nv_bfloat16*>(v_out)[ev] = __float2bfloat16_rn(val);
+    }
   }
 }
 

@@ -37,7 +37,7 @@ struct bitstack_layer_s {
   void* v = nullptr;
   float* inv_s = nullptr;
   float* zscale = nullptr;
-  float* y_acc = nullptr;  // [16][rows_pad]
+  float* y_part = nullptr; // [max(sm_count, row_tiles)][kPartStride] split-K partial slots
   uint8_t* zq = nullptr;   // e4m3 path: Zq units of the current call (grown on demand)
   int64_t zq_bytes = 0;
   int* status = nullptr;   // sticky device-side numeric-range flag
@@ -393,7 +393,7 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
   prm.inv_s = L->inv_s;
   prm.x = reinterpret_cast<const uint8_t*>(x) + b0 * L->d_in * xsz;
   prm.y = reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz;
-  prm.y_acc = L->y_acc;
+  prm.y_part = L->y_part;
   prm.counters = L->counters;
   prm.x_stride = L->d_in;
   prm.y_stride = L->rows_local;
@@ -575,7 +575,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   if (e == cudaSuccess) e = alloc(&L->v, v_bytes * n_capacity);
   if (e == cudaSuccess) e = alloc((void**)&L->inv_s, L->d_in_pad * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * 16 * 4);
-  if (e == cudaSuccess) e = alloc((void**)&L->y_acc, (int64_t)16 * L->rows_pad * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->y_part, (int64_t)std::max(L->sm_count, L->row_tiles) * bs::kPartStride * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->status, 16);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -597,7 +597,7 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   cudaFree(L->v);
   cudaFree(L->inv_s);
   cudaFree(L->zscale);
-  cudaFree(L->y_acc);
+  cudaFree(L->y_part);
   cudaFree(L->counters);
   cudaFree(L->status);
   cudaFree(L->zq);
@@ -643,9 +643,9 @@ bitstack_status bitstack_set_num_blocks(bitstack_layer L, int32_t n) {
   return BITSTACK_OK;
 }
 
-bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int32_t count,
-                                     const uint8_t* signs, const void* u, const void* v,
-                                     const float* s, void* stream) {
+// Validation shared by the two load entry points (before any device state changes).
+static bitstack_status check_load_args(bitstack_layer L, int32_t first_block, int32_t count, const uint8_t* signs,
+                                       const void* u, const void* v, const float* s) {
   if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
   if (count < 0) return fail(BITSTACK_E_INVALID_ARG, "count < 0");
   if (first_block < 0 || first_block > L->n_res)
@@ -657,14 +657,10 @@ bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int3
   if (first_block > 0 && s) return fail(BITSTACK_E_INVALID_ARG, "s must be NULL when first_block > 0");
   if (count > 0 && (!signs || !u || !v)) return fail(BITSTACK_E_INVALID_ARG, "NULL block buffer");
   DeviceGuard guard(L->device);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-
   const int64_t nbits = L->d_out * L->d_in;
   const int64_t cbytes = (nbits + 7) / 8;
   const int pad = (int)(cbytes * 8 - nbits);
-  const int fs = dsize(L->fdt);
-
-  // pad-bit validation (SPEC S:203 MalformedBuffer) before touching device state
+  // pad-bit validation (SPEC S:203 MalformedBuffer): one byte per block
   if (count > 0 && pad) {
     const uint8_t mask = (uint8_t)(0xFFu << (8 - pad));
     const bool dev = is_device_ptr(signs);
@@ -690,56 +686,173 @@ bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int3
       if (!(sp[c] > 0.f) || !std::isfinite(sp[c]))
         return fail(BITSTACK_E_INVALID_ARG, "s[%lld] = %g is not a positive finite scale", (long long)c, sp[c]);
   }
+  return BITSTACK_OK;
+}
 
-  if (count > 0) {
-    uint8_t* st_signs = nullptr;
-    void* st_u = nullptr;
-    void* st_v = nullptr;
-    const int64_t ub = (int64_t)count * L->d_out * L->k * fs, vb = (int64_t)count * L->d_in * L->k * fs;
-    CK(cudaMalloc(&st_signs, (size_t)(cbytes * count)));
-    CK(cudaMalloc(&st_u, (size_t)ub));
-    CK(cudaMalloc(&st_v, (size_t)vb));
-    CK(cudaMemcpyAsync(st_signs, signs, (size_t)(cbytes * count), cudaMemcpyDefault, st));
-    CK(cudaMemcpyAsync(st_u, u, (size_t)ub, cudaMemcpyDefault, st));
-    CK(cudaMemcpyAsync(st_v, v, (size_t)vb, cudaMemcpyDefault, st));
-    const int64_t words_per_block = (int64_t)L->nq * L->rows_pad * 4;
-    const int64_t total = words_per_block * count;
+// Per-device staging for block loads: two slots used alternately, each guarded by an event
+// recorded after the kernels that read it, so a slot is refilled (on any stream) only after
+// its previous contents were consumed.  Grow-only; growth waits for the slot's event.
+struct StagePool {
+  std::mutex mu;
+  uint8_t* buf[2] = {nullptr, nullptr};
+  int64_t bytes[2] = {0, 0};
+  cudaEvent_t ev[2] = {nullptr, nullptr};      // slot's last reader (kernels) done
+  cudaEvent_t copied[2] = {nullptr, nullptr};  // slot's copies done
+  cudaEvent_t entry = nullptr;                 // the caller's stream at entry
+  cudaStream_t copy = nullptr;                 // DMA stream: block b+1's copies overlap block b's kernels
+  int next = 0;
+};
+
+// Lazily created per-device pool objects (under pool.mu); grows slot sl to `need` bytes.
+static bitstack_status pool_slot(StagePool& pool, int sl, int64_t need) {
+  if (!pool.copy) {
+    CK(cudaStreamCreateWithFlags(&pool.copy, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&pool.entry, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&pool.ev[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&pool.copied[i], cudaEventDisableTiming));
+    }
+  }
+  if (pool.bytes[sl] < need) {
+    CK(cudaEventSynchronize(pool.ev[sl]));
+    cudaFree(pool.buf[sl]);
+    pool.buf[sl] = nullptr;
+    pool.bytes[sl] = 0;
+    CK(cudaMalloc((void**)&pool.buf[sl], (size_t)need));
+    pool.bytes[sl] = need;
+  }
+  return BITSTACK_OK;
+}
+static StagePool g_stage[64];
+
+// Enqueue the transfer + repack of blocks [first_block, first_block + count): per block, the
+// canonical sign bytes of this handle's rows, its U rows and all of V are copied into a staging
+// slot on the pool's DMA stream (cudaMemcpyAsync: asynchronous from pinned host or device
+// memory; pageable host memory makes the copy synchronous), then `st` waits for the copy and
+// repacks / rebalances from the slot.  Two slots: the copies of block b+1 overlap the kernels
+// of block b.  The DMA stream first waits for `st` (the sources may be produced there).
+static bitstack_status enqueue_blocks(bitstack_layer L, int32_t first_block, int32_t count, const uint8_t* signs,
+                                      const void* u, const void* v, cudaStream_t st) {
+  const int64_t nbits = L->d_out * L->d_in;
+  const int64_t cbytes = (nbits + 7) / 8;
+  const int fs = dsize(L->fdt);
+  const bool rows_aligned = L->d_in % 8 == 0;     // every row starts on a byte: copy the shard only
+  const int64_t sb0 = rows_aligned ? L->row_begin * (L->d_in / 8) : 0;
+  const int64_t sbytes = rows_aligned ? L->rows_local * (L->d_in / 8) : cbytes;
+  const int64_t ubytes = L->rows_local * L->k * fs;
+  const int64_t vbytes = L->d_in * L->k * fs;
+  auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
+  const int64_t need = up(sbytes) + up(ubytes) + up(vbytes) + 64;
+  const int64_t words_per_block = (int64_t)L->nq * L->rows_pad * 4;
+  const int64_t fsd = L->dev_fdt ? 2 : 4;
+  const int in_dt = L->fdt == BITSTACK_F32 ? 0 : (L->fdt == BITSTACK_BF16 ? 1 : 2);
+  StagePool& pool = g_stage[L->device & 63];
+  std::lock_guard<std::mutex> lk(pool.mu);
+  bitstack_status rs = pool_slot(pool, 0, 0);
+  if (rs) return rs;
+  CK(cudaEventRecord(pool.entry, st));
+  CK(cudaStreamWaitEvent(pool.copy, pool.entry, 0));
+  for (int b = 0; b < count; ++b) {
+    const int sl = pool.next;
+    pool.next ^= 1;
+    rs = pool_slot(pool, sl, need);
+    if (rs) return rs;
+    uint8_t* st_signs = pool.buf[sl];
+    uint8_t* st_u = st_signs + up(sbytes);
+    uint8_t* st_v = st_u + up(ubytes);
+    unsigned int* vmax = reinterpret_cast<unsigned int*>(st_v + up(vbytes));
+    const int64_t blk = first_block + b;
+    CK(cudaStreamWaitEvent(pool.copy, pool.ev[sl], 0));          // slot's previous readers done
+    CK(cudaMemcpyAsync(st_signs, signs + b * cbytes + sb0, (size_t)sbytes, cudaMemcpyDefault, pool.copy));
+    CK(cudaMemcpyAsync(st_u, reinterpret_cast<const uint8_t*>(u) + (b * L->d_out + L->row_begin) * L->k * fs,
+                       (size_t)ubytes, cudaMemcpyDefault, pool.copy));
+    CK(cudaMemcpyAsync(st_v, reinterpret_cast<const uint8_t*>(v) + b * vbytes, (size_t)vbytes, cudaMemcpyDefault,
+                       pool.copy));
+    CK(cudaMemsetAsync(vmax, 0, 64, pool.copy));
+    CK(cudaEventRecord(pool.copied[sl], pool.copy));
+    CK(cudaStreamWaitEvent(st, pool.copied[sl], 0));
+    uint32_t* dst = reinterpret_cast<uint32_t*>(L->signs) + blk * words_per_block;
     const int threads = 256;
-    const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 65536);
-    bs::repack_signs_kernel<<<blocks, threads, 0, st>>>(
-        st_signs, reinterpret_cast<uint32_t*>(L->signs) + (int64_t)first_block * words_per_block, count,
-        cbytes, L->d_in, L->nq, L->rows_pad, L->rows_local, L->row_begin, L->layout);
+    const int cap = L->sm_count * 8;
+    if (rows_aligned) {
+      const int64_t total = (int64_t)L->rows_pad * L->nq;
+      const int grid = (int)std::min<int64_t>((total + threads - 1) / threads, cap);
+      bs::repack_rows_kernel<<<grid, threads, 0, st>>>(st_signs, sbytes, reinterpret_cast<uint4*>(dst), 1, L->d_in,
+                                                       L->nq, L->rows_pad, L->rows_local, L->layout);
+    } else {
+      const int grid = (int)std::min<int64_t>((words_per_block + threads - 1) / threads, 65536);
+      bs::repack_signs_kernel<<<grid, threads, 0, st>>>(st_signs, dst, 1, cbytes, L->d_in, L->nq, L->rows_pad,
+                                                        L->rows_local, L->row_begin, L->layout);
+    }
     count_launch();
     CK(cudaGetLastError());
-    const int64_t fsd = L->dev_fdt ? 2 : 4;
-    uint8_t* u_dst = reinterpret_cast<uint8_t*>(L->u) + (int64_t)first_block * L->rows_pad * 16 * fsd;
-    uint8_t* v_dst = reinterpret_cast<uint8_t*>(L->v) + (int64_t)first_block * L->d_in_pad * 16 * fsd;
-    const int in_dt = L->fdt == BITSTACK_F32 ? 0 : (L->fdt == BITSTACK_BF16 ? 1 : 2);
-    bs::prep_factors_kernel<<<count, 256, 0, st>>>(st_u, st_v, in_dt, L->k, L->d_out, L->d_in,
-                                                    L->row_begin, L->rows_local, L->rows_pad,
-                                                    L->d_in_pad, u_dst, v_dst, L->dev_fdt ? 1 : 0,
-                                                    L->zscale + (int64_t)first_block * 16);
+    uint8_t* u_dst = reinterpret_cast<uint8_t*>(L->u) + blk * L->rows_pad * 16 * fsd;
+    uint8_t* v_dst = reinterpret_cast<uint8_t*>(L->v) + blk * L->d_in_pad * 16 * fsd;
+    const int mgrid = (int)std::min<int64_t>((L->d_in + threads - 1) / threads, L->sm_count);
+    bs::factor_max_kernel<<<mgrid, threads, 0, st>>>(st_v, in_dt, L->k, L->d_in, vmax);
     count_launch();
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
-    cudaFree(st_signs);
-    cudaFree(st_u);
-    cudaFree(st_v);
+    const int64_t elems = ((int64_t)L->rows_pad + L->d_in_pad) * 16;
+    const int sgrid = (int)std::min<int64_t>((elems + threads - 1) / threads, cap);
+    bs::factor_scale_kernel<<<sgrid, threads, 0, st>>>(st_u, st_v, in_dt, L->k, L->rows_local, L->rows_pad, L->d_in,
+                                                        L->d_in_pad, vmax, u_dst, v_dst, L->dev_fdt ? 1 : 0,
+                                                        L->zscale + blk * 16);
+    count_launch();
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(pool.ev[sl], st));
+  }
+  return BITSTACK_OK;
+}
+
+// 1/s into the handle (Eq.4), staged like the blocks (on `st` only: it is tiny).
+static bitstack_status enqueue_scale(bitstack_layer L, const float* s, cudaStream_t st) {
+  StagePool& pool = g_stage[L->device & 63];
+  std::lock_guard<std::mutex> lk(pool.mu);
+  const int sl = pool.next;
+  pool.next ^= 1;
+  bitstack_status rs = pool_slot(pool, sl, L->d_in * 4);
+  if (rs) return rs;
+  CK(cudaStreamWaitEvent(st, pool.ev[sl], 0));
+  float* st_s = reinterpret_cast<float*>(pool.buf[sl]);
+  CK(cudaMemcpyAsync(st_s, s, (size_t)(L->d_in * 4), cudaMemcpyDefault, st));
+  bs::inv_s_kernel<<<(int)((L->d_in_pad + 255) / 256), 256, 0, st>>>(st_s, L->inv_s, L->d_in, L->d_in_pad);
+  count_launch();
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(pool.ev[sl], st));
+  return BITSTACK_OK;
+}
+
+static bitstack_status load_blocks_impl(bitstack_layer L, int32_t first_block, int32_t count, const uint8_t* signs,
+                                        const void* u, const void* v, const float* s, void* stream, bool wait) {
+  bitstack_status rs = check_load_args(L, first_block, count, signs, u, v, s);
+  if (rs) return rs;
+  DeviceGuard guard(L->device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (count > 0) {
+    rs = enqueue_blocks(L, first_block, count, signs, u, v, st);
+    if (rs) return rs;
   }
   if (s) {
-    float* st_s = nullptr;
-    CK(cudaMalloc(&st_s, L->d_in * 4));
-    CK(cudaMemcpyAsync(st_s, s, L->d_in * 4, cudaMemcpyDefault, st));
-    bs::inv_s_kernel<<<(int)((L->d_in_pad + 255) / 256), 256, 0, st>>>(st_s, L->inv_s, L->d_in, L->d_in_pad);
-    count_launch();
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
-    cudaFree(st_s);
+    rs = enqueue_scale(L, s, st);
+    if (rs) return rs;
   }
+  if (wait) CK(cudaStreamSynchronize(st));
   L->n_res = first_block + count;
   L->n_act = std::min(L->n_act, L->n_res);
   if (first_block == 0 && count > 0 && L->n_act == 0) L->n_act = L->n_res;
   return BITSTACK_OK;
+}
+
+bitstack_status bitstack_load_blocks(bitstack_layer L, int32_t first_block, int32_t count,
+                                     const uint8_t* signs, const void* u, const void* v,
+                                     const float* s, void* stream) {
+  return load_blocks_impl(L, first_block, count, signs, u, v, s, stream, true);
+}
+
+bitstack_status bitstack_load_blocks_async(bitstack_layer L, int32_t first_block, int32_t count,
+                                           const uint8_t* signs, const void* u, const void* v,
+                                           const float* s, void* stream) {
+  return load_blocks_impl(L, first_block, count, signs, u, v, s, stream, false);
 }
 
 // bitstack_matmul with device-accessible x / y (device memory, or pinned host memory read /

@@ -473,11 +473,10 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
       }
     }
 #undef BS_TRACE
-    if (active && nunits > 0) {
-      const int row = row0 + t * kTileRows + row_in_tile;
+    if (active) {   // this CTA's partial y -> its split-K slot (zeros if it had no units)
 #pragma unroll
       for (int b = 0; b < NB; ++b)
-        if (b < p.batch) atomicAdd(p.y_acc + (long long)b * p.rows_pad + row, yacc[b]);
+        if (b < p.batch) store_partial(p, (int)blockIdx.x, R * kTileRows, t * kTileRows + row_in_tile, b, yacc[b]);
     }
   }
 
@@ -502,20 +501,7 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
   __syncthreads();
   if (*last_flag) {
     __threadfence();
-    const int rows_in_group = Rg * kTileRows;
-    const int total = rows_in_group * p.batch;
-    for (int e = threadIdx.x; e < total; e += C::kThreads) {
-      const int b = e / rows_in_group;
-      const int row = row0 + e % rows_in_group;
-      float* src = p.y_acc + (long long)b * p.rows_pad + row;
-      const float val = __ldcg(src);
-      *src = 0.f;
-      if (row < p.rows_local) {
-        const long long o = (long long)b * p.y_stride + row;
-        if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = val;
-        else reinterpret_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(val);
-      }
-    }
+    finalize_group(p, g, R * kTileRows, Rg, row0);
     if (threadIdx.x == 0) p.counters[g] = 0;
   }
 }

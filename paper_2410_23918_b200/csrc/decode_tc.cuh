@@ -47,7 +47,7 @@ struct DecodeParams {
   const float* inv_s;   // [d_in_pad], 1/s, 0 in the pad
   const void* x;        // [batch][x_stride]
   void* y;              // [batch][y_stride]
-  float* y_acc;         // [16][rows_pad] fp32 workspace, zero on entry and on exit
+  float* y_part;        // [grid][kPartStride] fp32 split-K partials, one slot per CTA (no init needed)
   int* counters;        // [n_groups], zero on entry and on exit
   long long x_stride, y_stride;
   int n, nq, rows_pad, rows_local, d_in, d_in_pad, row_tiles, n_groups, ctas_per_group;
@@ -59,6 +59,52 @@ struct DecodeParams {
   const uint8_t* zq;              // e4m3 kernel: Zq units built by zq_kernel (else null)
   int* status;                    // sticky numeric-range flag (e4m3 kernel), may be null
 };
+
+// Split-K reduction, shared by every decode kernel.  Each CTA stores the
+// partial y of its row group (R*128 rows x batch) into its own slot; the last CTA of the group
+// to finish sums the group's slots in CTA order, so y does not depend on which CTA finished
+// first (bitwise reproducible for a given launch shape).  R*128*NB <= 1024 in every config.
+constexpr int kPartStride = 1024;
+
+__device__ __forceinline__ void store_partial(const DecodeParams& p, int cta, int group_rows, int r, int b,
+                                              float v) {
+  p.y_part[(long long)cta * kPartStride + b * group_rows + r] = v;
+}
+
+// Called by every thread of the last CTA of row group g (after the group counter said so).
+__device__ __forceinline__ void finalize_group(const DecodeParams& p, int g, int group_rows, int Rg, int row0) {
+  const int rows_in_group = Rg * kTileRows;
+  const int total = rows_in_group * p.batch;
+  const float* base = p.y_part + (long long)g * p.ctas_per_group * kPartStride;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int b = e / rows_in_group;
+    const int r = e % rows_in_group;
+    const float* src = base + b * group_rows + r;
+    // all loads of a batch are issued before the (in-order) adds: one L2 round trip per 16 CTAs
+    float acc = 0.f;
+    int j = 0;
+    for (; j + 16 <= p.ctas_per_group; j += 16) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = __ldcg(src + (long long)(j + i) * kPartStride);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc += v[i];
+    }
+    {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = (j + i < p.ctas_per_group) ? __ldcg(src + (long long)(j + i) * kPartStride) : 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc += v[i];
+    }
+    const int row = row0 + r;
+    if (row < p.rows_local) {
+      const long long o = (long long)b * p.y_stride + row;
+      if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = acc;
+      else reinterpret_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(acc);
+    }
+  }
+}
 
 __device__ __forceinline__ float load_act(const void* p, long long idx, int dt) {
   if (dt == 0) return __ldg(reinterpret_cast<const float*>(p) + idx);
@@ -512,17 +558,14 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const Deco
         if (lane == 0) mbar_arrive(acc_empty);
       }
     }
-    // ---- fold this CTA's partial y into the fp32 workspace
-    if (u1 > u0) {
+    // ---- this CTA's partial y -> its split-K slot (zeros if it had no units)
 #pragma unroll
-      for (int a = 0; a < kMyTiles; ++a) {
-        const int t = wg + 2 * a;
-        if (t < Rg) {
-          const int row = row0 + t * kTileRows + row_in_tile;
+    for (int a = 0; a < kMyTiles; ++a) {
+      const int t = wg + 2 * a;
+      if (t < Rg) {
 #pragma unroll
-          for (int b = 0; b < NB; ++b)
-            if (b < p.batch) atomicAdd(p.y_acc + (long long)b * p.rows_pad + row, yacc[a][b]);
-        }
+        for (int b = 0; b < NB; ++b)
+          if (b < p.batch) store_partial(p, blockIdx.x, R * kTileRows, t * kTileRows + row_in_tile, b, yacc[a][b]);
       }
     }
   }
@@ -543,20 +586,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const Deco
   __syncthreads();
   if (*last_flag) {
     __threadfence();
-    const int rows_in_group = Rg * kTileRows;
-    const int total = rows_in_group * p.batch;
-    for (int e = threadIdx.x; e < total; e += kDecodeThreads) {
-      const int b = e / rows_in_group;
-      const int row = row0 + e % rows_in_group;
-      float* src = p.y_acc + (long long)b * p.rows_pad + row;
-      const float val = __ldcg(src);
-      *src = 0.f;
-      if (row < p.rows_local) {
-        const long long o = (long long)b * p.y_stride + row;
-        if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = val;
-        else reinterpret_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(val);
-      }
-    }
+    finalize_group(p, g, R * kTileRows, Rg, row0);
     if (threadIdx.x == 0) p.counters[g] = 0;
   }
 }

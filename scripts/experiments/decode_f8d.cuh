@@ -1,4 +1,6 @@
 // EXPERIMENT (not built into the library; needs an int* wq [n_groups] field in DecodeParams):
+// (Written against the round-1 atomicAdd y workspace `p.y_acc`; the library now uses per-CTA
+// split-K slots -- replace its fold/finalise with store_partial / finalize_group to rebuild.)
 // dynamic unit assignment; correct but 27.9 us vs 24.4 us static (shorter accumulation runs ->
 // more drains, atomics on the producer path).  DESIGN.md §6.2.
 // e4m3 decode kernel: per-warpgroup issuer warps + DYNAMIC unit assignment.

@@ -1,4 +1,6 @@
 // EXPERIMENT (not built into the library): group-pipelined decode kernel, measured 33 us vs
+// (Written against the round-1 atomicAdd y workspace `p.y_acc`; the library now uses per-CTA
+// split-K slots -- replace its fold/finalise with store_partial / finalize_group to rebuild.)
 // 29.8 us for decode_f8_kernel on C2 n=16 B=1. Kept for the record; to try it,
 // include it from bitstack.cu and launch decode_f8g_kernel<NB, 2> with R = 2 row tiles per CTA.
 // Group-pipelined variant of the e4m3 decode kernel.

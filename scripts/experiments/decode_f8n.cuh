@@ -1,4 +1,6 @@
 // EXPERIMENT (not built into the library): MMA warp fed by named barriers; measured 28.7 us vs
+// (Written against the round-1 atomicAdd y workspace `p.y_acc`; the library now uses per-CTA
+// split-K slots -- replace its fold/finalise with store_partial / finalize_group to rebuild.)
 // 28.3 us for decode_f8_kernel on C2 n=16 B=1.
 // e4m3 decode kernel with a dedicated MMA warp fed through NAMED barriers.
 //

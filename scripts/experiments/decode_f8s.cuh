@@ -1,4 +1,6 @@
 // EXPERIMENT (not built into the library): staggered warpgroups (4 chains on different units,
+// (Written against the round-1 atomicAdd y workspace `p.y_acc`; the library now uses per-CTA
+// split-K slots -- replace its fold/finalise with store_partial / finalize_group to rebuild.)
 // shared double-buffered accumulators); correct, measured 31.8 us vs 28.3 us.
 // e4m3 decode kernel with STAGGERED warpgroups -- the production decode
 // kernel for bf16 / fp16 factors.

@@ -316,6 +316,82 @@ def test_host_buffers(bs, batch):
     assert O.relative_l2(y_dev.numpy().astype(np.float64), ref) <= 1e-3
 
 
+# ------------------------------------------------------------------ block streaming (async load)
+@pytest.mark.parametrize("shape,rows", [((640, 1024), None), ((520, 1000), (130, 390)), ((300, 200), (0, 300)),
+                                        ((256, 100), (64, 256))])
+def test_async_load_streaming_matches_sync(bs, shape, rows):
+    """bitstack_load_blocks_async from pinned host memory on a side stream, blocks pushed in
+    pieces (row shards with d_in % 8 == 0 copy only the shard's bytes; d_in % 8 != 0 falls
+    back to full-block staging): after the stream passes, the device state is bit-identical
+    to the synchronous load (fp32 reconstruct compared exactly) and y matches the oracle."""
+    d_out, d_in = shape
+    r0, r1 = rows or (0, d_out)
+    g, s32, blocks = compress_case(d_out, d_in, 5, "bf16", 151 + d_in)
+    signs, u, v = stack_blocks(blocks, "bf16")
+    ref_lay = bs.Layer(d_out, d_in, k=16, n_capacity=5, factor_dtype="bf16", row_begin=r0, row_end=r1)
+    ref_lay.load_blocks(0, signs, u, v, s32)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16) if a.dtype == np.uint16 else np.ascontiguousarray(a)).pin_memory()
+    ps, pu, pv, pss = pin(signs), pin(u), pin(v), pin(s32)
+    lay = bs.Layer(d_out, d_in, k=16, n_capacity=5, factor_dtype="bf16", row_begin=r0, row_end=r1)
+    side = torch.cuda.Stream()
+    lay.load_blocks_async(0, ps[:2], pu[:2], pv[:2], pss, stream=side)
+    assert lay.info()["n_resident"] == 2
+    lay.load_blocks_async(2, ps[2:], pu[2:], pv[2:], stream=side)
+    ev = torch.cuda.Event()
+    ev.record(side)
+    torch.cuda.current_stream().wait_event(ev)
+    assert lay.info()["n_resident"] == 5
+    for n in (1, 3, 5):
+        lay.set_num_blocks(n)
+        ref_lay.set_num_blocks(n)
+        assert torch.equal(lay.reconstruct(torch.float32), ref_lay.reconstruct(torch.float32))
+    x = make_x(2, g, 8)
+    y, xr = gpu_y(lay, x)
+    full = oracle_y(blocks, s32, 5, xr)
+    assert O.relative_l2(y, full[:, r0:r1]) <= 1e-3
+
+
+def test_async_load_overlaps_matmul_on_another_stream(bs):
+    """Streaming a new block into one handle on a side stream while another handle keeps
+    computing on the main stream; the new level is used only after an event wait."""
+    g, s32, blocks = compress_case(512, 1024, 4, "bf16", 171)
+    signs, u, v = stack_blocks(blocks, "bf16")
+    busy = make_layer(bs, 512, 1024, blocks, s32, "bf16")
+    lay = make_layer(bs, 512, 1024, blocks[:2], s32, "bf16", n_capacity=4)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16) if a.dtype == np.uint16 else np.ascontiguousarray(a)).pin_memory()
+    ps, pu, pv = pin(signs[2:]), pin(u[2:]), pin(v[2:])
+    x = torch.from_numpy(make_x(1, g, 3).astype(np.float32)).cuda()
+    side = torch.cuda.Stream()
+    lay.load_blocks_async(2, ps, pu, pv, stream=side)
+    ys = [busy.matmul(x) for _ in range(50)]          # main stream keeps working meanwhile
+    ev = torch.cuda.Event()
+    ev.record(side)
+    torch.cuda.current_stream().wait_event(ev)
+    assert lay.info()["n_active"] == 2                # a push never raises the active level
+    lay.set_num_blocks(4)
+    y = lay.matmul(x)
+    torch.cuda.synchronize()
+    xr = x.cpu().numpy().astype(np.float64)
+    assert O.relative_l2(y.cpu().numpy().astype(np.float64), oracle_y(blocks, s32, 4, xr)) <= 1e-3
+    assert all(torch.equal(a, ys[0]) for a in ys)
+
+
+# ------------------------------------------------------------------ H7: deterministic split-K
+@pytest.mark.parametrize("dtype,batch", [("bf16", 1), ("bf16", 3), ("f32", 1), ("f32", 5)])
+def test_split_k_reduction_is_deterministic(bs, dtype, batch):
+    """Split-K partials are summed in CTA order by the last CTA of each row group (no float
+    atomics): repeated calls give bitwise identical y, with many CTAs per row group."""
+    g, s32, blocks = compress_case(512, 2048, 6, dtype, 131)
+    lay = make_layer(bs, 512, 2048, blocks, s32, dtype)
+    x = torch.from_numpy(make_x(batch, g, 17).astype(np.float32)).cuda()
+    y0 = lay.matmul(x)
+    for _ in range(20):
+        assert torch.equal(lay.matmul(x), y0)
+    torch.cuda.synchronize()
+    ref = oracle_y(blocks, s32, 6, x.cpu().numpy().astype(np.float64))
+    assert O.relative_l2(y0.cpu().numpy().astype(np.float64), ref) <= (1e-3 if dtype == "bf16" else 1e-5)
+
+
 # ------------------------------------------------------------------ grouped decode launches
 def _grouped_case(bs, shapes, seed):
     out = []
