@@ -146,10 +146,21 @@ bool decode_issuer() {
   return v;
 }
 
-template <int NB> struct F8Geom;   // R: row tiles per CTA
-template <> struct F8Geom<1> { static constexpr int R = 4; };
-template <> struct F8Geom<2> { static constexpr int R = 2; };
-template <> struct F8Geom<4> { static constexpr int R = 2; };
+// e4m3 decode geometry per batch class: R row tiles per CTA, P units per hand-off
+// (decode_f8i.cuh).  TMEM: R x 2 x P x 32 A columns + R x 48 NB accumulator columns <= 512.
+#ifndef BS_F8_R1
+#define BS_F8_R1 4
+#endif
+#ifndef BS_F8_P1
+#define BS_F8_P1 1
+#endif
+#ifndef BS_F8_P2
+#define BS_F8_P2 2
+#endif
+template <int NB> struct F8Geom;
+template <> struct F8Geom<1> { static constexpr int R = BS_F8_R1, P = BS_F8_P1; };
+template <> struct F8Geom<2> { static constexpr int R = 2, P = BS_F8_P2; };
+template <> struct F8Geom<4> { static constexpr int R = 2, P = 1; };
 
 // Z workspace of layer L for `units` (block, 128-column chunk) pairs at batch class NB; grows
 // once per larger batch class (a stream sync + cudaMalloc), never inside steady state.
@@ -187,12 +198,12 @@ template <int NB>
 bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_in, int grid, cudaStream_t st) {
   using G = F8Geom<NB>;
   using C = bs::DecodeF8Cfg<NB, G::R>;
-  using CI = bs::DecodeF8ICfg<NB, G::R>;
+  using CI = bs::DecodeF8ICfg<NB, G::R, G::P>;
   static bool attr_done = false;
   if (!attr_done) {
     CK(cudaFuncSetAttribute(bs::decode_f8_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             C::kSmemBytes));
-    CK(cudaFuncSetAttribute(bs::decode_f8i_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(bs::decode_f8i_kernel<NB, G::R, G::P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             CI::kSmemBytes));
     attr_done = true;
   }
@@ -220,7 +231,7 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (iss) CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_kernel<NB, G::R>, prm));
+  if (iss) CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_kernel<NB, G::R, G::P>, prm));
   else CK(cudaLaunchKernelEx(&cfg, bs::decode_f8_kernel<NB, G::R>, prm));
   count_launch();
   return BITSTACK_OK;
@@ -425,11 +436,11 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
 template <int NB>
 bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const void* const* xs, int xdt,
                                          int xsz, void* const* ys, int ydt, int ysz, int bc, cudaStream_t st) {
-  constexpr int R = F8Geom<NB>::R;
-  using CI = bs::DecodeF8ICfg<NB, R>;
+  constexpr int R = F8Geom<NB>::R, P = F8Geom<NB>::P;
+  using CI = bs::DecodeF8ICfg<NB, R, P>;
   static bool attr_done = false;
   if (!attr_done) {
-    CK(cudaFuncSetAttribute(bs::decode_f8i_grouped_kernel<NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(bs::decode_f8i_grouped_kernel<NB, R, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             CI::kSmemBytes));
     attr_done = true;
   }
@@ -491,7 +502,7 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_grouped_kernel<NB, R>, dg));
+  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_grouped_kernel<NB, R, P>, dg));
   count_launch();
   return record_prof(st, false, &slot);
 }
@@ -906,7 +917,7 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
     const int bc = (int)std::min<int64_t>(nbmax, batch - b0);
     int nb = 1;
     while (nb < bc) nb <<= 1;
-    const int R = f8 ? (nb == 1 ? F8Geom<1>::R : F8Geom<2>::R) : r_tiles_for(nb, 2);
+    const int R = f8 ? (nb == 1 ? F8Geom<1>::R : (nb == 2 ? F8Geom<2>::R : F8Geom<4>::R)) : r_tiles_for(nb, 2);
     const int n_groups = (L->row_tiles + R - 1) / R;
     const int64_t units = (int64_t)L->n_act * L->nq;
     int cpg = std::max(1, L->sm_count / n_groups);

@@ -2,40 +2,40 @@
 //
 // Same computation and operands as decode_f8_kernel (decode_f8.cuh).  Each of the R
 // warpgroups owns a row tile and has 4 expander warps (TMEM lane quadrants) plus its own
-// issuer warp.  The expanders hand each tile to their issuer through a double-buffered named
-// barrier (bar.arrive by the 128 expander threads, bar.sync by the issuer), so they never
-// wait for MMA issue; one expander polls the stage / slot mbarriers one unit ahead and the
-// 4 expanders meet on a named "go" barrier.  Measured motivation (scripts/exp_decode.sh):
-// the per-unit chain of hand-offs, not data movement or math, bounds the kernel; taking the
-// ~250-cycle elected MMA block off the expanders' chain shortens it.
-// Double-buffering the tile barriers by unit parity is race-free: the expanders reach unit
-// k+2 only after their A slot (NSLOT = 2) was released by the MMAs of unit k, which the
-// issuer issued after its bar.sync of unit k.
+// issuer warp.  Work moves in GROUPS of up to P consecutive units of one block (a unit = one
+// 128-column subchunk): the producer fills one ring stage per group, the expanders expand the
+// group's P sign tiles into one A slot (P x 32 TMEM columns) and hand it to their issuer
+// through a named barrier (bar.arrive by the 128 expander threads, bar.sync by the issuer),
+// so they never wait for MMA issue; the issuer polls the stage / slot mbarriers one group
+// ahead and releases the expanders for the next group on a named "go" barrier before issuing
+// the group's 4P MMAs.  P > 1 amortises the per-hand-off synchronisation and control code
+// over P units.  Measured motivation (scripts/exp_decode.sh): the per-unit chain of
+// hand-offs, not data movement or math, bounds the kernel.
 #pragma once
 #include "decode_f8.cuh"
 
 namespace bs {
 
-template <int NB, int R_>
+template <int NB, int R_, int P_ = 1>
 struct DecodeF8ICfg {
   static constexpr int N = ZqCfg<NB>::N;
   static constexpr int R = R_;                               // row tiles = warpgroups
+  static constexpr int P = P_;                               // units per group (hand-off)
   static constexpr int kThreads = 32 * (5 * R + 1);          // R x (4 expanders + issuer) + producer
   static constexpr int kWarpProducer = 5 * R;
   static constexpr int kZBytes = ZqCfg<NB>::kZBytes;
   static constexpr int kZUnit = ZqCfg<NB>::kZUnit;
-  static constexpr int kSignBytes = R * kTileRows * 16;
-  static constexpr int kOffZ = kSignBytes;
-  static constexpr int kOffMeta = kOffZ + kZBytes;
-  static constexpr int kStageBytes = (kOffZ + kZUnit + 127) / 128 * 128;
+  static constexpr int kUnitSign = R * kTileRows * 16;       // sign bytes of one unit (R row tiles)
+  static constexpr int kOffZ = P * kUnitSign;                // Zq of unit u at kOffZ + u kZUnit
+  static constexpr int kStageBytes = (kOffZ + P * kZUnit + 127) / 128 * 128;
   static constexpr int S0 = (200 * 1024) / kStageBytes;
   static constexpr int STAGES = S0 > 12 ? 12 : (S0 < 2 ? 2 : S0);
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes;
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr int kACols = 32;                          // 128 rows x 128 e4m3 per tile
+  static constexpr int kACols = 32;                          // 128 rows x 128 e4m3 per unit
   static constexpr int NSLOT = 2;                            // A slots per row tile
-  static constexpr uint32_t kAccCol = R * NSLOT * kACols;
+  static constexpr uint32_t kAccCol = R * NSLOT * P * kACols;
   static constexpr uint32_t LBO = (N / 8) * 128;
   static constexpr uint32_t SBO = 128;
   static_assert(N <= 256 && N % 16 == 0, "invalid MMA N");
@@ -43,14 +43,24 @@ struct DecodeF8ICfg {
   static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
   static_assert(2 * R <= 15, "named barriers 1..2R");
   static_assert(5 * R + 1 <= 32, "warps");
+  static_assert(kZUnit % 16 == 0, "Zq unit alignment (smem descriptor)");
 };
+
+// Units [k, k + cnt) of a CTA's range form one group: at most P, never across a block end.
+template <int P>
+__device__ __forceinline__ int group_count(int k, int q, int nunits, int nq) {
+  if constexpr (P == 1) return 1;
+  int c = nq - q;
+  c = c < P ? c : P;
+  return c < nunits - k ? c : nunits - k;
+}
 
 // The kernel body, for CTA `cta` of the launch that computes the layer described by p
 // (decode_f8i_kernel: one layer, cta = cta; decode_f8i_grouped_kernel: several).
-template <int NB, int R_>
+template <int NB, int R_, int P_>
 __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int cta) {
-  using C = DecodeF8ICfg<NB, R_>;
-  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT;
+  using C = DecodeF8ICfg<NB, R_, P_>;
+  constexpr int N = C::N, R = C::R, P = C::P, STAGES = C::STAGES, NSLOT = C::NSLOT;
   extern __shared__ __align__(1024) uint8_t smem[];
 
   uint8_t* bar_area = smem + STAGES * C::kStageBytes;
@@ -75,8 +85,8 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
   const int row0 = g * R * kTileRows;
   // named barriers of warpgroup w: go = 1 + 2w (issuer arrives, expanders sync), tile-ready =
   // 2 + 2w (expanders arrive, issuer syncs).  Single-buffered is race-free: the issuer
-  // releases unit k+1 only after syncing on unit k's tile, and the expanders arrive on unit
-  // k+1's tile only after that release.
+  // releases group k+1 only after syncing on group k's tile, and the expanders arrive on
+  // group k+1's tile only after that release.
 #ifdef BS_DECODE_TRACE
   long long* trace = (p.dbg_acc && cta == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
   const long long tstart = clock64();
@@ -111,80 +121,106 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
       const uint64_t pol_sign = policy_evict_first();
       const uint64_t pol_keep = policy_evict_last();
       const uint32_t sign_bytes = (uint32_t)Rg * kTileRows * 16;
-      const int pre = nunits < STAGES ? nunits : STAGES;
-      int i = i_start, q = q_start;
-      for (int k = 0; k < pre; ++k) {  // first `pre` stages: sign tiles before the dependency wait
-        mbar_arrive_expect_tx(&full[k], sign_bytes + C::kZUnit);
-        bulk_g2s(smem + k * C::kStageBytes, p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0, sign_bytes,
-                 &full[k], pol_sign);
-        if (++q == p.nq) { q = 0; ++i; }
+      // first STAGES groups: sign tiles before the dependency wait, then their Zq
+      int k = 0, q = q_start, gi = 0;
+      long long ui = (long long)i_start * p.nq;   // i * nq of the current block
+      for (; gi < STAGES && k < nunits; ++gi) {
+        const int cnt = group_count<P>(k, q, nunits, p.nq);
+        mbar_arrive_expect_tx(&full[gi], (uint32_t)cnt * (sign_bytes + C::kZUnit));
+        for (int u = 0; u < cnt; ++u)
+          bulk_g2s(smem + gi * C::kStageBytes + u * C::kUnitSign, p.signs + (ui + q + u) * p.rows_pad + row0,
+                   sign_bytes, &full[gi], pol_sign);
+        k += cnt;
+        q += cnt;
+        if (q == p.nq) { q = 0; ui += p.nq; }
       }
+      const int pre = gi;
       asm volatile("griddepcontrol.wait;" ::: "memory");  // Zq of this call is complete and visible
-      for (int k = 0; k < pre; ++k)
-        bulk_g2s(smem + k * C::kStageBytes + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, C::kZUnit, &full[k], pol_keep);
+      {
+        int kk = 0, qq = q_start;
+        for (int g2 = 0; g2 < pre; ++g2) {
+          const int cnt = group_count<P>(kk, qq, nunits, p.nq);
+          bulk_g2s(smem + g2 * C::kStageBytes + C::kOffZ, p.zq + (u0 + kk) * C::kZUnit,
+                   (uint32_t)cnt * C::kZUnit, &full[g2], pol_keep);
+          kk += cnt;
+          qq += cnt;
+          if (qq == p.nq) qq = 0;
+        }
+      }
       int s = pre % STAGES;
       uint32_t ph = pre == STAGES ? 1u : 0u;
-      for (int k = pre; k < nunits; ++k) {
+      while (k < nunits) {
+        const int cnt = group_count<P>(k, q, nunits, p.nq);
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + s * C::kStageBytes;
-        mbar_arrive_expect_tx(&full[s], sign_bytes + C::kZUnit);
-        bulk_g2s(st, p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0, sign_bytes, &full[s], pol_sign);
-        bulk_g2s(st + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, C::kZUnit, &full[s], pol_keep);
-        if (++q == p.nq) { q = 0; ++i; }
+        mbar_arrive_expect_tx(&full[s], (uint32_t)cnt * (sign_bytes + C::kZUnit));
+        for (int u = 0; u < cnt; ++u)
+          bulk_g2s(st + u * C::kUnitSign, p.signs + (ui + q + u) * p.rows_pad + row0, sign_bytes, &full[s], pol_sign);
+        bulk_g2s(st + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, (uint32_t)cnt * C::kZUnit, &full[s], pol_keep);
+        k += cnt;
+        q += cnt;
+        if (q == p.nq) { q = 0; ui += p.nq; }
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp % 5 == 4) {
     // ================= issuer of warpgroup t =================
-    // Polls the stage / slot mbarriers of unit k+1 while the expanders work on unit k, and
-    // releases them for unit k+1 (bar.arrive "go") as soon as unit k's tile is in TMEM --
-    // before issuing unit k's MMAs, so expansion of k+1 overlaps MMA issue of k.
+    // Polls the stage / slot mbarriers of group k+1 while the expanders work on group k, and
+    // releases them for group k+1 (bar.arrive "go") as soon as group k's tile is in TMEM --
+    // before issuing group k's MMAs, so expansion of k+1 overlaps MMA issue of k.
     const int t = warp / 5;
     if (t < Rg) {
       constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(kTileRows >> 4) << 24);
       const uint64_t bdesc_s0 = smem_desc_kmajor(smem_u32(smem + C::kOffZ), C::LBO, C::SBO);
       const uint32_t d_acc = tbase + C::kAccCol + (uint32_t)(t * N);
       const int bar_go = 1 + 2 * t, bar_tile = 2 + 2 * t;
-      int s = 0, slot = 0, q = q_start;
-      uint32_t ph = 0, sph = 0;
-      int sn = 0, slotn = 0;                 // stage / slot of unit k+1
+      int s = 0, slot = 0, q = q_start, k = 0, gk = 0;
+      int sn = 0, slotn = 0;                 // stage / slot of group gk+1
       uint32_t phn = 0, sphn = 0;
       mbar_wait(&full[0], 0);
       mbar_wait(&a_empty[t * NSLOT], 1);
       asm volatile("bar.arrive %0, 160;" ::"r"(bar_go) : "memory");
-      for (int k = 0; k < nunits; ++k) {
+      while (k < nunits) {
+        const int cnt = group_count<P>(k, q, nunits, p.nq);
         const bool first = (k == 0) || (q == 0);
-        const bool last = (k == nunits - 1) || (q == p.nq - 1);
+        const bool last = (k + cnt == nunits) || (q + cnt == p.nq);
         if (++sn == STAGES) { sn = 0; phn ^= 1; }
         if (++slotn == NSLOT) { slotn = 0; sphn ^= 1; }
-        if (k + 1 < nunits) {
+        if (k + cnt < nunits) {
           mbar_wait(&full[sn], phn);
           mbar_wait(&a_empty[t * NSLOT + slotn], sphn ^ 1);
         }
-        if (t == 3) BS_ITRACE(k, 8);
-        asm volatile("bar.sync %0, 160;" ::"r"(bar_tile) : "memory");   // unit k's tile in TMEM
-        if (k + 1 < nunits) asm volatile("bar.arrive %0, 160;" ::"r"(bar_go) : "memory");
-        if (t == 3) BS_ITRACE(k, 9);
+        if (t == 1) BS_ITRACE(gk, 8);
+        asm volatile("bar.sync %0, 160;" ::"r"(bar_tile) : "memory");   // group k's tile in TMEM
+        if (k + cnt < nunits) asm volatile("bar.arrive %0, 160;" ::"r"(bar_go) : "memory");
+        if (t == 1) BS_ITRACE(gk, 9);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t bdesc0 = bdesc_s0 + (uint64_t)((s * C::kStageBytes) >> 4);
-          const uint32_t a_col = tbase + (uint32_t)(C::kACols * (t * NSLOT + slot));
+          const uint32_t a_col = tbase + (uint32_t)(C::kACols * P * (t * NSLOT + slot));
 #pragma unroll
-          for (int m = 0; m < kSubK / 32; ++m)
-            mma_f8_ts(d_acc, a_col + 8 * m, bdesc0 + (uint64_t)((m * 2 * C::LBO) >> 4), idesc,
-                      (m > 0 || !first) ? 1u : 0u);
+          for (int u = 0; u < P; ++u) {
+            if (u < cnt) {
+#pragma unroll
+              for (int m = 0; m < kSubK / 32; ++m)
+                mma_f8_ts(d_acc, a_col + (uint32_t)(C::kACols * u + 8 * m),
+                          bdesc0 + (uint64_t)((u * C::kZUnit + m * 2 * C::LBO) >> 4), idesc,
+                          (m > 0 || u > 0 || !first) ? 1u : 0u);
+            }
+          }
           mma_commit(&a_empty[t * NSLOT + slot]);
           mma_commit(&empty[s]);
           if (last) mma_commit(&acc_full[t]);
         }
         __syncwarp();
-        if (t == 3) BS_ITRACE(k, 10);
-        s = sn; ph = phn;
-        slot = slotn; sph = sphn;
-        if (++q == p.nq) q = 0;
+        if (t == 1) BS_ITRACE(gk, 10);
+        s = sn;
+        slot = slotn;
+        k += cnt;
+        q += cnt;
+        if (q == p.nq) q = 0;
+        ++gk;
       }
-      (void)ph;
-      (void)sph;
     }
   } else {
     // ================= expander warps of warpgroup wg (TMEM lane quadrant = warp % 4) =================
@@ -199,59 +235,67 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
     float yacc[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) yacc[b] = 0.f;
-    int s = 0, i = i_start, q = q_start;
+    int s = 0, i = i_start, q = q_start, k = 0, gk = 0;
     uint32_t acc_ph = 0;
     int E = kZqSentinel;                   // set by the CTA's first non-empty unit
     // per-thread constant addresses: this row's 16-byte sign vector in stage 0, the two A slots
     const uint32_t sw_addr0 = smem_u32(smem) + (uint32_t)((t * kTileRows + row_in_tile) * 16);
-    const uint32_t meta_addr0 = smem_u32(smem) + (uint32_t)C::kOffMeta;
-    uint32_t a_addr = tbase + (uint32_t)(C::kACols * t * NSLOT) + lane_base;
-    const uint32_t a_flip = (uint32_t)C::kACols;   // slot 0 <-> slot 1 (NSLOT = 2)
+    const uint32_t meta_addr0 = smem_u32(smem) + (uint32_t)(C::kOffZ + C::kZBytes);
+    const uint32_t a_slot0 = tbase + (uint32_t)(C::kACols * P * t * NSLOT) + lane_base;
+    uint32_t a_addr = a_slot0;
+    const uint32_t a_flip = a_slot0 ^ (a_slot0 + (uint32_t)(C::kACols * P));   // slot 0 <-> slot 1
     static_assert(NSLOT == 2, "slot toggle");
-    for (int k = 0; active && k < nunits; ++k) {
-      const bool last = (k == nunits - 1) || (q == p.nq - 1);
-      if (warp == 15) BS_ITRACE(k, 0);
+    const long long row_abs = row0 + t * kTileRows + row_in_tile;
+    while (active && k < nunits) {
+      const int cnt = group_count<P>(k, q, nunits, p.nq);
+      const bool last = (k + cnt == nunits) || (q + cnt == p.nq);
+      if (warp == 5) BS_ITRACE(gk, 0);
       asm volatile("bar.sync %0, 160;" ::"r"(bar_go) : "memory");   // stage full, slot free
-      if (warp == 15) BS_ITRACE(k, 1);
+      if (warp == 5) BS_ITRACE(gk, 1);
       tc_fence_after();
       const uint32_t so = (uint32_t)(s * C::kStageBytes);
-      uint4 sw;
-      int e_u;
-      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(sw.x), "=r"(sw.y), "=r"(sw.z), "=r"(sw.w)
-                   : "r"(sw_addr0 + so));
-      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(e_u) : "r"(meta_addr0 + so));
-      // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit; E = e_u of
-      // the CTA's first non-empty unit (the same in every warpgroup)
-      if (E == kZqSentinel) E = e_u;
-      const int a_raw = (e_u == kZqSentinel) ? 0 : E - e_u;
-      const int a_exp = min(max(a_raw, -6), 8);
-      if (a_exp != a_raw && lane == 0 && p.status) atomicOr(p.status, 1);   // beyond the e4m3 A range
-      const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
-      {
-        uint32_t o[32];
-        expand_e4m3(sw.x, e8, o);
-        expand_e4m3(sw.y, e8, o + 8);
-        expand_e4m3(sw.z, e8, o + 16);
-        expand_e4m3(sw.w, e8, o + 24);
-        tmem_st32(a_addr, o);
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (u < cnt) {
+          uint4 sw;
+          int e_u;
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(sw.x), "=r"(sw.y), "=r"(sw.z), "=r"(sw.w)
+                       : "r"(sw_addr0 + so + (uint32_t)(u * C::kUnitSign)));
+          asm volatile("ld.shared.b32 %0, [%1];" : "=r"(e_u) : "r"(meta_addr0 + so + (uint32_t)(u * C::kZUnit)));
+          // A = +-2^a with a = E - e_u, so that A * (Z 2^e_u) = +-Z 2^E for every unit; E = e_u
+          // of the CTA's first non-empty unit (the same in every warpgroup)
+          if (E == kZqSentinel) E = e_u;
+          const int a_raw = (e_u == kZqSentinel) ? 0 : E - e_u;
+          const int a_exp = min(max(a_raw, -6), 8);
+          if (a_exp != a_raw && lane == 0 && p.status) atomicOr(p.status, 1);   // beyond the e4m3 A range
+          const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
+          uint32_t o[32];
+          expand_e4m3(sw.x, e8, o);
+          expand_e4m3(sw.y, e8, o + 8);
+          expand_e4m3(sw.z, e8, o + 16);
+          expand_e4m3(sw.w, e8, o + 24);
+          tmem_st32(a_addr + (uint32_t)(C::kACols * u), o);
+        }
       }
-      if (warp == 15) BS_ITRACE(k, 2);
+      if (warp == 5) BS_ITRACE(gk, 2);
       tmem_st_wait();
-      if (warp == 15) BS_ITRACE(k, 3);
+      if (warp == 5) BS_ITRACE(gk, 3);
       tc_fence_before();
       asm volatile("bar.arrive %0, 160;" ::"r"(bar_tile) : "memory");   // quarter in TMEM
       a_addr ^= a_flip;
       if (++s == STAGES) s = 0;
       const int ci = i;
-      if (++q == p.nq) { q = 0; ++i; }
-      if (warp == 15) BS_ITRACE(k, 4);
+      k += cnt;
+      q += cnt;
+      if (q == p.nq) { q = 0; ++i; }
+      if (warp == 5) BS_ITRACE(gk, 4);
+      ++gk;
 
       if (last) {
         // ---- epilogue for block ci: y += 2^-E sum_r U'_ci[row, r] (T_d0 + T_d1 + T_d2)[row, r]
         float uu[16];
         {
-          const long long row = row0 + t * kTileRows + row_in_tile;
-          const long long base = ((long long)ci * p.rows_pad + row) * 16;
+          const long long base = ((long long)ci * p.rows_pad + row_abs) * 16;
           if (p.f_dtype == 1) {
             const uint4* up = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.u) + base);
             const uint4 r0v = __ldg(up), r1v = __ldg(up + 1);
@@ -332,9 +376,9 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
   }
 }
 
-template <int NB, int R_>
-__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_kernel(const DecodeParams p) {
-  decode_f8i_body<NB, R_>(p, (int)blockIdx.x);
+template <int NB, int R_, int P_>
+__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_, P_>::kThreads, 1) decode_f8i_kernel(const DecodeParams p) {
+  decode_f8i_body<NB, R_, P_>(p, (int)blockIdx.x);
 }
 
 // Grouped launch (bitstack_matmul_grouped): layers [0, count) of one launch, CTAs
@@ -347,11 +391,11 @@ struct DecodeGroup {
   DecodeParams prm[kMaxGroup];
 };
 
-template <int NB, int R_>
-__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_>::kThreads, 1) decode_f8i_grouped_kernel(const __grid_constant__ DecodeGroup grp) {
+template <int NB, int R_, int P_>
+__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_, P_>::kThreads, 1) decode_f8i_grouped_kernel(const __grid_constant__ DecodeGroup grp) {
   int i = 0;
   while (i + 1 < grp.count && (int)blockIdx.x >= grp.cta_start[i + 1]) ++i;
-  decode_f8i_body<NB, R_>(grp.prm[i], (int)blockIdx.x - grp.cta_start[i]);
+  decode_f8i_body<NB, R_, P_>(grp.prm[i], (int)blockIdx.x - grp.cta_start[i]);
 }
 
 }  // namespace bs
