@@ -96,11 +96,12 @@ def main(r, key="c2_n16_b1_g1"):
              f"{'kernel':60s} {'launches':>8s} {'avg_us':>10s} {'total_us':>11s} {'share':>7s}"]
     agg = launches(lp)
     tot = sum(sum(v) for v in agg.values())
-    steady = {k: v for k, v in agg.items() if "repack" not in k and "prep_factors" not in k and "inv_s" not in k}
+    steady = {k: v for k, v in agg.items()
+              if not any(t in k for t in ("repack", "prep_factors", "inv_s", "factor_max", "factor_scale"))}
     tot_steady = sum(sum(v) for v in steady.values())
     for k, v in agg.items():
         lines.append(f"{k:60s} {len(v):8d} {sum(v) / len(v):10.2f} {sum(v):11.1f} {sum(v) / tot:7.3f}")
-    lines.append("# per-call share (excluding one-off load_blocks kernels: repack/prep/inv_s):")
+    lines.append("# per-call share (excluding one-off load_blocks kernels: repack / factor prep / inv_s):")
     for k, v in steady.items():
         lines.append(f"#   {k:56s} {sum(v) / tot_steady:6.3f}")
     open(os.path.join(ROOT, "profiles", f"{r}_launches.txt"), "w").write("\n".join(lines) + "\n")
