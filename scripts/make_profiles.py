@@ -90,9 +90,9 @@ def prefill(r, key="c3_up_n8_b2048_g1"):
 def main(r, key="c2_n16_b1_g1"):
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     lp = os.path.join(ROOT, "gpurun_out", f"launches_{r}.csv")
-    lines = [f"# ncu launch list of `python bench.py --steps 40 --warmup 5 --no-cpu-baseline --no-graph`",
+    lines = [f"# ncu launch list (-k regex:'zq_kernel|decode_f8i') of `python bench.py --steps 40 --warmup 5 --no-cpu-baseline --no-graph`",
              "# (--metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised: PDL overlap",
-             "#  of zq_kernel with decode_f8_kernel is lost under ncu, so compare SHARES, not absolutes)",
+             "#  of zq_kernel with decode_f8i_kernel is lost under ncu, so compare SHARES, not absolutes)",
              f"{'kernel':60s} {'launches':>8s} {'avg_us':>10s} {'total_us':>11s} {'share':>7s}"]
     agg = launches(lp)
     tot = sum(sum(v) for v in agg.values())
