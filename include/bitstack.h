@@ -194,6 +194,35 @@ BITSTACK_API int64_t bitstack_block_size_bits(int64_t m, int64_t n, int32_t k, i
 /* Thread-local message of the last error on this thread ("" if none). */
 BITSTACK_API const char* bitstack_last_error(void);
 
+/* ---- GPU compression (Alg.1 P:423-445 for one weight matrix) ----
+ * Produces the stored form that bitstack_load_blocks takes, on the device:
+ *   s_c = ||x_cal[:, c]||_2 clamped at 1e-8 max_c s_c (Eq.3; reading R5),
+ *   R_0 = W diag(s) (Eq.4), and for i < n (Eq.5-7):
+ *     S_i = sign(R_i) with sign(0) = +1 (reading R6), packed canonically,
+ *     |R_i| ~= a diag(sigma) b^T, the top-k singular triplets by seeded randomized subspace
+ *       iteration (ell = min(k + oversample, d_out, d_in) columns, `power_iters` power
+ *       iterations each re-orthonormalised by QR; reading of §8(c) "SVD method"),
+ *     U_i = a sqrt(sigma), V_i = b sqrt(sigma) (Eq.2 balanced split), the largest-|entry| of
+ *       each a_r made positive, rounded to factor_dtype (RNE),
+ *     R_{i+1} = R_i - S_i (.) U_i V_i^T with the ROUNDED factors (reading R8).
+ * All buffers are device memory on one device (E_INVALID_ARG otherwise):
+ *   w      [d_out, d_in] f32 row-major         x_cal [p, d_in] f32 row-major (calibration X)
+ *   signs  out [n][ceil(d_out d_in / 8)] u8    u out [n][d_out][k], v out [n][d_in][k] (factor_dtype)
+ *   s      out [d_in] f32                      sigma out [n][k] f32 (may be NULL)
+ *   resid  out [n + 1] f32 = ||R_0||_F .. ||R_n||_F (may be NULL)
+ * 1 <= k <= min(d_out, d_in, 32), ell <= 64.  The skinny GEMMs with |R| and the tall-skinny
+ * products run in cuBLAS (fp32 SGEMM, no TF32); the QR is CholeskyQR2 and the SVD of the
+ * small projected matrix goes through its ell x ell Gram matrix (Jacobi eigensolver): those
+ * ell x ell steps and the element-wise / reduction steps run in this library's kernels.
+ * The Gaussian test matrix of block i is Philox(seed + 7919 i) (so factor values
+ * differ from the CPU oracle's numpy generator; SVD outputs are compared by invariants).
+ * Workspace ~2 d_out d_in x 4 bytes, allocated per call.  Returns after `stream` has
+ * finished the work.  Errors: E_INVALID_ARG, E_OOM, E_CUDA. */
+BITSTACK_API bitstack_status bitstack_compress(const float* w, const float* x_cal, int64_t p, int64_t d_out,
+                                  int64_t d_in, int32_t n, int32_t k, bitstack_dtype factor_dtype,
+                                  int32_t oversample, int32_t power_iters, uint64_t seed, uint8_t* signs,
+                                  void* u, void* v, float* s, float* sigma, float* resid, void* stream);
+
 /* ---- measurement hooks (used by bench.py; not part of the paper's problem) ----
  * While enabled, the dominant kernel launch of every bitstack_matmul call (decode:
  * the Zq + decode kernel pair; SIMT: its kernel; prefill: the GEMM) is bracketed

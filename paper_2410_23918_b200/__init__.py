@@ -2,6 +2,6 @@
 ~1-bit residual blocks, as hand-written sm_100a CUDA behind a C ABI
 (include/bitstack.h).  Python here is argument marshalling only."""
 from .bitstack import (  # noqa: F401
-    BF16, F16, F32, BitStackError, Group, Layer, block_size_bits, launch_count, load_library, matmul_grouped,
+    BF16, F16, F32, BitStackError, Group, Layer, block_size_bits, compress, launch_count, load_library, matmul_grouped,
     profile_begin, profile_end,
 )

@@ -29,7 +29,7 @@ EXPORTED_SYMBOLS = (
     "bitstack_create", "bitstack_destroy", "bitstack_load_blocks", "bitstack_load_blocks_async",
     "bitstack_set_num_blocks",
     "bitstack_matmul", "bitstack_matmul_grouped", "bitstack_reconstruct", "bitstack_get_info", "bitstack_set_kernel",
-    "bitstack_block_size_bits", "bitstack_last_error", "bitstack_profile_begin",
+    "bitstack_block_size_bits", "bitstack_last_error", "bitstack_compress", "bitstack_profile_begin",
     "bitstack_profile_end", "bitstack_launch_count",
 )
 
@@ -81,6 +81,8 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
         "bitstack_set_kernel": (I32, [VP, I32]),
         "bitstack_block_size_bits": (I64, [I64, I64, I32, I32]),
         "bitstack_last_error": (ctypes.c_char_p, []),
+        "bitstack_compress": (I32, [VP, VP, I64, I64, I64, I32, I32, I32, I32, I32, ctypes.c_uint64, VP, VP, VP, VP,
+                                    VP, VP, VP]),
         "bitstack_profile_begin": (I32, [I32]),
         "bitstack_profile_end": (I32, [P(I32), P(ctypes.c_double)]),
         "bitstack_launch_count": (I64, []),
@@ -276,3 +278,28 @@ def matmul_grouped(layers, xs, y_dtype=None, stream=None):
     Group(layers, [_ptr(x) for x in xs], [_ptr(y) for y in ys])(xdt, dtype_code(ys[0].dtype), batch,
                                                                     _stream_handle(stream))
     return ys
+
+
+def compress(w, x_cal, n: int, k: int = 16, factor_dtype="bf16", oversample: int = 16, power_iters: int = 4,
+             seed: int = 0, stream=None):
+    """bitstack_compress (include/bitstack.h): Alg.1 for one matrix on the device.
+    w [d_out, d_in], x_cal [p, d_in]: device float32 tensors.  Returns device tensors
+    (signs [n, nbytes] uint8, u [n, d_out, k], v [n, d_in, k] in factor_dtype, s [d_in] f32,
+    sigma [n, k] f32, resid [n + 1] f32) -- the first four are bitstack_load_blocks' inputs."""
+    import torch
+    lib = load_library()
+    d_out, d_in = int(w.shape[0]), int(w.shape[1])
+    p = int(x_cal.shape[0])
+    fdt = dtype_code(factor_dtype)
+    tdt = {F32: torch.float32, BF16: torch.bfloat16, F16: torch.float16}[fdt]
+    dev = w.device
+    signs = torch.empty((n, (d_out * d_in + 7) // 8), dtype=torch.uint8, device=dev)
+    u = torch.empty((n, d_out, k), dtype=tdt, device=dev)
+    v = torch.empty((n, d_in, k), dtype=tdt, device=dev)
+    s = torch.empty(d_in, dtype=torch.float32, device=dev)
+    sigma = torch.empty((n, k), dtype=torch.float32, device=dev)
+    resid = torch.empty(n + 1, dtype=torch.float32, device=dev)
+    _check(lib.bitstack_compress(_ptr(w), _ptr(x_cal), p, d_out, d_in, int(n), int(k), fdt, int(oversample),
+                                 int(power_iters), int(seed), _ptr(signs), _ptr(u), _ptr(v), _ptr(s), _ptr(sigma),
+                                 _ptr(resid), _stream_handle(stream)))
+    return signs, u, v, s, sigma, resid

@@ -15,7 +15,10 @@
 #include <vector>
 
 #include "../../include/bitstack.h"
+#include <cublas_v2.h>
+
 #include "aux_kernels.cuh"
+#include "compress.cuh"
 #include "decode_f8.cuh"
 #include "decode_f8i.cuh"
 #include "decode_tc.cuh"
@@ -507,6 +510,30 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
   return record_prof(st, false, &slot);
 }
 
+// Per-device cuBLAS handles (created on first use).
+struct LinalgHandles {
+  std::mutex mu;
+  cublasHandle_t blas = nullptr;
+  void* ws = nullptr;          // cuBLAS workspace (set explicitly: required under stream capture)
+};
+constexpr size_t kBlasWorkspace = 64ull << 20;
+LinalgHandles g_linalg[64];
+
+// Device allocations of one call, freed on every exit path.
+struct Scratch {
+  std::vector<void*> ptrs;
+  ~Scratch() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <typename T>
+  cudaError_t get(T** out, int64_t count) {
+    void* p = nullptr;
+    const cudaError_t e = cudaMalloc(&p, (size_t)std::max<int64_t>(count, 1) * sizeof(T));
+    if (e == cudaSuccess) ptrs.push_back(p);
+    *out = reinterpret_cast<T*>(p);
+    return e;
+  }
+};
 }  // namespace
 
 extern "C" {
@@ -1050,6 +1077,180 @@ bitstack_status bitstack_reconstruct(bitstack_layer L, void* w, bitstack_dtype w
                                                 L->dev_fdt, wdt, L->layout);
   count_launch();
   CK(cudaGetLastError());
+  return BITSTACK_OK;
+}
+
+// ---------------------------------------------------------------- GPU compression
+
+#define CKB(call)                                                                         \
+  do {                                                                                    \
+    cublasStatus_t b_ = (call);                                                           \
+    if (b_ != CUBLAS_STATUS_SUCCESS) return fail(BITSTACK_E_CUDA, "%s failed: cuBLAS status %d", #call, (int)b_); \
+  } while (0)
+bitstack_status bitstack_compress(const float* w, const float* x_cal, int64_t p, int64_t d_out, int64_t d_in,
+                                  int32_t n, int32_t k, bitstack_dtype factor_dtype, int32_t oversample,
+                                  int32_t power_iters, uint64_t seed, uint8_t* signs, void* u, void* v, float* s,
+                                  float* sigma, float* resid, void* stream) {
+  if (!w || !x_cal || !s || (n > 0 && (!signs || !u || !v))) return fail(BITSTACK_E_INVALID_ARG, "NULL argument");
+  if (d_out < 1 || d_in < 1 || p < 1 || n < 0 || oversample < 0 || power_iters < 0)
+    return fail(BITSTACK_E_INVALID_ARG, "bad sizes");
+  if (k < 1 || k > std::min<int64_t>(d_out, d_in) || k > 32)
+    return fail(BITSTACK_E_INVALID_ARG, "k=%d outside [1, min(d_out, d_in, 32)]", k);
+  if (!valid_dtype(factor_dtype)) return fail(BITSTACK_E_INVALID_ARG, "bad factor dtype");
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, w) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return fail(BITSTACK_E_INVALID_ARG, "w must be device memory");
+  }
+  const void* outs[] = {x_cal, s, signs, u, v, sigma, resid};
+  for (const void* q : outs)
+    if (q && !is_device_ptr(q)) return fail(BITSTACK_E_INVALID_ARG, "all buffers must be device memory");
+  DeviceGuard guard(pa.device);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  LinalgHandles& H = g_linalg[pa.device & 63];
+  std::lock_guard<std::mutex> lk(H.mu);
+  if (!H.blas) CKB(cublasCreate(&H.blas));
+  CKB(cublasSetStream(H.blas, st));
+  CKB(cublasSetMathMode(H.blas, CUBLAS_DEFAULT_MATH));   // fp32 FFMA GEMMs (no TF32)
+
+  const int ell = (int)std::min<int64_t>(k + oversample, std::min(d_out, d_in));
+  if (ell > bs::kSmallMax) return fail(BITSTACK_E_INVALID_ARG, "k + oversample = %d > %d", ell, bs::kSmallMax);
+  const int64_t total = d_out * d_in;
+  const int64_t cbytes = (total + 7) / 8;
+  const int fs = dsize(factor_dtype);
+  const int out_dt = factor_dtype == BITSTACK_F32 ? 0 : (factor_dtype == BITSTACK_BF16 ? 1 : 2);
+  Scratch sc;
+  float *R, *M, *Om, *Y, *Z, *G, *Rinv, *Wv, *Acol, *Bb, *sig, *uf, *vf;
+  double *s2, *sumsq;
+  unsigned long long* smax;
+  CK(sc.get(&R, total));
+  CK(sc.get(&M, total));
+  CK(sc.get(&Om, d_in * ell));
+  CK(sc.get(&Y, d_out * ell));
+  CK(sc.get(&Z, d_in * ell));
+  CK(sc.get(&G, (int64_t)ell * ell));
+  CK(sc.get(&Rinv, (int64_t)ell * ell));
+  CK(sc.get(&Wv, (int64_t)ell * ell));
+  CK(sc.get(&Acol, d_out * k));
+  CK(sc.get(&Bb, d_in * k));
+  CK(sc.get(&sig, ell));
+  CK(sc.get(&uf, d_out * k));
+  CK(sc.get(&vf, d_in * k));
+  CK(sc.get(&s2, d_in));
+  CK(sc.get(&sumsq, n + 1));
+  CK(sc.get(&smax, 1));
+  // The ~100 launches per block (many of them tiny) are recorded once into a CUDA graph: issued
+  // one by one, host launch overhead doubled the wall time of a 4096 x 4096 block.
+  if (!H.ws) {
+    CK(cudaMalloc(&H.ws, kBlasWorkspace));
+    CKB(cublasSetWorkspace(H.blas, H.ws, kBlasWorkspace));
+  }
+  auto body = [&](cudaStream_t st) -> bitstack_status {
+    const float one = 1.f, zero = 0.f;
+    // CholeskyQR: A [m, ell] col-major <- an orthonormal basis of its range (G = A^T A,
+    // G = R^T R, A <- A R^-1 by a triangular solve; rank-deficient directions become ~zero
+    // columns).  One pass inside the power iteration (only the subspace matters there), two
+    // (CholeskyQR2) for the final basis Q.
+    auto qr = [&](float* A, int64_t m, int passes) -> bitstack_status {
+      for (int pass = 0; pass < passes; ++pass) {
+        CKB(cublasSgemm(H.blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, (int)m, &one, A, (int)m, A, (int)m, &zero, G, ell));
+        if (ell <= 32) bs::chol_warp_kernel<<<1, 32, 0, st>>>(G, ell, Rinv);
+        else bs::chol_kernel<<<1, 1024, 0, st>>>(G, ell, Rinv);
+        count_launch();
+        CK(cudaGetLastError());
+        CKB(cublasStrsm(H.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, ell,
+                        &one, Rinv, ell, A, (int)m));                                    // A <- A R^-1
+      }
+      return BITSTACK_OK;
+    };
+    const int T = 256;
+    const int egrid = (int)std::min<int64_t>((total + T - 1) / T, 148 * 16);
+
+    // Eq.3-4: s (fp64 sums of squares, clamped), R_0 = W diag(s)
+    CK(cudaMemsetAsync(s2, 0, d_in * sizeof(double), st));
+    CK(cudaMemsetAsync(smax, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(sumsq, 0, (n + 1) * sizeof(double), st));
+    bs::colsq_kernel<<<dim3((unsigned)((d_in + T - 1) / T), (unsigned)std::min<int64_t>(p, 64)), T, 0, st>>>(x_cal, p, d_in, s2);
+    bs::colmax_kernel<<<(int)std::min<int64_t>((d_in + T - 1) / T, 148), T, 0, st>>>(s2, d_in, smax);
+    bs::scale_clamp_kernel<<<(int)((d_in + T - 1) / T), T, 0, st>>>(s2, smax, d_in, s);
+    bs::scale_w_kernel<<<egrid, T, 0, st>>>(w, s, d_out, d_in, R);
+    bs::sumsq_kernel<<<egrid, T, 0, st>>>(R, total, sumsq);
+    for (int i = 0; i < 5; ++i) count_launch();
+    CK(cudaGetLastError());
+
+    for (int i = 0; i < n; ++i) {
+      // Eq.5: S_i = sign(R), M = |R|
+      bs::sign_abs_kernel<<<egrid, T, 0, st>>>(R, total, signs + (int64_t)i * cbytes, M);
+      bs::gauss_kernel<<<(int)((d_in * ell + T - 1) / T), T, 0, st>>>(Om, d_in * ell, seed + 7919ull * (uint64_t)i);
+      count_launch();
+      count_launch();
+      CK(cudaGetLastError());
+      // top-k SVD of M by randomized subspace iteration (row-major M = col-major M^T, ld d_in)
+      CKB(cublasSgemm(H.blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)d_out, ell, (int)d_in, &one, M, (int)d_in, Om, (int)d_in,
+                      &zero, Y, (int)d_out));                                              // Y = M Om
+      bitstack_status rs = qr(Y, d_out, power_iters > 0 ? 1 : 2);
+      if (rs) return rs;
+      for (int it = 0; it < power_iters; ++it) {
+        CKB(cublasSgemm(H.blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)d_in, ell, (int)d_out, &one, M, (int)d_in, Y,
+                        (int)d_out, &zero, Z, (int)d_in));                                 // Z = M^T Q
+        rs = qr(Z, d_in, 1);
+        if (rs) return rs;
+        CKB(cublasSgemm(H.blas, CUBLAS_OP_T, CUBLAS_OP_N, (int)d_out, ell, (int)d_in, &one, M, (int)d_in, Z,
+                        (int)d_in, &zero, Y, (int)d_out));                                 // Y = M Z
+        rs = qr(Y, d_out, it + 1 == power_iters ? 2 : 1);
+        if (rs) return rs;
+      }
+      CKB(cublasSgemm(H.blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)d_in, ell, (int)d_out, &one, M, (int)d_in, Y, (int)d_out,
+                      &zero, Z, (int)d_in));                                               // Bt = (Q^T M)^T
+      // SVD of B = Q^T M through its Gram matrix: B B^T = Bt^T Bt = W diag(sigma^2) W^T; left
+      // vectors a = Q W, right vectors B^T w / sigma = Bt W / sigma (factor_out divides)
+      CKB(cublasSgemm(H.blas, CUBLAS_OP_T, CUBLAS_OP_N, ell, ell, (int)d_in, &one, Z, (int)d_in, Z, (int)d_in, &zero, G,
+                      ell));
+      bs::symeig_kernel<<<1, 1024, 0, st>>>(G, ell, sig, Wv);
+      count_launch();
+      CK(cudaGetLastError());
+      CKB(cublasSgemm(H.blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)d_out, k, ell, &one, Y, (int)d_out, Wv, ell, &zero, Acol,
+                      (int)d_out));                                                        // a = Q W[:, :k]
+      CKB(cublasSgemm(H.blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)d_in, k, ell, &one, Z, (int)d_in, Wv, ell, &zero, Bb,
+                      (int)d_in));                                                         // Bt W[:, :k]
+      // Eq.2 split + sign convention + storage rounding; Eq.7 residual with the rounded factors
+      bs::factor_out_kernel<<<k, T, 0, st>>>(Acol, d_out, Bb, d_in, sig, d_out, d_in, k, out_dt,
+                                             reinterpret_cast<uint8_t*>(u) + (int64_t)i * d_out * k * fs,
+                                             reinterpret_cast<uint8_t*>(v) + (int64_t)i * d_in * k * fs, uf, vf);
+      bs::residual_kernel<<<dim3((unsigned)((d_in + 255) / 256), (unsigned)((d_out + bs::kResRows - 1) / bs::kResRows)),
+                            256, 0, st>>>(R, uf, vf, d_out, d_in, k, sumsq + i + 1);
+      count_launch();
+      count_launch();
+      CK(cudaGetLastError());
+      if (sigma) CK(cudaMemcpyAsync(sigma + (int64_t)i * k, sig, k * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    }
+    return BITSTACK_OK;
+  };
+  cudaStream_t cap = nullptr;
+  CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  CKB(cublasSetStream(H.blas, cap));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t ce = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+  bitstack_status rs0 = ce == cudaSuccess ? body(cap) : BITSTACK_OK;
+  const cudaError_t ee = cudaStreamEndCapture(cap, &graph);
+  if (ce == cudaSuccess) ce = ee;
+  if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphInstantiate(&exec, graph, 0);
+  if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphLaunch(exec, st);
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(cap);
+  cublasSetStream(H.blas, st);
+  if (rs0) return rs0;
+  if (ce != cudaSuccess) return fail(BITSTACK_E_CUDA, "compress graph: %s", cudaGetErrorString(ce));
+  std::vector<double> hs(n + 1);
+  CK(cudaMemcpyAsync(hs.data(), sumsq, (n + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (resid) {
+    std::vector<float> hr(n + 1);
+    for (int i = 0; i <= n; ++i) hr[i] = (float)std::sqrt(hs[i]);
+    CK(cudaMemcpy(resid, hr.data(), (n + 1) * sizeof(float), cudaMemcpyHostToDevice));
+  }
   return BITSTACK_OK;
 }
 
