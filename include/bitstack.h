@@ -120,9 +120,10 @@ BITSTACK_API bitstack_status bitstack_load_blocks(bitstack_layer layer, int32_t 
  * residuals from storage when available memory increases" (Fig.2) overlapped with
  * compute on other streams.  Same arguments, layouts, validation and errors.  Per block, the
  * canonical sign bytes of this handle's rows (only the shard when d_in % 8 == 0), its U rows
- * and V are copied with cudaMemcpyAsync on `stream` into a per-device staging area (two slots,
- * grown once to the largest block seen; each slot is reused only after an event says its last
- * reader finished), then repacked and rebalanced on `stream`.  The call returns once this is
+ * and V are copied with cudaMemcpyAsync into a per-device staging area (two slots, grown once
+ * to the largest block seen; each slot is reused only after an event says its last reader
+ * finished) on the library's copy stream, which first waits for `stream`; `stream` then waits
+ * for each copy and repacks / rebalances on the device.  The call returns once this is
  * enqueued: from PINNED host memory or device memory the copies are asynchronous and the caller
  * must keep the buffers unchanged until `stream` passes this point (e.g. an event recorded
  * after the call); from pageable host memory cudaMemcpyAsync returns after the data is staged,
