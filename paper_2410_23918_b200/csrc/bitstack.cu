@@ -40,7 +40,7 @@ struct bitstack_layer_s {
   void* v = nullptr;
   float* inv_s = nullptr;
   float* zscale = nullptr;
-  float* y_part = nullptr; // [max(sm_count, row_tiles)][kPartStride] split-K partial slots
+  float* y_part = nullptr; // [max(2 sm_count, row_tiles)][kPartStride] split-K partial slots (<= 2 CTAs/SM)
   uint8_t* zq = nullptr;   // e4m3 path: Zq units of the current call (grown on demand)
   int64_t zq_bytes = 0;
   int* status = nullptr;   // sticky device-side numeric-range flag
@@ -160,10 +160,13 @@ bool decode_issuer() {
 #ifndef BS_F8_P2
 #define BS_F8_P2 2
 #endif
-template <int NB> struct F8Geom;
-template <> struct F8Geom<1> { static constexpr int R = BS_F8_R1, P = BS_F8_P1; };
-template <> struct F8Geom<2> { static constexpr int R = 2, P = BS_F8_P2; };
-template <> struct F8Geom<4> { static constexpr int R = 2, P = 1; };
+#ifndef BS_F8_OCC1
+#define BS_F8_OCC1 1
+#endif
+template <int NB> struct F8Geom;   // OCC: resident decode CTAs per SM (each with 512/OCC TMEM columns)
+template <> struct F8Geom<1> { static constexpr int R = BS_F8_R1, P = BS_F8_P1, OCC = BS_F8_OCC1; };
+template <> struct F8Geom<2> { static constexpr int R = 2, P = BS_F8_P2, OCC = 1; };
+template <> struct F8Geom<4> { static constexpr int R = 2, P = 1, OCC = 1; };
 
 // Z workspace of layer L for `units` (block, 128-column chunk) pairs at batch class NB; grows
 // once per larger batch class (a stream sync + cudaMalloc), never inside steady state.
@@ -201,12 +204,12 @@ template <int NB>
 bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_in, int grid, cudaStream_t st) {
   using G = F8Geom<NB>;
   using C = bs::DecodeF8Cfg<NB, G::R>;
-  using CI = bs::DecodeF8ICfg<NB, G::R, G::P>;
+  using CI = bs::DecodeF8ICfg<NB, G::R, G::P, G::OCC>;
   static bool attr_done = false;
   if (!attr_done) {
     CK(cudaFuncSetAttribute(bs::decode_f8_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             C::kSmemBytes));
-    CK(cudaFuncSetAttribute(bs::decode_f8i_kernel<NB, G::R, G::P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(bs::decode_f8i_kernel<NB, G::R, G::P, G::OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             CI::kSmemBytes));
     attr_done = true;
   }
@@ -234,7 +237,7 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (iss) CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_kernel<NB, G::R, G::P>, prm));
+  if (iss) CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_kernel<NB, G::R, G::P, G::OCC>, prm));
   else CK(cudaLaunchKernelEx(&cfg, bs::decode_f8_kernel<NB, G::R>, prm));
   count_launch();
   return BITSTACK_OK;
@@ -439,11 +442,11 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
 template <int NB>
 bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const void* const* xs, int xdt,
                                          int xsz, void* const* ys, int ydt, int ysz, int bc, cudaStream_t st) {
-  constexpr int R = F8Geom<NB>::R, P = F8Geom<NB>::P;
-  using CI = bs::DecodeF8ICfg<NB, R, P>;
+  constexpr int R = F8Geom<NB>::R, P = F8Geom<NB>::P, OCC = F8Geom<NB>::OCC;
+  using CI = bs::DecodeF8ICfg<NB, R, P, OCC>;
   static bool attr_done = false;
   if (!attr_done) {
-    CK(cudaFuncSetAttribute(bs::decode_f8i_grouped_kernel<NB, R, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(bs::decode_f8i_grouped_kernel<NB, R, P, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             CI::kSmemBytes));
     attr_done = true;
   }
@@ -459,7 +462,7 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
     cpg[i] = 1;
     total += n_groups[i];
   }
-  const int budget = layers[0]->sm_count;
+  const int budget = layers[0]->sm_count * OCC;
   for (;;) {
     int best = -1;
     double best_w = 0.0;
@@ -505,7 +508,7 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_grouped_kernel<NB, R, P>, dg));
+  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_grouped_kernel<NB, R, P, OCC>, dg));
   count_launch();
   return record_prof(st, false, &slot);
 }
@@ -613,7 +616,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   if (e == cudaSuccess) e = alloc(&L->v, v_bytes * n_capacity);
   if (e == cudaSuccess) e = alloc((void**)&L->inv_s, L->d_in_pad * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * 16 * 4);
-  if (e == cudaSuccess) e = alloc((void**)&L->y_part, (int64_t)std::max(L->sm_count, L->row_tiles) * bs::kPartStride * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->y_part, (int64_t)std::max(2 * L->sm_count, L->row_tiles) * bs::kPartStride * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->status, 16);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -945,9 +948,10 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
     int nb = 1;
     while (nb < bc) nb <<= 1;
     const int R = f8 ? (nb == 1 ? F8Geom<1>::R : (nb == 2 ? F8Geom<2>::R : F8Geom<4>::R)) : r_tiles_for(nb, 2);
+    const int occ = f8 ? (nb == 1 ? F8Geom<1>::OCC : (nb == 2 ? F8Geom<2>::OCC : F8Geom<4>::OCC)) : 1;
     const int n_groups = (L->row_tiles + R - 1) / R;
     const int64_t units = (int64_t)L->n_act * L->nq;
-    int cpg = std::max(1, L->sm_count / n_groups);
+    int cpg = std::max(1, occ * L->sm_count / n_groups);
     cpg = (int)std::min<int64_t>(cpg, units);
     const bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
     int slot = -1;

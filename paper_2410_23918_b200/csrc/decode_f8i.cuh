@@ -16,8 +16,9 @@
 
 namespace bs {
 
-template <int NB, int R_, int P_ = 1>
+template <int NB, int R_, int P_ = 1, int OCC_ = 1>
 struct DecodeF8ICfg {
+  static constexpr int OCC = OCC_;                           // resident CTAs per SM (TMEM / smem split)
   static constexpr int N = ZqCfg<NB>::N;
   static constexpr int R = R_;                               // row tiles = warpgroups
   static constexpr int P = P_;                               // units per group (hand-off)
@@ -28,11 +29,11 @@ struct DecodeF8ICfg {
   static constexpr int kUnitSign = R * kTileRows * 16;       // sign bytes of one unit (R row tiles)
   static constexpr int kOffZ = P * kUnitSign;                // Zq of unit u at kOffZ + u kZUnit
   static constexpr int kStageBytes = (kOffZ + P * kZUnit + 127) / 128 * 128;
-  static constexpr int S0 = (200 * 1024) / kStageBytes;
+  static constexpr int S0 = (200 * 1024 / OCC_) / kStageBytes;
   static constexpr int STAGES = S0 > 12 ? 12 : (S0 < 2 ? 2 : S0);
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes;
-  static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kTmemCols = 512 / OCC_;
   static constexpr int kACols = 32;                          // 128 rows x 128 e4m3 per unit
   static constexpr int NSLOT = 2;                            // A slots per row tile
   static constexpr uint32_t kAccCol = R * NSLOT * P * kACols;
@@ -40,7 +41,7 @@ struct DecodeF8ICfg {
   static constexpr uint32_t SBO = 128;
   static_assert(N <= 256 && N % 16 == 0, "invalid MMA N");
   static_assert(kAccCol + R * N <= kTmemCols, "TMEM overflow");
-  static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
+  static_assert(kSmemBytes * OCC_ <= 227 * 1024, "smem overflow");
   static_assert(2 * R <= 15, "named barriers 1..2R");
   static_assert(5 * R + 1 <= 32, "warps");
   static_assert(kZUnit % 16 == 0, "Zq unit alignment (smem descriptor)");
@@ -57,9 +58,9 @@ __device__ __forceinline__ int group_count(int k, int q, int nunits, int nq) {
 
 // The kernel body, for CTA `cta` of the launch that computes the layer described by p
 // (decode_f8i_kernel: one layer, cta = cta; decode_f8i_grouped_kernel: several).
-template <int NB, int R_, int P_>
+template <int NB, int R_, int P_, int OCC_>
 __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int cta) {
-  using C = DecodeF8ICfg<NB, R_, P_>;
+  using C = DecodeF8ICfg<NB, R_, P_, OCC_>;
   constexpr int N = C::N, R = C::R, P = C::P, STAGES = C::STAGES, NSLOT = C::NSLOT;
   extern __shared__ __align__(1024) uint8_t smem[];
 
@@ -376,9 +377,9 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
   }
 }
 
-template <int NB, int R_, int P_>
-__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_, P_>::kThreads, 1) decode_f8i_kernel(const DecodeParams p) {
-  decode_f8i_body<NB, R_, P_>(p, (int)blockIdx.x);
+template <int NB, int R_, int P_, int OCC_>
+__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_, P_, OCC_>::kThreads, OCC_) decode_f8i_kernel(const DecodeParams p) {
+  decode_f8i_body<NB, R_, P_, OCC_>(p, (int)blockIdx.x);
 }
 
 // Grouped launch (bitstack_matmul_grouped): layers [0, count) of one launch, CTAs
@@ -391,11 +392,11 @@ struct DecodeGroup {
   DecodeParams prm[kMaxGroup];
 };
 
-template <int NB, int R_, int P_>
-__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_, P_>::kThreads, 1) decode_f8i_grouped_kernel(const __grid_constant__ DecodeGroup grp) {
+template <int NB, int R_, int P_, int OCC_>
+__global__ void __launch_bounds__(DecodeF8ICfg<NB, R_, P_, OCC_>::kThreads, OCC_) decode_f8i_grouped_kernel(const __grid_constant__ DecodeGroup grp) {
   int i = 0;
   while (i + 1 < grp.count && (int)blockIdx.x >= grp.cta_start[i + 1]) ++i;
-  decode_f8i_body<NB, R_, P_>(grp.prm[i], (int)blockIdx.x - grp.cta_start[i]);
+  decode_f8i_body<NB, R_, P_, OCC_>(grp.prm[i], (int)blockIdx.x - grp.cta_start[i]);
 }
 
 }  // namespace bs

@@ -1,15 +1,15 @@
-export BITSTACK_LIB=$PWD/scripts/libbitstack_drift.so
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "c2 or bf16 or grouped or split or zero or host" > gpurun_out/pt_drift.log 2>&1; echo drift_rc=$?; tail -3 gpurun_out/pt_drift.log
+export BITSTACK_LIB=$PWD/scripts/libbitstack_occ2.so
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "c2 or bf16 or grouped or split or zero or host" > gpurun_out/pt_occ2.log 2>&1; echo occ2_rc=$?; tail -3 gpurun_out/pt_occ2.log
 for rep in 1 2; do
-for v in def drift; do
-  if [ $v = def ]; then unset BITSTACK_LIB; else export BITSTACK_LIB=$PWD/scripts/libbitstack_drift.so; fi
+for v in def occ2; do
+  if [ $v = def ]; then unset BITSTACK_LIB; else export BITSTACK_LIB=$PWD/scripts/libbitstack_occ2.so; fi
   for wl in c2 c5; do timeout 200 python bench.py --workload $wl --steps 1000 --warmup 20 --no-cpu-baseline > gpurun_out/d_${v}_${wl}_$rep.json 2>/dev/null; done
   timeout 200 python bench.py --workload c4 --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/d_${v}_c4_$rep.json 2>/dev/null
 done
 done
 python - <<'P'
 import json
-for v in ("def", "drift"):
+for v in ("def", "occ2"):
     out = []
     for wl in ("c2", "c5", "c4"):
         for rep in (1, 2):
