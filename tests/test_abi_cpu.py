@@ -79,3 +79,29 @@ def test_create_rejects_bad_arguments_without_gpu(lib):
     assert lib.bitstack_matmul(None, None, 0, None, 0, 1, None) == -1
     with pytest.raises(bsmod.BitStackError):
         bsmod.Layer(64, 64, k=0)
+
+
+def test_grouped_load_and_compress_validate_without_gpu(lib):
+    """Host-side validation of the later entry points (no device call needed)."""
+    from paper_2410_23918_b200 import bitstack as bsmod
+    VP = ctypes.c_void_p
+    # grouped: count 0 is a no-op; NULL arrays with count > 0 are rejected
+    assert lib.bitstack_matmul_grouped(None, 0, None, 1, None, 0, 1, None) == 0
+    assert lib.bitstack_matmul_grouped(None, 2, None, 1, None, 0, 1, None) == -1
+    # async load: NULL handle, like the synchronous one
+    assert lib.bitstack_load_blocks_async(None, 0, 1, None, None, None, None, None) == -1
+    assert lib.bitstack_load_blocks(None, 0, 1, None, None, None, None, None) == -1
+    # compress: NULL inputs, bad k, bad sizes -- all before touching a device
+    assert lib.bitstack_compress(None, None, 1, 8, 8, 1, 4, 1, 0, 0, 0, None, None, None, None, None, None, None) == -1
+    dummy = VP(1)
+    assert lib.bitstack_compress(dummy, dummy, 1, 8, 8, 1, 0, 1, 0, 0, 0, dummy, dummy, dummy, dummy, None, None,
+                                 None) == -1                                     # k < 1
+    assert lib.bitstack_compress(dummy, dummy, 1, 64, 64, 1, 33, 1, 0, 0, 0, dummy, dummy, dummy, dummy, None, None,
+                                 None) == -1                                     # k > 32
+    assert b"k=33" in lib.bitstack_last_error()
+    assert lib.bitstack_compress(dummy, dummy, 0, 8, 8, 1, 4, 1, 0, 0, 0, dummy, dummy, dummy, dummy, None, None,
+                                 None) == -1                                     # p < 1
+    # Python-side argument checks of the grouped helpers
+    with pytest.raises(ValueError):
+        bsmod.Group([], [1], [])
+    assert bsmod.matmul_grouped([], []) == []
