@@ -59,7 +59,7 @@ typedef enum {
   BITSTACK_E_CAPACITY = -5,           /* first_block + count > n_capacity */
   BITSTACK_E_OOM = -6,                /* device allocation failed */
   BITSTACK_E_CUDA = -7,               /* CUDA runtime error (message has the CUDA string) */
-  BITSTACK_E_UNSUPPORTED = -8         /* not an sm_100 device, k != 16 on a tensor-core path, ... */
+  BITSTACK_E_UNSUPPORTED = -8         /* not an sm_100 device, a forced path that cannot run, ... */
 } bitstack_status;
 
 /* Kernel selection for bitstack_matmul (bitstack_set_kernel). */
@@ -86,7 +86,10 @@ typedef struct {
  * [row_begin, row_end) (row sharding); capacity n_capacity blocks,
  * rank k, factors stored as factor_dtype (Q7: the paper stores FP16).
  * Allocates all device memory up front on `device`.
- * Errors: E_INVALID_ARG (k<1, k>min(d_out,d_in), k>16, n_capacity<1, bad dtype, out==NULL),
+ * k <= 16 is stored zero-padded to 16 ranks; 16 < k <= 32 (the paper's k ablation)
+ * is stored as two 16-rank halves that share the block's sign tile (every path handles a
+ * half as a block of its own, so the decode streams that sign tile once per half).
+ * Errors: E_INVALID_ARG (k<1, k>min(d_out,d_in), k>32, n_capacity<1, bad dtype, out==NULL),
  *         E_DIM_MISMATCH (bad row range), E_UNSUPPORTED (device not sm_100), E_OOM, E_CUDA. */
 BITSTACK_API bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t n_capacity,
                                 bitstack_dtype factor_dtype, int64_t row_begin, int64_t row_end,
@@ -164,7 +167,7 @@ BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x
  * Each member keeps its own level n_i, dtypes of x / y are shared, xs[i] / ys[i] follow
  * bitstack_matmul's layouts (xs[i] may be the same buffer for several members).
  * When count <= 8, 1 <= batch <= 4, the members are distinct handles on one device on the
- * e4m3 decode path (bf16/f16 factors, k <= 16, d_in % 8 == 0, n_i >= 1, AUTO or TC kernel)
+ * e4m3 decode path (bf16/f16 factors, d_in % 8 == 0, n_i >= 1, AUTO or TC kernel)
  * and all xs / ys are 16-byte aligned device buffers, the whole group runs as ONE Zq launch
  * and ONE decode launch whose CTAs are shared out among the members in proportion to their
  * work; otherwise the members run one after another through bitstack_matmul.  Results are

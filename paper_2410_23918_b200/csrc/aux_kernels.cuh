@@ -171,7 +171,9 @@ __global__ void prep_factors_kernel(const void* __restrict__ u_in, const void* _
 // reduces max_c |V[c, r]| into vmax[16] (float bits as uint: |v| >= 0 orders like its bits;
 // vmax zeroed before), factor_scale_kernel derives the same power-of-two e_r and writes
 // U' = U 2^-e_r, V' = V 2^e_r (rows_pad x 16 and d_in_pad x 16, zero padded) and zscale.
-__global__ void factor_max_kernel(const void* __restrict__ v_in, int in_dt, int k, long long d_in,
+// The input is the stored [rows, ld] factor; columns [col0, col0 + k) (k <= 16) form one rank
+// half (k > 16 is held as two 16-rank halves sharing the sign tile).
+__global__ void factor_max_kernel(const void* __restrict__ v_in, int in_dt, int ld, int col0, int k, long long d_in,
                                   unsigned int* __restrict__ vmax) {
   __shared__ float red[16];
   if (threadIdx.x < 16) red[threadIdx.x] = 0.f;
@@ -182,7 +184,7 @@ __global__ void factor_max_kernel(const void* __restrict__ v_in, int in_dt, int 
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d_in; c += (long long)gridDim.x * blockDim.x)
 #pragma unroll
     for (int r = 0; r < 16; ++r)
-      if (r < k) m[r] = fmaxf(m[r], fabsf(ld_factor(v_in, c * k + r, in_dt)));
+      if (r < k) m[r] = fmaxf(m[r], fabsf(ld_factor(v_in, c * ld + col0 + r, in_dt)));
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     float x = m[r];
@@ -203,8 +205,8 @@ __device__ __forceinline__ float factor_scale(const unsigned int* vmax, int r) {
   return ldexpf(1.0f, e);
 }
 
-__global__ void factor_scale_kernel(const void* __restrict__ u_in, const void* __restrict__ v_in, int in_dt, int k,
-                                    long long rows_local, int rows_pad, long long d_in, long long d_in_pad,
+__global__ void factor_scale_kernel(const void* __restrict__ u_in, const void* __restrict__ v_in, int in_dt, int ld,
+                                    int col0, int k, long long rows_local, int rows_pad, long long d_in, long long d_in_pad,
                                     const unsigned int* __restrict__ vmax, void* u_out, void* v_out, int out_dt,
                                     float* zscale_out) {
   __shared__ float scale[16];
@@ -218,14 +220,14 @@ __global__ void factor_scale_kernel(const void* __restrict__ u_in, const void* _
     if (e < nu) {
       const long long j = e / 16;
       const int r = (int)(e % 16);
-      if (j < rows_local && r < k) val = ld_factor(u_in, j * k + r, in_dt) / scale[r];
+      if (j < rows_local && r < k) val = ld_factor(u_in, j * ld + col0 + r, in_dt) / scale[r];
       if (out_dt == 0) reinterpret_cast<float*>(u_out)[e] = val;
       else reinterpret_cast<__nv_bfloat16*>(u_out)[e] = __float2bfloat16_rn(val);
     } else {
       const long long ev = e - nu;
       const long long c = ev / 16;
       const int r = (int)(ev % 16);
-      if (c < d_in && r < k) val = ld_factor(v_in, c * k + r, in_dt) * scale[r];
+      if (c < d_in && r < k) val = ld_factor(v_in, c * ld + col0 + r, in_dt) * scale[r];
       if (out_dt == 0) reinterpret_cast<float*>(v_out)[ev] = val;
       else reinterpret_cast<__nv_bfloat16*>(v_out)[ev] = __float2bfloat16_rn(val);
     }
@@ -255,7 +257,7 @@ __global__ void __launch_bounds__(128) matmul_simt_kernel(
     const uint4* __restrict__ signs, const void* __restrict__ u, const void* __restrict__ v,
     const float* __restrict__ inv_s, const void* __restrict__ x, void* __restrict__ y, int n,
     int nq, int rows_pad, long long rows_local, long long d_in, long long d_in_pad, int f_dt,
-    int x_dt, int y_dt, long long x_stride, long long y_stride, int layout) {
+    int x_dt, int y_dt, long long x_stride, long long y_stride, int layout, int ksh) {
   __shared__ float zs[128][17];
   const int tile = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int row = tile * 128 + tid;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(128) matmul_simt_kernel(
           zs[tid][r] = ld_dev_factor(v, ((long long)i * d_in_pad + c) * 16 + r, f_dt) * xs;
       }
       __syncthreads();
-      const uint4 sw = signs[((long long)i * nq + q) * rows_pad + row];
+      const uint4 sw = signs[((long long)(i >> ksh) * nq + q) * rows_pad + row];   // rank half i of block i >> ksh
       const uint32_t words[4] = {sw.x, sw.y, sw.z, sw.w};
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
@@ -300,7 +302,7 @@ __global__ void __launch_bounds__(128) matmul_simt_kernel(
 __global__ void __launch_bounds__(256) reconstruct_kernel(
     const uint4* __restrict__ signs, const void* __restrict__ u, const void* __restrict__ v,
     const float* __restrict__ inv_s, void* __restrict__ w, int n, int nq, int rows_pad,
-    long long rows_local, long long d_in, long long d_in_pad, int f_dt, int w_dt, int layout) {
+    long long rows_local, long long d_in, long long d_in_pad, int f_dt, int w_dt, int layout, int ksh) {
   __shared__ float us[8][16];
   __shared__ float vs[32][17];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(256) reconstruct_kernel(
 #pragma unroll
       for (int r = 0; r < 16; ++r) m = fmaf(us[ty][r], vs[tx][r], m);
       const int q = (int)(c / 128), cl = (int)(c % 128);
-      const uint4 sw = signs[((long long)i * nq + q) * rows_pad + row];
+      const uint4 sw = signs[((long long)(i >> ksh) * nq + q) * rows_pad + row];
       const uint32_t words[4] = {sw.x, sw.y, sw.z, sw.w};
       const uint32_t word = words[cl / 32];
       const int pb = col_to_dev_bit(layout, cl % 32);

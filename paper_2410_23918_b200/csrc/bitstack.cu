@@ -29,6 +29,7 @@ struct bitstack_layer_s {
   int rows_pad = 0, nq = 0, row_tiles = 0;
   int64_t d_in_pad = 0;
   int32_t k = 0, n_cap = 0, n_res = 0, n_act = 0;
+  int32_t kh = 1;          // 16-rank halves per block (k > 16: 2, sharing the block's sign tile)
   bitstack_dtype fdt = BITSTACK_BF16;
   int dev_fdt = 1;  // device factor storage: 0 f32, 1 bf16
   int layout = 1;   // device sign layout: 0 = F16 (fp32 factors, fp16 MMA), 1 = F8 (e4m3 MMA)
@@ -177,7 +178,7 @@ bitstack_status ensure_zq(bitstack_layer L, int64_t units, cudaStream_t st) {
   CK(cudaStreamSynchronize(st));
   cudaFree(L->zq);
   L->zq = nullptr;
-  const int64_t cap = (int64_t)L->n_cap * L->nq * C::kZUnit;
+  const int64_t cap = (int64_t)L->n_cap * L->kh * L->nq * C::kZUnit;
   CK(cudaMalloc((void**)&L->zq, (size_t)cap));
   L->bytes += cap - L->zq_bytes;
   L->zq_bytes = cap;
@@ -305,7 +306,8 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
     CK(cudaFuncSetAttribute(bs::wtile_kernel<kWtileG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_done = true;
   }
-  if (L->n_act > 16) return fail(BITSTACK_E_UNSUPPORTED, "prefill path supports n <= 16 active blocks");
+  if (L->n_act * L->kh > 16)
+    return fail(BITSTACK_E_UNSUPPORTED, "prefill path supports n <= 16 active blocks (n <= 8 for k > 16)");
   const int kc = (int)(L->d_in_pad / bs::kPK);
   const int rt_img = (L->row_tiles + 1) / 2 * 2;
   const int nt = (int)((batch + BN - 1) / BN);
@@ -327,7 +329,8 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   wp.u = reinterpret_cast<const __nv_bfloat16*>(L->u);
   wp.v = reinterpret_cast<const __nv_bfloat16*>(L->v);
   wp.img = L->pf_w;
-  wp.n = L->n_act;
+  wp.n = L->n_act * L->kh;
+  wp.ksh = L->kh == 2 ? 1 : 0;
   wp.nq = L->nq;
   wp.rows_pad = L->rows_pad;
   wp.row_tiles = L->row_tiles;
@@ -335,7 +338,7 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   wp.row_tiles_img = rt_img;
   // persistent: 512 / kTmemCols CTAs per SM (G = 2: two CTAs of 256 TMEM columns each)
   const int wgrid = (int)std::min<int64_t>((int64_t)rt_img * kc, (int64_t)L->sm_count * (512 / WC::kTmemCols));
-  bs::wtile_kernel<kWtileG><<<wgrid, WC::kThreads, WC::kSmem(L->n_act), st>>>(wp);
+  bs::wtile_kernel<kWtileG><<<wgrid, WC::kThreads, WC::kSmem(wp.n), st>>>(wp);
   count_launch();
   CK(cudaGetLastError());
 
@@ -414,7 +417,8 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
   prm.counters = L->counters;
   prm.x_stride = L->d_in;
   prm.y_stride = L->rows_local;
-  prm.n = L->n_act;
+  prm.n = L->n_act * L->kh;               // 16-rank halves
+  prm.ksh = L->kh == 2 ? 1 : 0;
   prm.nq = L->nq;
   prm.rows_pad = L->rows_pad;
   prm.rows_local = (int)L->rows_local;
@@ -457,7 +461,7 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
   for (int i = 0; i < count; ++i) {
     bitstack_layer L = layers[i];
     n_groups[i] = (L->row_tiles + R - 1) / R;
-    units[i] = (int64_t)L->n_act * L->nq;
+    units[i] = (int64_t)L->n_act * L->kh * L->nq;
     work[i] = (double)units[i] * L->row_tiles;
     cpg[i] = 1;
     total += n_groups[i];
@@ -562,8 +566,8 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   if (!out) return fail(BITSTACK_E_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (d_out < 1 || d_in < 1) return fail(BITSTACK_E_INVALID_ARG, "dims must be positive");
-  if (k < 1 || k > std::min<int64_t>(d_out, d_in) || k > 16)
-    return fail(BITSTACK_E_INVALID_ARG, "k=%d outside [1, min(d_out, d_in, 16)]", k);
+  if (k < 1 || k > std::min<int64_t>(d_out, d_in) || k > 32)
+    return fail(BITSTACK_E_INVALID_ARG, "k=%d outside [1, min(d_out, d_in, 32)]", k);
   if (n_capacity < 1) return fail(BITSTACK_E_INVALID_ARG, "n_capacity must be >= 1");
   if (!valid_dtype(factor_dtype)) return fail(BITSTACK_E_INVALID_ARG, "bad factor dtype");
   if (row_begin < 0 || row_end > d_out || row_begin >= row_end)
@@ -590,6 +594,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   L->d_in_pad = (d_in + 127) / 128 * 128;
   L->nq = (int)(L->d_in_pad / 128);
   L->k = k;
+  L->kh = k > 16 ? 2 : 1;
   L->n_cap = n_capacity;
   L->fdt = factor_dtype;
   L->dev_fdt = factor_dtype == BITSTACK_BF16 ? 1 : 0;
@@ -599,9 +604,9 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
 
   const int64_t fs = L->dev_fdt ? 2 : 4;
   const int64_t sign_bytes = (int64_t)L->nq * L->rows_pad * 16;
-  const int64_t u_bytes = (int64_t)L->rows_pad * 16 * fs;
+  const int64_t u_bytes = (int64_t)L->rows_pad * 16 * fs;   // per 16-rank half
   const int64_t v_bytes = L->d_in_pad * 16 * fs;
-  L->block_bytes = sign_bytes + u_bytes + v_bytes;
+  L->block_bytes = sign_bytes + L->kh * (u_bytes + v_bytes);
   auto alloc = [&](void** p, int64_t bytes) -> cudaError_t {
     cudaError_t e = cudaMalloc(p, (size_t)bytes);
     if (e == cudaSuccess) {
@@ -612,10 +617,10 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   };
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = alloc((void**)&L->signs, sign_bytes * n_capacity);
-  if (e == cudaSuccess) e = alloc(&L->u, u_bytes * n_capacity);
-  if (e == cudaSuccess) e = alloc(&L->v, v_bytes * n_capacity);
+  if (e == cudaSuccess) e = alloc(&L->u, u_bytes * n_capacity * L->kh);
+  if (e == cudaSuccess) e = alloc(&L->v, v_bytes * n_capacity * L->kh);
   if (e == cudaSuccess) e = alloc((void**)&L->inv_s, L->d_in_pad * 4);
-  if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * 16 * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * L->kh * 16 * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->y_part, (int64_t)std::max(2 * L->sm_count, L->row_tiles) * bs::kPartStride * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->status, 16);
@@ -783,7 +788,7 @@ static bitstack_status enqueue_blocks(bitstack_layer L, int32_t first_block, int
   const int64_t ubytes = L->rows_local * L->k * fs;
   const int64_t vbytes = L->d_in * L->k * fs;
   auto up = [](int64_t x) { return (x + 255) / 256 * 256; };
-  const int64_t need = up(sbytes) + up(ubytes) + up(vbytes) + 64;
+  const int64_t need = up(sbytes) + up(ubytes) + up(vbytes) + 128;   // + vmax[32]
   const int64_t words_per_block = (int64_t)L->nq * L->rows_pad * 4;
   const int64_t fsd = L->dev_fdt ? 2 : 4;
   const int in_dt = L->fdt == BITSTACK_F32 ? 0 : (L->fdt == BITSTACK_BF16 ? 1 : 2);
@@ -809,7 +814,7 @@ static bitstack_status enqueue_blocks(bitstack_layer L, int32_t first_block, int
                        (size_t)ubytes, cudaMemcpyDefault, pool.copy));
     CK(cudaMemcpyAsync(st_v, reinterpret_cast<const uint8_t*>(v) + b * vbytes, (size_t)vbytes, cudaMemcpyDefault,
                        pool.copy));
-    CK(cudaMemsetAsync(vmax, 0, 64, pool.copy));
+    CK(cudaMemsetAsync(vmax, 0, 128, pool.copy));
     CK(cudaEventRecord(pool.copied[sl], pool.copy));
     CK(cudaStreamWaitEvent(st, pool.copied[sl], 0));
     uint32_t* dst = reinterpret_cast<uint32_t*>(L->signs) + blk * words_per_block;
@@ -827,19 +832,25 @@ static bitstack_status enqueue_blocks(bitstack_layer L, int32_t first_block, int
     }
     count_launch();
     CK(cudaGetLastError());
-    uint8_t* u_dst = reinterpret_cast<uint8_t*>(L->u) + blk * L->rows_pad * 16 * fsd;
-    uint8_t* v_dst = reinterpret_cast<uint8_t*>(L->v) + blk * L->d_in_pad * 16 * fsd;
-    const int mgrid = (int)std::min<int64_t>((L->d_in + threads - 1) / threads, L->sm_count);
-    bs::factor_max_kernel<<<mgrid, threads, 0, st>>>(st_v, in_dt, L->k, L->d_in, vmax);
-    count_launch();
-    CK(cudaGetLastError());
-    const int64_t elems = ((int64_t)L->rows_pad + L->d_in_pad) * 16;
-    const int sgrid = (int)std::min<int64_t>((elems + threads - 1) / threads, cap);
-    bs::factor_scale_kernel<<<sgrid, threads, 0, st>>>(st_u, st_v, in_dt, L->k, L->rows_local, L->rows_pad, L->d_in,
-                                                        L->d_in_pad, vmax, u_dst, v_dst, L->dev_fdt ? 1 : 0,
-                                                        L->zscale + blk * 16);
-    count_launch();
-    CK(cudaGetLastError());
+    // factors of rank half h (columns [16h, 16h + 16) of the stored [rows, k] U, V) -> internal
+    // block blk * kh + h; one vmax[16] per half
+    for (int h = 0; h < L->kh; ++h) {
+      const int64_t vb = blk * L->kh + h;
+      const int kc = std::min(16, L->k - 16 * h);
+      uint8_t* u_dst = reinterpret_cast<uint8_t*>(L->u) + vb * L->rows_pad * 16 * fsd;
+      uint8_t* v_dst = reinterpret_cast<uint8_t*>(L->v) + vb * L->d_in_pad * 16 * fsd;
+      const int mgrid = (int)std::min<int64_t>((L->d_in + threads - 1) / threads, L->sm_count);
+      bs::factor_max_kernel<<<mgrid, threads, 0, st>>>(st_v, in_dt, L->k, 16 * h, kc, L->d_in, vmax + 16 * h);
+      count_launch();
+      CK(cudaGetLastError());
+      const int64_t elems = ((int64_t)L->rows_pad + L->d_in_pad) * 16;
+      const int sgrid = (int)std::min<int64_t>((elems + threads - 1) / threads, cap);
+      bs::factor_scale_kernel<<<sgrid, threads, 0, st>>>(st_u, st_v, in_dt, L->k, 16 * h, kc, L->rows_local,
+                                                          L->rows_pad, L->d_in, L->d_in_pad, vmax + 16 * h, u_dst,
+                                                          v_dst, L->dev_fdt ? 1 : 0, L->zscale + vb * 16);
+      count_launch();
+      CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(pool.ev[sl], st));
   }
   return BITSTACK_OK;
@@ -909,7 +920,7 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype);
   // large batch: restored-tile GEMM path (bf16 factors); forced with BITSTACK_KERNEL_PREFILL
-  const bool pf_ok = L->dev_fdt == 1 && L->layout == 1 && L->n_act <= 16;
+  const bool pf_ok = L->dev_fdt == 1 && L->layout == 1 && L->n_act * L->kh <= 16;
   if (L->kernel == BITSTACK_KERNEL_PREFILL && !pf_ok)
     return fail(BITSTACK_E_UNSUPPORTED, "prefill path needs bf16 factors and n <= 16");
   if (L->kernel == BITSTACK_KERNEL_PREFILL || (L->kernel == BITSTACK_KERNEL_AUTO && pf_ok && batch >= kPrefillMinBatch))
@@ -917,7 +928,7 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
 
   // tcgen05 path: k <= 16 (zero-padded columns of U', V'), x rows bulk-copied by the
   // TMA engine -> 16-byte aligned x and d_in % 8 == 0.
-  const bool tc_ok = L->k <= 16 && L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  const bool tc_ok = L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
   const bool use_tc = L->kernel == BITSTACK_KERNEL_TC || (L->kernel == BITSTACK_KERNEL_AUTO && tc_ok);
   if (L->kernel == BITSTACK_KERNEL_TC && !tc_ok)
     return fail(BITSTACK_E_UNSUPPORTED, "tcgen05 decode kernel needs k <= 16, d_in %% 8 == 0 and a 16-byte aligned x");
@@ -931,8 +942,9 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
       dim3 grid(L->row_tiles, nb);
       bs::matmul_simt_kernel<<<grid, 128, 0, st>>>(
           L->signs, L->u, L->v, L->inv_s, reinterpret_cast<const uint8_t*>(x) + b0 * L->d_in * xsz,
-          reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz, L->n_act, L->nq, L->rows_pad,
-          L->rows_local, L->d_in, L->d_in_pad, L->dev_fdt, xdt, ydt, L->d_in, L->rows_local, L->layout);
+          reinterpret_cast<uint8_t*>(y) + b0 * L->rows_local * ysz, L->n_act * L->kh, L->nq, L->rows_pad,
+          L->rows_local, L->d_in, L->d_in_pad, L->dev_fdt, xdt, ydt, L->d_in, L->rows_local, L->layout,
+          L->kh == 2 ? 1 : 0);
       count_launch();
       CK(cudaGetLastError());
       ps = record_prof(st, false, &slot);
@@ -950,7 +962,7 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
     const int R = f8 ? (nb == 1 ? F8Geom<1>::R : (nb == 2 ? F8Geom<2>::R : F8Geom<4>::R)) : r_tiles_for(nb, 2);
     const int occ = f8 ? (nb == 1 ? F8Geom<1>::OCC : (nb == 2 ? F8Geom<2>::OCC : F8Geom<4>::OCC)) : 1;
     const int n_groups = (L->row_tiles + R - 1) / R;
-    const int64_t units = (int64_t)L->n_act * L->nq;
+    const int64_t units = (int64_t)L->n_act * L->kh * L->nq;
     int cpg = std::max(1, occ * L->sm_count / n_groups);
     cpg = (int)std::min<int64_t>(cpg, units);
     const bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
@@ -995,7 +1007,7 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
   // is the kernels' own PCIe traffic.  Everything else is staged through device memory with
   // cudaMemcpyAsync on `stream` (synchronous with respect to pageable host memory).
   const bool pf = L->kernel == BITSTACK_KERNEL_PREFILL ||
-                  (L->kernel == BITSTACK_KERNEL_AUTO && L->dev_fdt == 1 && L->layout == 1 && L->n_act <= 16 &&
+                  (L->kernel == BITSTACK_KERNEL_AUTO && L->dev_fdt == 1 && L->layout == 1 && L->n_act * L->kh <= 16 &&
                    batch >= kPrefillMinBatch);
   const bool plain_io = !pf && (L->layout == 1 || L->kernel == BITSTACK_KERNEL_SIMT) && L->n_act > 0;
   const bool small = xbytes <= (1 << 20) && ybytes <= (1 << 20);
@@ -1044,7 +1056,7 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   for (int i = 0; fused && i < count; ++i) {
     bitstack_layer L = layers[i];
     fused = L && xs[i] && ys[i] && L->device == layers[0]->device && L->layout == 1 && L->n_res > 0 &&
-            L->n_act > 0 && L->n_act <= L->n_res && L->k <= 16 && L->d_in % 8 == 0 &&
+            L->n_act > 0 && L->n_act <= L->n_res && L->d_in % 8 == 0 &&
             (L->kernel == BITSTACK_KERNEL_AUTO || L->kernel == BITSTACK_KERNEL_TC) &&
             (reinterpret_cast<uintptr_t>(xs[i]) % 16) == 0 && mem_kind(xs[i]) == kMemDevice &&
             mem_kind(ys[i]) == kMemDevice;
@@ -1076,9 +1088,9 @@ bitstack_status bitstack_reconstruct(bitstack_layer L, void* w, bitstack_dtype w
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int wdt = w_dtype == BITSTACK_F32 ? 0 : (w_dtype == BITSTACK_BF16 ? 1 : 2);
   dim3 grid((unsigned)((L->d_in + 31) / 32), (unsigned)((L->rows_local + 7) / 8));
-  bs::reconstruct_kernel<<<grid, 256, 0, st>>>(L->signs, L->u, L->v, L->inv_s, w, L->n_act, L->nq,
+  bs::reconstruct_kernel<<<grid, 256, 0, st>>>(L->signs, L->u, L->v, L->inv_s, w, L->n_act * L->kh, L->nq,
                                                 L->rows_pad, L->rows_local, L->d_in, L->d_in_pad,
-                                                L->dev_fdt, wdt, L->layout);
+                                                L->dev_fdt, wdt, L->layout, L->kh == 2 ? 1 : 0);
   count_launch();
   CK(cudaGetLastError());
   return BITSTACK_OK;

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
       int i = i_start, q = q_start;
       for (int k = 0; k < pre; ++k) {  // first `pre` stages: sign tiles before the dependency wait
         mbar_arrive_expect_tx(&full[k], sign_bytes + C::kZUnit);
-        bulk_g2s(smem + k * C::kStageBytes, p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0, sign_bytes,
+        bulk_g2s(smem + k * C::kStageBytes, p.signs + ((long long)(i >> p.ksh) * p.nq + q) * p.rows_pad + row0, sign_bytes,
                  &full[k], pol_sign);
         if (++q == p.nq) { q = 0; ++i; }
       }
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(DecodeF8Cfg<NB, R_>::kThreads, 1) decode_f8_ke
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + s * C::kStageBytes;
         mbar_arrive_expect_tx(&full[s], sign_bytes + C::kZUnit);
-        bulk_g2s(st, p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0, sign_bytes, &full[s], pol_sign);
+        bulk_g2s(st, p.signs + ((long long)(i >> p.ksh) * p.nq + q) * p.rows_pad + row0, sign_bytes, &full[s], pol_sign);
         bulk_g2s(st + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, C::kZUnit, &full[s], pol_keep);
         if (++q == p.nq) { q = 0; ++i; }
         if (++s == STAGES) { s = 0; ph ^= 1; }

@@ -123,8 +123,8 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
       const uint64_t pol_keep = policy_evict_last();
       const uint32_t sign_bytes = (uint32_t)Rg * kTileRows * 16;
       // first STAGES groups: sign tiles before the dependency wait, then their Zq
-      int k = 0, q = q_start, gi = 0;
-      long long ui = (long long)i_start * p.nq;   // i * nq of the current block
+      int k = 0, q = q_start, gi = 0, iv = i_start;
+      long long ui = (long long)(iv >> p.ksh) * p.nq;   // (sign block of block iv) * nq
       for (; gi < STAGES && k < nunits; ++gi) {
         const int cnt = group_count<P>(k, q, nunits, p.nq);
         mbar_arrive_expect_tx(&full[gi], (uint32_t)cnt * (sign_bytes + C::kZUnit));
@@ -133,7 +133,7 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
                    sign_bytes, &full[gi], pol_sign);
         k += cnt;
         q += cnt;
-        if (q == p.nq) { q = 0; ui += p.nq; }
+        if (q == p.nq) { q = 0; ++iv; ui = (long long)(iv >> p.ksh) * p.nq; }
       }
       const int pre = gi;
       asm volatile("griddepcontrol.wait;" ::: "memory");  // Zq of this call is complete and visible
@@ -160,7 +160,7 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
         bulk_g2s(st + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, (uint32_t)cnt * C::kZUnit, &full[s], pol_keep);
         k += cnt;
         q += cnt;
-        if (q == p.nq) { q = 0; ui += p.nq; }
+        if (q == p.nq) { q = 0; ++iv; ui = (long long)(iv >> p.ksh) * p.nq; }
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }

@@ -58,6 +58,7 @@ struct DecodeParams {
   uint32_t* dbg_z;                // test hook: CTA 0's first Z tile as stored in SMEM (or null)
   const uint8_t* zq;              // e4m3 kernel: Zq units built by zq_kernel (else null)
   int* status;                    // sticky numeric-range flag (e4m3 kernel), may be null
+  int ksh;                        // blocks are 16-rank halves: sign tile of block i is i >> ksh (k > 16: 1)
 };
 
 // Split-K reduction, shared by every decode kernel.  Each CTA stores the
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const Deco
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + s * C::kStageBytes;
         mbar_arrive_expect_tx(&full[s], sign_bytes + v_bytes + x_bytes * p.batch + kSubK * 4);
-        const uint4* src_s = p.signs + ((long long)i * p.nq + q) * p.rows_pad + row0;
+        const uint4* src_s = p.signs + ((long long)(i >> p.ksh) * p.nq + q) * p.rows_pad + row0;
         bulk_g2s(st, src_s, sign_bytes, &full[s], pol_sign);
         const uint8_t* src_v = reinterpret_cast<const uint8_t*>(p.v) +
                                ((long long)i * p.d_in_pad + (long long)q * kSubK) * 16 * fsz;

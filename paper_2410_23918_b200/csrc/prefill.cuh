@@ -98,6 +98,7 @@ struct WtileParams {
   const __nv_bfloat16* v; // [n_cap][d_in_pad][16] V'
   uint8_t* img;           // [row_tiles_img][kc] tiles of kImgTileA bytes
   int n, nq, rows_pad, row_tiles, row_tiles_img, kc;
+  int ksh;                // sign tile of block i is i >> ksh (16-rank halves of a k > 16 block)
 };
 
 template <int G>  // blocks per MMA step
@@ -211,10 +212,10 @@ __global__ void __launch_bounds__(256, (2 * G * kPK <= 256) ? 2 : 1) wtile_kerne
       mma_commit(&mma_bar[tb]);
     };
     auto load_signs = [&](int c, int gi, uint32_t (&w)[G]) {
-      const uint8_t* b = s_src + (long long)(c >> 1) * p.rows_pad * 16 + (c & 1) * 8 + (gi * G) * s_blk;
+      const uint8_t* b = s_src + (long long)(c >> 1) * p.rows_pad * 16 + (c & 1) * 8;
 #pragma unroll
       for (int gl = 0; gl < G; ++gl)
-        w[gl] = gi * G + gl < p.n ? __ldg(reinterpret_cast<const uint32_t*>(b + gl * s_blk)) : 0u;
+        w[gl] = gi * G + gl < p.n ? __ldg(reinterpret_cast<const uint32_t*>(b + ((gi * G + gl) >> p.ksh) * s_blk)) : 0u;
     };
 
     // (chunk, group) of steps s, s+1, s+2 -- advanced incrementally (no divisions in the loop)

@@ -70,7 +70,7 @@ def test_create_rejects_bad_arguments_without_gpu(lib):
     from paper_2410_23918_b200 import bitstack as bsmod
     h = ctypes.c_void_p()
     assert lib.bitstack_create(64, 64, 0, 4, 1, 0, 64, 0, ctypes.byref(h)) == -1       # k < 1
-    assert lib.bitstack_create(64, 64, 17, 4, 1, 0, 64, 0, ctypes.byref(h)) == -1      # k > 16
+    assert lib.bitstack_create(64, 64, 33, 4, 1, 0, 64, 0, ctypes.byref(h)) == -1      # k > 32
     assert lib.bitstack_create(64, 64, 16, 4, 7, 0, 64, 0, ctypes.byref(h)) == -1      # dtype
     assert lib.bitstack_create(64, 64, 16, 4, 1, 10, 5, 0, ctypes.byref(h)) == -2      # rows
     assert lib.bitstack_create(64, 64, 16, 4, 1, 0, 65, 0, ctypes.byref(h)) == -2

@@ -95,14 +95,16 @@ def test_compress_pins(bs, shape, fdt, k, over):
     assert err_gpu <= 1.02 * err_rnd + 1e-6 and err_gpu <= 1.05 * err_ref + 1e-6, (err_gpu, err_rnd, err_ref)
 
 
-def test_compressed_blocks_feed_the_decode_path(bs):
+@pytest.mark.parametrize("k", [16, 32])
+def test_compressed_blocks_feed_the_decode_path(bs, k):
     """Device outputs of bitstack_compress go straight into bitstack_load_blocks; the decode
-    kernel on them matches the oracle on the same stored blocks."""
+    kernel on them matches the oracle on the same stored blocks (k = 32: the paper's largest
+    ablation rank)."""
     d_out, d_in, n = 640, 1024, 5
     g, w, x_cal = _case(d_out, d_in, 512, 77)
     signs, u, v, s, sigma, resid = bs.compress(torch.from_numpy(w.astype(np.float32)).cuda(),
-                                               torch.from_numpy(x_cal.astype(np.float32)).cuda(), n, 16)
-    lay = bs.Layer(d_out, d_in, 16, n, "bf16")
+                                               torch.from_numpy(x_cal.astype(np.float32)).cuda(), n, k)
+    lay = bs.Layer(d_out, d_in, k, n, "bf16")
     lay.load_blocks(0, signs, u, v, s)
     blocks = _blocks(signs, u, v, sigma)
     s64 = s.cpu().numpy().astype(np.float64)

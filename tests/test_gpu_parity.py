@@ -30,18 +30,18 @@ def bs():
     return pkg
 
 
-def compress_case(d_out, d_in, n, dtype, seed, method="exact", p=None):
+def compress_case(d_out, d_in, n, dtype, seed, method="exact", p=None, k=16):
     g = channel_gains(d_in, seed + 4)
     w = make_weight(d_out, d_in, seed)
     x_cal = make_calibration(p or max(256, d_in), g, seed + 1)
-    s, blocks = O.compress(w, x_cal, n, 16, dtype=dtype, method=method, seed=seed)
+    s, blocks = O.compress(w, x_cal, n, k, dtype=dtype, method=method, seed=seed)
     s32 = s.astype(np.float32)
     return g, s32, blocks
 
 
 def make_layer(bs, d_out, d_in, blocks, s32, dtype, n_capacity=None, row_begin=0, row_end=None):
     signs, u, v = stack_blocks(blocks, dtype)
-    lay = bs.Layer(d_out, d_in, k=16, n_capacity=n_capacity or len(blocks), factor_dtype=dtype,
+    lay = bs.Layer(d_out, d_in, k=int(u.shape[-1]), n_capacity=n_capacity or len(blocks), factor_dtype=dtype,
                    row_begin=row_begin, row_end=row_end)
     lay.load_blocks(0, signs, u, v, s32)
     torch.cuda.synchronize()
@@ -374,6 +374,43 @@ def test_async_load_overlaps_matmul_on_another_stream(bs):
     xr = x.cpu().numpy().astype(np.float64)
     assert O.relative_l2(y.cpu().numpy().astype(np.float64), oracle_y(blocks, s32, 4, xr)) <= 1e-3
     assert all(torch.equal(a, ys[0]) for a in ys)
+
+
+# ------------------------------------------------------------------ k > 16 (the paper's k ablation)
+@pytest.mark.parametrize("k,dtype", [(32, "bf16"), (24, "bf16"), (32, "f32"), (20, "f16")])
+def test_rank_above_16_every_path(bs, k, dtype):
+    """k in (16, 32]: each block is held as two 16-rank halves sharing its sign tile; the
+    decode kernels (e4m3 / fp16), the prefill path, the SIMT kernel, reconstruct and grouped
+    calls all match the oracle on the same stored blocks."""
+    d_out, d_in, n = 384, 640, 3
+    g, s32, blocks = compress_case(d_out, d_in, n, dtype, 191 + k, k=k)
+    lay = make_layer(bs, d_out, d_in, blocks, s32, dtype)
+    assert lay.info()["k"] == k
+    tol = 1e-5 if dtype == "f32" else 1e-3
+    for batch in (1, 2, 3):
+        x = make_x(batch, g, 30 + batch)
+        for level in (1, n):
+            lay.set_num_blocks(level)
+            y, xr = gpu_y(lay, x)
+            assert O.relative_l2(y, oracle_y(blocks, s32, level, xr)) <= tol, (batch, level)
+    lay.set_num_blocks(n)
+    w = lay.reconstruct(torch.float32).cpu().numpy().astype(np.float64)
+    assert O.relative_l2(w, O.reconstruct(blocks, s32.astype(np.float64), n, d_out, d_in)) <= 1e-6
+    x = make_x(40, g, 77)
+    lay.set_kernel("simt")
+    y, xr = gpu_y(lay, x[:2])
+    assert O.relative_l2(y, oracle_y(blocks, s32, n, xr)) <= 1e-5
+    if dtype == "bf16":
+        lay.set_kernel("prefill")
+        y, xr = gpu_y(lay, x, x_dtype=torch.bfloat16)
+        assert O.relative_l2(y, oracle_y(blocks, s32, n, xr)) <= 1e-3
+    lay.set_kernel("auto")
+    if dtype != "f32":
+        xs = [torch.from_numpy(make_x(1, g, 5).astype(np.float32)).cuda()]
+        ys = bs.matmul_grouped([lay], xs)
+        torch.cuda.synchronize()
+        ref = oracle_y(blocks, s32, n, xs[0].cpu().numpy().astype(np.float64))
+        assert O.relative_l2(ys[0].cpu().numpy().astype(np.float64), ref) <= 1e-3
 
 
 # ------------------------------------------------------------------ H7: deterministic split-K
