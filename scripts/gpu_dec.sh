@@ -1,7 +1,7 @@
-export BITSTACK_LIB=$PWD/scripts/libbitstack_dec3.so
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "c2 or bf16 or grouped or split or zero or host or rank" > gpurun_out/pt_dec.log 2>&1; echo dec_rc=$?; tail -3 gpurun_out/pt_dec.log
+export BITSTACK_LIB=$PWD/scripts/libbitstack_pref.so
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "c2 or bf16 or grouped or split or zero or host or rank" > gpurun_out/pt_pref.log 2>&1; echo pref_rc=$?; tail -3 gpurun_out/pt_pref.log
 for rep in 1 2; do
-for v in def r3 dec3; do
+for v in def pref; do
   if [ $v = def ]; then unset BITSTACK_LIB; else export BITSTACK_LIB=$PWD/scripts/libbitstack_$v.so; fi
   for wl in c2 c5; do timeout 200 python bench.py --workload $wl --steps 1000 --warmup 20 --no-cpu-baseline > gpurun_out/e_${v}_${wl}_$rep.json 2>/dev/null; done
   timeout 200 python bench.py --workload c4 --steps 100 --warmup 5 --no-cpu-baseline > gpurun_out/e_${v}_c4_$rep.json 2>/dev/null
@@ -9,7 +9,7 @@ done
 done
 python - <<'P'
 import json
-for v in ("def", "r3", "dec3"):
+for v in ("def", "pref"):
     out = []
     for wl in ("c2", "c5", "c4"):
         for rep in (1, 2):
