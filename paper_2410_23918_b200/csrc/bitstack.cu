@@ -522,23 +522,22 @@ struct LinalgHandles {
   std::mutex mu;
   cublasHandle_t blas = nullptr;
   void* ws = nullptr;          // cuBLAS workspace (set explicitly: required under stream capture)
+  uint8_t* arena = nullptr;    // compression scratch (Arena), grow-only
+  int64_t arena_bytes = 0;
 };
 constexpr size_t kBlasWorkspace = 64ull << 20;
 LinalgHandles g_linalg[64];
 
-// Device allocations of one call, freed on every exit path.
-struct Scratch {
-  std::vector<void*> ptrs;
-  ~Scratch() {
-    for (void* p : ptrs) cudaFree(p);
-  }
+// Bump allocator over the per-device compression arena (grow-only, kept across calls: large
+// cudaMalloc / cudaFree pairs per call made the call time erratic).  Run once with base ==
+// nullptr to size it, then again over the arena.
+struct Arena {
+  uint8_t* base = nullptr;
+  int64_t off = 0;
   template <typename T>
-  cudaError_t get(T** out, int64_t count) {
-    void* p = nullptr;
-    const cudaError_t e = cudaMalloc(&p, (size_t)std::max<int64_t>(count, 1) * sizeof(T));
-    if (e == cudaSuccess) ptrs.push_back(p);
-    *out = reinterpret_cast<T*>(p);
-    return e;
+  void take(T** out, int64_t count) {
+    *out = reinterpret_cast<T*>(base + off);
+    off += (std::max<int64_t>(count, 1) * (int64_t)sizeof(T) + 255) / 256 * 256;
   }
 };
 }  // namespace
@@ -1132,36 +1131,53 @@ bitstack_status bitstack_compress(const float* w, const float* x_cal, int64_t p,
   const int ell = (int)std::min<int64_t>(k + oversample, std::min(d_out, d_in));
   if (ell > bs::kSmallMax) return fail(BITSTACK_E_INVALID_ARG, "k + oversample = %d > %d", ell, bs::kSmallMax);
   const int64_t total = d_out * d_in;
-  const int64_t cbytes = (total + 7) / 8;
   const int fs = dsize(factor_dtype);
   const int out_dt = factor_dtype == BITSTACK_F32 ? 0 : (factor_dtype == BITSTACK_BF16 ? 1 : 2);
-  Scratch sc;
   float *R, *M, *Om, *Y, *Z, *G, *Rinv, *Wv, *Acol, *Bb, *sig, *uf, *vf;
   double *s2, *sumsq;
   unsigned long long* smax;
-  CK(sc.get(&R, total));
-  CK(sc.get(&M, total));
-  CK(sc.get(&Om, d_in * ell));
-  CK(sc.get(&Y, d_out * ell));
-  CK(sc.get(&Z, d_in * ell));
-  CK(sc.get(&G, (int64_t)ell * ell));
-  CK(sc.get(&Rinv, (int64_t)ell * ell));
-  CK(sc.get(&Wv, (int64_t)ell * ell));
-  CK(sc.get(&Acol, d_out * k));
-  CK(sc.get(&Bb, d_in * k));
-  CK(sc.get(&sig, ell));
-  CK(sc.get(&uf, d_out * k));
-  CK(sc.get(&vf, d_in * k));
-  CK(sc.get(&s2, d_in));
-  CK(sc.get(&sumsq, n + 1));
-  CK(sc.get(&smax, 1));
+  int* bi = nullptr;               // device block counter of the block graph
+  auto carve = [&](Arena& ar) {
+    ar.take(&R, total);
+    ar.take(&M, total);
+    ar.take(&Om, d_in * ell);
+    ar.take(&Y, d_out * ell);
+    ar.take(&Z, d_in * ell);
+    ar.take(&G, (int64_t)ell * ell);
+    ar.take(&Rinv, (int64_t)ell * ell);
+    ar.take(&Wv, (int64_t)ell * ell);
+    ar.take(&Acol, d_out * k);
+    ar.take(&Bb, d_in * k);
+    ar.take(&sig, ell);
+    ar.take(&uf, d_out * k);
+    ar.take(&vf, d_in * k);
+    ar.take(&s2, d_in);
+    ar.take(&sumsq, n + 1);
+    ar.take(&smax, 1);
+    ar.take(&bi, 1);
+  };
+  {
+    Arena sizing;
+    carve(sizing);
+    if (sizing.off > H.arena_bytes) {
+      CK(cudaDeviceSynchronize());
+      cudaFree(H.arena);
+      H.arena = nullptr;
+      H.arena_bytes = 0;
+      CK(cudaMalloc((void**)&H.arena, (size_t)sizing.off));
+      H.arena_bytes = sizing.off;
+    }
+    Arena ar;
+    ar.base = H.arena;
+    carve(ar);
+  }
   // The ~100 launches per block (many of them tiny) are recorded once into a CUDA graph: issued
   // one by one, host launch overhead doubled the wall time of a 4096 x 4096 block.
   if (!H.ws) {
     CK(cudaMalloc(&H.ws, kBlasWorkspace));
     CKB(cublasSetWorkspace(H.blas, H.ws, kBlasWorkspace));
   }
-  auto body = [&](cudaStream_t st) -> bitstack_status {
+  auto body = [&](cudaStream_t st, int part) -> bitstack_status {   // part 0: prologue, 1: one block
     const float one = 1.f, zero = 0.f;
     // CholeskyQR: A [m, ell] col-major <- an orthonormal basis of its range (G = A^T A,
     // G = R^T R, A <- A R^-1 by a triangular solve; rank-deficient directions become ~zero
@@ -1182,6 +1198,7 @@ bitstack_status bitstack_compress(const float* w, const float* x_cal, int64_t p,
     const int T = 256;
     const int egrid = (int)std::min<int64_t>((total + T - 1) / T, 148 * 16);
 
+    if (part == 0) {
     // Eq.3-4: s (fp64 sums of squares, clamped), R_0 = W diag(s)
     CK(cudaMemsetAsync(s2, 0, d_in * sizeof(double), st));
     CK(cudaMemsetAsync(smax, 0, sizeof(unsigned long long), st));
@@ -1193,11 +1210,14 @@ bitstack_status bitstack_compress(const float* w, const float* x_cal, int64_t p,
     bs::sumsq_kernel<<<egrid, T, 0, st>>>(R, total, sumsq);
     for (int i = 0; i < 5; ++i) count_launch();
     CK(cudaGetLastError());
+    CK(cudaMemsetAsync(bi, 0, sizeof(int), st));
+    return BITSTACK_OK;
+    }
 
-    for (int i = 0; i < n; ++i) {
+    {   // one block (block-indexed outputs through the device counter bi)
       // Eq.5: S_i = sign(R), M = |R|
-      bs::sign_abs_kernel<<<egrid, T, 0, st>>>(R, total, signs + (int64_t)i * cbytes, M);
-      bs::gauss_kernel<<<(int)((d_in * ell + T - 1) / T), T, 0, st>>>(Om, d_in * ell, seed + 7919ull * (uint64_t)i);
+      bs::sign_abs_kernel<<<egrid, T, 0, st>>>(R, total, signs, bi, M);
+      bs::gauss_kernel<<<(int)((d_in * ell + T - 1) / T), T, 0, st>>>(Om, d_in * ell, seed, bi);
       count_launch();
       count_launch();
       CK(cudaGetLastError());
@@ -1230,31 +1250,41 @@ bitstack_status bitstack_compress(const float* w, const float* x_cal, int64_t p,
       CKB(cublasSgemm(H.blas, CUBLAS_OP_N, CUBLAS_OP_N, (int)d_in, k, ell, &one, Z, (int)d_in, Wv, ell, &zero, Bb,
                       (int)d_in));                                                         // Bt W[:, :k]
       // Eq.2 split + sign convention + storage rounding; Eq.7 residual with the rounded factors
-      bs::factor_out_kernel<<<k, T, 0, st>>>(Acol, d_out, Bb, d_in, sig, d_out, d_in, k, out_dt,
-                                             reinterpret_cast<uint8_t*>(u) + (int64_t)i * d_out * k * fs,
-                                             reinterpret_cast<uint8_t*>(v) + (int64_t)i * d_in * k * fs, uf, vf);
+      bs::factor_out_kernel<<<k, T, 0, st>>>(Acol, d_out, Bb, d_in, sig, d_out, d_in, k, out_dt, u, v, bi, uf, vf);
       bs::residual_kernel<<<dim3((unsigned)((d_in + 255) / 256), (unsigned)((d_out + bs::kResRows - 1) / bs::kResRows)),
-                            256, 0, st>>>(R, uf, vf, d_out, d_in, k, sumsq + i + 1);
+                            256, 0, st>>>(R, uf, vf, d_out, d_in, k, sumsq, bi);
       count_launch();
       count_launch();
       CK(cudaGetLastError());
-      if (sigma) CK(cudaMemcpyAsync(sigma + (int64_t)i * k, sig, k * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      bs::block_done_kernel<<<1, 32, 0, st>>>(sig, sigma, k, bi);   // sigma out, ++bi
+      count_launch();
+      CK(cudaGetLastError());
     }
     return BITSTACK_OK;
   };
+  // Two captured graphs: the prologue and one block's ~60 launches; the block graph is
+  // replayed n times (host launch overhead of the many small kernels is paid once per call).
   cudaStream_t cap = nullptr;
   CK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
   CKB(cublasSetStream(H.blas, cap));
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
-  cudaError_t ce = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-  bitstack_status rs0 = ce == cudaSuccess ? body(cap) : BITSTACK_OK;
-  const cudaError_t ee = cudaStreamEndCapture(cap, &graph);
-  if (ce == cudaSuccess) ce = ee;
-  if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphInstantiate(&exec, graph, 0);
-  if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphLaunch(exec, st);
-  if (exec) cudaGraphExecDestroy(exec);
-  if (graph) cudaGraphDestroy(graph);
+  cudaGraph_t graphs[2] = {nullptr, nullptr};
+  cudaGraphExec_t execs[2] = {nullptr, nullptr};
+  bitstack_status rs0 = BITSTACK_OK;
+  cudaError_t ce = cudaSuccess;
+  for (int g = 0; g < 2 && ce == cudaSuccess && rs0 == BITSTACK_OK; ++g) {
+    ce = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (ce != cudaSuccess) break;
+    rs0 = body(cap, g);
+    const cudaError_t ee = cudaStreamEndCapture(cap, &graphs[g]);
+    if (ce == cudaSuccess) ce = ee;
+    if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphInstantiate(&execs[g], graphs[g], 0);
+  }
+  if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphLaunch(execs[0], st);
+  for (int i = 0; i < n && ce == cudaSuccess && rs0 == BITSTACK_OK; ++i) ce = cudaGraphLaunch(execs[1], st);
+  for (int g = 0; g < 2; ++g) {
+    if (execs[g]) cudaGraphExecDestroy(execs[g]);
+    if (graphs[g]) cudaGraphDestroy(graphs[g]);
+  }
   cudaStreamDestroy(cap);
   cublasSetStream(H.blas, st);
   if (rs0) return rs0;

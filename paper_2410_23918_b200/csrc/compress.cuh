@@ -60,9 +60,12 @@ __global__ void scale_w_kernel(const float* __restrict__ w, const float* __restr
 
 // Canonical packing (bit e = element e of the row-major [d_out, d_in] matrix, LSB first,
 // 1 = +1): one thread per output byte; pad bits 0.  Also M = |R| for the SVD.
-__global__ void sign_abs_kernel(const float* __restrict__ r, long long total, uint8_t* __restrict__ signs,
-                                float* __restrict__ m) {
+// Block-indexed outputs (signs, factors, sigma, residual norms) are addressed through the
+// device-side block counter *bi, so one captured CUDA graph of a block's work serves every block.
+__global__ void sign_abs_kernel(const float* __restrict__ r, long long total, uint8_t* __restrict__ signs_base,
+                                const int* __restrict__ bi, float* __restrict__ m) {
   const long long nbytes = (total + 7) / 8;
+  uint8_t* signs = signs_base + (long long)*bi * nbytes;
   for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nbytes; b += (long long)gridDim.x * blockDim.x) {
     uint32_t byte = 0;
 #pragma unroll
@@ -78,9 +81,11 @@ __global__ void sign_abs_kernel(const float* __restrict__ r, long long total, ui
   }
 }
 
-__global__ void gauss_kernel(float* __restrict__ out, long long count, unsigned long long seed) {
+__global__ void gauss_kernel(float* __restrict__ out, long long count, unsigned long long seed0,
+                             const int* __restrict__ bi) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= count) return;
+  const unsigned long long seed = seed0 + 7919ull * (unsigned long long)*bi;
   curandStatePhilox4_32_10_t st;
   curand_init(seed, (unsigned long long)i, 0, &st);
   out[i] = curand_normal(&st);
@@ -94,9 +99,12 @@ __global__ void gauss_kernel(float* __restrict__ out, long long count, unsigned 
 // also kept as f32 ([rows, k]) for the residual update.  One CTA per r.
 __global__ void factor_out_kernel(const float* __restrict__ a, long long lda, const float* __restrict__ b,
                                   long long ldb, const float* __restrict__ sigma, long long d_out, long long d_in,
-                                  int k, int out_dt, void* __restrict__ u_out, void* __restrict__ v_out,
-                                  float* __restrict__ u_f, float* __restrict__ v_f) {
+                                  int k, int out_dt, void* __restrict__ u_base, void* __restrict__ v_base,
+                                  const int* __restrict__ blk_i, float* __restrict__ u_f, float* __restrict__ v_f) {
   const int r = blockIdx.x;
+  const int fsz = out_dt == 0 ? 4 : 2;
+  void* u_out = reinterpret_cast<uint8_t*>(u_base) + (long long)*blk_i * d_out * k * fsz;
+  void* v_out = reinterpret_cast<uint8_t*>(v_base) + (long long)*blk_i * d_in * k * fsz;
   __shared__ float best_v[32];
   __shared__ long long best_i[32];
   __shared__ float sgn_s;
@@ -152,7 +160,8 @@ __global__ void factor_out_kernel(const float* __restrict__ a, long long lda, co
 constexpr int kResRows = 16;
 __global__ void __launch_bounds__(256) residual_kernel(float* __restrict__ r, const float* __restrict__ u_f,
                                                        const float* __restrict__ v_f, long long d_out, long long d_in,
-                                                       int k, double* __restrict__ sumsq) {
+                                                       int k, double* __restrict__ sumsq_base, const int* __restrict__ bi) {
+  double* sumsq = sumsq_base + *bi + 1;
   __shared__ float us[kResRows][32];
   const long long c = blockIdx.x * 256LL + threadIdx.x;
   const long long j0 = (long long)blockIdx.y * kResRows;
@@ -350,6 +359,14 @@ __global__ void __launch_bounds__(1024) symeig_kernel(const float* __restrict__ 
     const int i = e % ell, j = e / ell;
     w_out[e] = v[i][order[j]];
   }
+}
+
+// End of a block: sigma[:k] -> sigma_out + bi k (if any), then the block counter advances.
+__global__ void block_done_kernel(const float* __restrict__ sig, float* __restrict__ sigma_out, int k, int* __restrict__ bi) {
+  const int b = *bi;
+  if (sigma_out && threadIdx.x < k) sigma_out[(long long)b * k + threadIdx.x] = sig[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) *bi = b + 1;
 }
 
 __global__ void sumsq_kernel(const float* __restrict__ r, long long total, double* __restrict__ sumsq) {

@@ -11,6 +11,7 @@ timeout 300 python bench.py --workload c5 --steps 2000 --warmup 20 > gpurun_out/
 timeout 300 python bench.py --workload c4 --steps 200 --warmup 5 > gpurun_out/bench_c4.json 2>gpurun_out/bench_c4.err; echo c4_rc=$?
 timeout 300 python bench.py --workload c4 --steps 200 --warmup 5 --no-group --no-cpu-baseline > gpurun_out/bench_c4_ungrouped.json 2>/dev/null; echo c4u_rc=$?
 timeout 300 python bench.py --workload load --steps 10 --warmup 3 > gpurun_out/bench_load.json 2>gpurun_out/bench_load.err; echo load_rc=$?
+timeout 300 python bench.py --workload compress --steps 5 --warmup 2 > gpurun_out/bench_compress.json 2>gpurun_out/bench_compress.err; echo compress_rc=$?
 for b in 2 4 8 16; do timeout 300 python bench.py --batch $b --steps 1000 --warmup 20 --no-cpu-baseline > gpurun_out/bench_c2_b$b.json 2>/dev/null; done
 for wl in c3_up c3_down; do timeout 300 python bench.py --workload $wl --steps 300 --warmup 5 > gpurun_out/pf_$wl.json 2>gpurun_out/pf_$wl.err; echo pf_rc=$?; done
 CMD="python bench.py --steps 40 --warmup 5 --no-cpu-baseline --no-graph"
