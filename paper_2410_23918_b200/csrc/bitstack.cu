@@ -1271,16 +1271,20 @@ bitstack_status bitstack_compress(const float* w, const float* x_cal, int64_t p,
   cudaGraphExec_t execs[2] = {nullptr, nullptr};
   bitstack_status rs0 = BITSTACK_OK;
   cudaError_t ce = cudaSuccess;
+  int64_t block_launches = 0;        // our kernels in the block graph (counted once at capture)
   for (int g = 0; g < 2 && ce == cudaSuccess && rs0 == BITSTACK_OK; ++g) {
     ce = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     if (ce != cudaSuccess) break;
+    const int64_t l0 = g_launches.load();
     rs0 = body(cap, g);
+    if (g == 1) block_launches = g_launches.load() - l0;
     const cudaError_t ee = cudaStreamEndCapture(cap, &graphs[g]);
     if (ce == cudaSuccess) ce = ee;
     if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphInstantiate(&execs[g], graphs[g], 0);
   }
   if (ce == cudaSuccess && rs0 == BITSTACK_OK) ce = cudaGraphLaunch(execs[0], st);
   for (int i = 0; i < n && ce == cudaSuccess && rs0 == BITSTACK_OK; ++i) ce = cudaGraphLaunch(execs[1], st);
+  if (n > 1) g_launches.fetch_add((n - 1) * block_launches, std::memory_order_relaxed);   // the replays
   for (int g = 0; g < 2; ++g) {
     if (execs[g]) cudaGraphExecDestroy(execs[g]);
     if (graphs[g]) cudaGraphDestroy(graphs[g]);
