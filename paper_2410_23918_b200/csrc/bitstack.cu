@@ -30,6 +30,8 @@ struct bitstack_layer_s {
   int64_t d_in_pad = 0;
   int32_t k = 0, n_cap = 0, n_res = 0, n_act = 0;
   int32_t kh = 1;          // 16-rank halves per block (k > 16: 2, sharing the block's sign tile)
+  cudaStream_t pf_side = nullptr;              // prefill: xprep runs here, concurrent with wtile
+  cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
   bitstack_dtype fdt = BITSTACK_BF16;
   int dev_fdt = 1;  // device factor storage: 0 f32, 1 bf16
   int layout = 1;   // device sign layout: 0 = F16 (fp32 factors, fp16 MMA), 1 = F8 (e4m3 MMA)
@@ -316,13 +318,23 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   rs = grow(L, &L->pf_x, &L->pf_x_bytes, (int64_t)nt * kc * BN * bs::kPK * 2, st);
   if (rs) return rs;
 
+  // xprep (X' image) and wtile (W' image) are independent: xprep runs on a side stream forked
+  // from `st` (fork / join by events, capturable into CUDA graphs), the GEMM waits for both
+  if (!L->pf_side) {
+    CK(cudaStreamCreateWithFlags(&L->pf_side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&L->pf_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&L->pf_join, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(L->pf_fork, st));
+  CK(cudaStreamWaitEvent(L->pf_side, L->pf_fork, 0));
   const long long pieces = (long long)nt * kc * BN * 8;
   const int xgrid = (int)std::min<long long>((pieces + 255) / 256, (long long)L->sm_count * 16);
   const bool xvec = L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-  bs::xprep_kernel<<<xgrid, 256, 0, st>>>(x, xdt, L->d_in, L->inv_s, (int)batch, (int)L->d_in, kc, BN, pieces,
-                                          reinterpret_cast<uint4*>(L->pf_x), xvec);
+  bs::xprep_kernel<<<xgrid, 256, 0, L->pf_side>>>(x, xdt, L->d_in, L->inv_s, (int)batch, (int)L->d_in, kc, BN,
+                                                  pieces, reinterpret_cast<uint4*>(L->pf_x), xvec);
   count_launch();
   CK(cudaGetLastError());
+  CK(cudaEventRecord(L->pf_join, L->pf_side));
 
   bs::WtileParams wp;
   wp.signs = L->signs;
@@ -341,6 +353,7 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   bs::wtile_kernel<kWtileG><<<wgrid, WC::kThreads, WC::kSmem(wp.n), st>>>(wp);
   count_launch();
   CK(cudaGetLastError());
+  CK(cudaStreamWaitEvent(st, L->pf_join, 0));
 
   bs::GemmParams gp;
   gp.a_img = L->pf_w;
@@ -642,6 +655,9 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   cudaFree(L->v);
   cudaFree(L->inv_s);
   cudaFree(L->zscale);
+  if (L->pf_side) cudaStreamDestroy(L->pf_side);
+  if (L->pf_fork) cudaEventDestroy(L->pf_fork);
+  if (L->pf_join) cudaEventDestroy(L->pf_join);
   cudaFree(L->y_part);
   cudaFree(L->counters);
   cudaFree(L->status);
