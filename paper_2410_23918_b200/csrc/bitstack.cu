@@ -1066,7 +1066,7 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   if (count == 0 || batch == 0) return BITSTACK_OK;
   // One launch pair when every member can take the e4m3 decode kernel on device buffers;
   // otherwise the members run one after another through bitstack_matmul (same results).
-  bool fused = count <= bs::kMaxGroup && batch >= 1 && batch <= 4 && decode_issuer() &&
+  bool fused = count <= bs::kMaxGroup && batch >= 1 && batch < kPrefillMinBatch && decode_issuer() &&
                valid_dtype(x_dtype) && (y_dtype == BITSTACK_F32 || y_dtype == BITSTACK_BF16);
   for (int i = 0; fused && i < count; ++i) {
     bitstack_layer L = layers[i];
@@ -1089,10 +1089,22 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype), ysz = y_dtype == BITSTACK_F32 ? 4 : 2;
-  const int bc = (int)batch;
-  if (bc == 1) return launch_grouped_f8<1>(layers, count, xs, xdt, xsz, ys, ydt, ysz, bc, st);
-  if (bc == 2) return launch_grouped_f8<2>(layers, count, xs, xdt, xsz, ys, ydt, ysz, bc, st);
-  return launch_grouped_f8<4>(layers, count, xs, xdt, xsz, ys, ydt, ysz, bc, st);
+  // batch chunks of <= 4 tokens (the decode kernels' widest batch class), one launch pair each
+  for (int64_t b0 = 0; b0 < batch; b0 += 4) {
+    const int bc = (int)std::min<int64_t>(4, batch - b0);
+    const void* xc[bs::kMaxGroup];
+    void* yc[bs::kMaxGroup];
+    for (int i = 0; i < count; ++i) {
+      xc[i] = reinterpret_cast<const uint8_t*>(xs[i]) + b0 * layers[i]->d_in * xsz;
+      yc[i] = reinterpret_cast<uint8_t*>(ys[i]) + b0 * layers[i]->rows_local * ysz;
+    }
+    bitstack_status rs;
+    if (bc == 1) rs = launch_grouped_f8<1>(layers, count, xc, xdt, xsz, yc, ydt, ysz, bc, st);
+    else if (bc == 2) rs = launch_grouped_f8<2>(layers, count, xc, xdt, xsz, yc, ydt, ysz, bc, st);
+    else rs = launch_grouped_f8<4>(layers, count, xc, xdt, xsz, yc, ydt, ysz, bc, st);
+    if (rs) return rs;
+  }
+  return BITSTACK_OK;
 }
 
 bitstack_status bitstack_reconstruct(bitstack_layer L, void* w, bitstack_dtype w_dtype, void* stream) {

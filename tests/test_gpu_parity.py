@@ -438,7 +438,7 @@ def _grouped_case(bs, shapes, seed):
     return out
 
 
-@pytest.mark.parametrize("batch", [1, 2, 3, 4])
+@pytest.mark.parametrize("batch", [1, 2, 3, 4, 7, 9])
 def test_grouped_matches_individual_and_oracle(bs, batch):
     """bitstack_matmul_grouped: members of different shapes (ragged rows, ragged d_in) and
     levels run as ONE zq + ONE decode launch and give the individual calls' y (up to the
@@ -453,7 +453,7 @@ def test_grouped_matches_individual_and_oracle(bs, batch):
     c0 = bs.launch_count()
     ys = bs.matmul_grouped(lays, xs)
     torch.cuda.synchronize()
-    assert bs.launch_count() - c0 == 2           # zq_grouped + decode_f8i_grouped
+    assert bs.launch_count() - c0 == 2 * ((batch + 3) // 4)   # zq_grouped + decode_f8i_grouped per 4 tokens
     for (g, s32, blocks, lay), n, x, y in zip(case, levels, xs, ys):
         y1 = lay.matmul(x)
         torch.cuda.synchronize()
@@ -478,13 +478,13 @@ def test_grouped_shared_x_more_ctas_than_sms(bs):
 
 
 def test_grouped_fallbacks(bs):
-    """Groups the single launch cannot take (fp32 factors, batch > 4, a repeated handle,
-    more than 8 members, n == 0) run member by member with identical results."""
+    """Groups the fused launches cannot take (fp32 factors, prefill-size batches, a repeated
+    handle, more than 8 members, n == 0) run member by member with identical results."""
     case = _grouped_case(bs, [(256, 384, 2), (384, 256, 3)], 701)
     g32, s32f, blocks32 = compress_case(200, 384, 2, "f32", 721)
     lay32 = make_layer(bs, 200, 384, blocks32, s32f, "f32")
     a, b = case[0][3], case[1][3]
-    for batch in (1, 6):
+    for batch in (1, 6, 20):
         xa = torch.from_numpy(make_x(batch, case[0][0], 9).astype(np.float32)).cuda()
         xb = torch.from_numpy(make_x(batch, case[1][0], 10).astype(np.float32)).cuda()
         for lays, xs in (([a, lay32, b], [xa, xa, xb]), ([a, a], [xa, xa]), ([b] * 9, [xb] * 9), ([a, b], [xa, xb])):
