@@ -127,15 +127,31 @@ bool is_device_ptr(const void* p) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// cudaFuncSetAttribute is per device context: apply `set` once per (call site, device).  Two
+// threads racing here both apply the (idempotent) attributes, which is harmless.
+template <typename F>
+bitstack_status once_per_device(std::atomic<unsigned long long>& done, F&& set) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return BITSTACK_OK;
+  const bitstack_status rs = set();
+  if (rs) return rs;
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return BITSTACK_OK;
+}
+
+
 template <int NB, int NDIG>
 bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_t st) {
   using C = bs::DecodeCfg<NB, NDIG>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static std::atomic<unsigned long long> attr_done{0};
+  bitstack_status attr_rs = once_per_device(attr_done, [&]() -> bitstack_status {
     CK(cudaFuncSetAttribute(bs::decode_tc_kernel<NB, NDIG>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
-    attr_done = true;
-  }
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    return BITSTACK_OK;
+  });
+  if (attr_rs) return attr_rs;
   bs::decode_tc_kernel<NB, NDIG><<<grid, bs::kDecodeThreads, C::kSmemBytes, st>>>(prm);
   count_launch();
   CK(cudaGetLastError());
@@ -208,18 +224,16 @@ bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_i
   using G = F8Geom<NB>;
   using C = bs::DecodeF8Cfg<NB, G::R>;
   using CI = bs::DecodeF8ICfg<NB, G::R, G::P, G::OCC>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static std::atomic<unsigned long long> attr_done{0};
+  bitstack_status attr_rs = once_per_device(attr_done, [&]() -> bitstack_status {
     CK(cudaFuncSetAttribute(bs::decode_f8_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             C::kSmemBytes));
     CK(cudaFuncSetAttribute(bs::decode_f8i_kernel<NB, G::R, G::P, G::OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             CI::kSmemBytes));
-    attr_done = true;
-  }
+    return BITSTACK_OK;
+  });
+  if (attr_rs) return attr_rs;
   const bool iss = decode_issuer();
-
-
-
   const int64_t units = (int64_t)prm_in.n * prm_in.nq;
   bitstack_status zs = ensure_zq<NB>(L, units, st);
   if (zs) return zs;
@@ -301,13 +315,14 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
                                cudaStream_t st) {
   using GC = bs::GemmCfg<BN, MH>;
   using WC = bs::WtileCfg<kWtileG>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static std::atomic<unsigned long long> attr_done{0};
+  bitstack_status attr_rs = once_per_device(attr_done, [&]() -> bitstack_status {
     CK(cudaFuncSetAttribute(bs::prefill_gemm_kernel<BN, MH>, cudaFuncAttributeMaxDynamicSharedMemorySize, GC::kSmemBytes));
     CK(cudaFuncSetAttribute(bs::wtile_kernel<kWtileG>, cudaFuncAttributeMaxDynamicSharedMemorySize, WC::kSmem(16) + 1024));
     CK(cudaFuncSetAttribute(bs::wtile_kernel<kWtileG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    attr_done = true;
-  }
+    return BITSTACK_OK;
+  });
+  if (attr_rs) return attr_rs;
   if (L->n_act * L->kh > 16)
     return fail(BITSTACK_E_UNSUPPORTED, "prefill path supports n <= 16 active blocks (n <= 8 for k > 16)");
   const int kc = (int)(L->d_in_pad / bs::kPK);
@@ -461,12 +476,13 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
                                          int xsz, void* const* ys, int ydt, int ysz, int bc, cudaStream_t st) {
   constexpr int R = F8Geom<NB>::R, P = F8Geom<NB>::P, OCC = F8Geom<NB>::OCC;
   using CI = bs::DecodeF8ICfg<NB, R, P, OCC>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static std::atomic<unsigned long long> attr_done{0};
+  bitstack_status attr_rs = once_per_device(attr_done, [&]() -> bitstack_status {
     CK(cudaFuncSetAttribute(bs::decode_f8i_grouped_kernel<NB, R, P, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             CI::kSmemBytes));
-    attr_done = true;
-  }
+    return BITSTACK_OK;
+  });
+  if (attr_rs) return attr_rs;
   int n_groups[bs::kMaxGroup], cpg[bs::kMaxGroup];
   int64_t units[bs::kMaxGroup];
   double work[bs::kMaxGroup];
