@@ -917,6 +917,26 @@ def main():
                "sample": f"dense oracle (fp64 numpy, Eq.8+Eq.4) for {rows_s} of {d_out} output rows, "
                          f"all {n} blocks, 1 call ({dt:.2f} s)"}
 
+    # N > 1: the NCCL all-gather of the output slices timed alone (kernel,
+    # collective and end-to-end reported separately); all ranks take part
+    coll = None
+    if world > 1:
+        try:
+            reps = 200
+            dist.barrier()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record()
+            for _ in range(reps):
+                dist.all_gather_into_tensor(y_full, y)
+            g1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([g0.elapsed_time(g1) / reps], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            coll = {"op": "NCCL all_gather_into_tensor of the fp32 y slices", "us": float(t.item()) * 1e3,
+                    "bytes_per_rank": int(y.numel() * y.element_size())}
+        except Exception as ex:  # noqa: BLE001 -- the main line must still print
+            coll = {"error": str(ex)[:200]}
     if rank == 0:
         line = {
             "metric": metric_name(w),
@@ -945,6 +965,8 @@ def main():
         }
         if sweep:
             line["n_sweep"] = sweep
+        if coll is not None:
+            line["collective"] = coll
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
