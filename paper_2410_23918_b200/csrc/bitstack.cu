@@ -216,6 +216,7 @@ bs::ZqParams zq_params(bitstack_layer L, const bs::DecodeParams& p) {
   zp.batch = p.batch;
   zp.x_dtype = p.x_dtype;
   zp.f_dtype = p.f_dtype;
+  zp.kfuse = p.kfuse;
   return zp;
 }
 
@@ -464,6 +465,7 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
   prm.dbg_z = g_dbg_z;
   prm.zq = nullptr;
   prm.status = nullptr;
+  prm.kfuse = 0;
   return prm;
 }
 
@@ -988,6 +990,27 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
   const int nbmax = f8 ? 4 : 8;
   for (int64_t b0 = 0; b0 < batch; b0 += nbmax) {
     const int bc = (int)std::min<int64_t>(nbmax, batch - b0);
+    // k > 16 with one token: both 16-rank halves of a block in ONE N = 96 contraction (the
+    // batch-2 kernel geometry, column b = rank half b), so each sign tile is streamed once
+    if (f8 && L->kh == 2 && bc == 1 && decode_issuer()) {
+      const int R = F8Geom<2>::R;
+      const int n_groups = (L->row_tiles + R - 1) / R;
+      const int64_t units = (int64_t)L->n_act * L->nq;
+      int cpg = std::max(1, F8Geom<2>::OCC * L->sm_count / n_groups);
+      cpg = (int)std::min<int64_t>(cpg, units);
+      bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
+      prm.n = L->n_act;
+      prm.ksh = 0;
+      prm.kfuse = 1;
+      int slot = -1;
+      bitstack_status ps = record_prof(st, true, &slot);
+      if (ps) return ps;
+      bitstack_status rs = launch_decode_f8<2>(L, prm, n_groups * cpg, st);
+      if (rs) return rs;
+      ps = record_prof(st, false, &slot);
+      if (ps) return ps;
+      continue;
+    }
     int nb = 1;
     while (nb < bc) nb <<= 1;
     const int R = f8 ? (nb == 1 ? F8Geom<1>::R : (nb == 2 ? F8Geom<2>::R : F8Geom<4>::R)) : r_tiles_for(nb, 2);

@@ -103,6 +103,8 @@ struct ZqParams {
   uint8_t* zq;          // [n][nq] units of kZUnit bytes
   long long x_stride;
   int nq, d_in, d_in_pad, batch, x_dtype, f_dtype;
+  int kfuse;            // 1: k > 16 at batch 1 -- column b of the NB = 2 layout is rank half b of
+                        //    block i (internal block 2 i + b), all on x row 0
 };
 
 // One CTA per unit (block i, subchunk q); thread c = column q*128 + c.
@@ -117,8 +119,8 @@ __device__ __forceinline__ void zq_body(const ZqParams& p, const int unit) {
   const int c = threadIdx.x;
   const int col = q * kSubK + c;
   float vv[16];
-  {
-    const long long base = ((long long)i * p.d_in_pad + col) * 16;
+  auto load_v = [&](int blk) {
+    const long long base = ((long long)blk * p.d_in_pad + col) * 16;
     if (p.f_dtype == 1) {
       const uint4* vp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.v) + base);
       const uint4 a = __ldg(vp), b = __ldg(vp + 1);
@@ -137,13 +139,17 @@ __device__ __forceinline__ void zq_body(const ZqParams& p, const int unit) {
         vv[4 * e] = f.x; vv[4 * e + 1] = f.y; vv[4 * e + 2] = f.z; vv[4 * e + 3] = f.w;
       }
     }
-  }
+  };
+  if (!p.kfuse) load_v(i);
   const float is = col < p.d_in ? __ldg(p.inv_s + col) : 0.f;
   float z[NB][16];
   float m = 0.f;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    const float xs = (b < p.batch && col < p.d_in) ? load_act(p.x, (long long)b * p.x_stride + col, p.x_dtype) * is : 0.f;
+    if (p.kfuse) load_v(2 * i + b);
+    const int xb = p.kfuse ? 0 : b;
+    const bool on = p.kfuse ? true : b < p.batch;
+    const float xs = (on && col < p.d_in) ? load_act(p.x, (long long)xb * p.x_stride + col, p.x_dtype) * is : 0.f;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       z[b][r] = vv[r] * xs;

@@ -295,8 +295,8 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
       if (last) {
         // ---- epilogue for block ci: y += 2^-E sum_r U'_ci[row, r] (T_d0 + T_d1 + T_d2)[row, r]
         float uu[16];
-        {
-          const long long base = ((long long)ci * p.rows_pad + row_abs) * 16;
+        auto load_u = [&](long long blk) {
+          const long long base = (blk * p.rows_pad + row_abs) * 16;
           if (p.f_dtype == 1) {
             const uint4* up = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.u) + base);
             const uint4 r0v = __ldg(up), r1v = __ldg(up + 1);
@@ -317,13 +317,15 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
               uu[4 * e] = f.x; uu[4 * e + 1] = f.y; uu[4 * e + 2] = f.z; uu[4 * e + 3] = f.w;
             }
           }
-        }
+        };
+        if (!p.kfuse) load_u(ci);
         mbar_wait(&acc_full[wg], acc_ph);
         acc_ph ^= 1;
         tc_fence_after();
         const float esc = exp2f((float)-E);
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
+          if (p.kfuse) load_u(2LL * ci + b);     // rank half b of block ci
           float tsum[16];
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
@@ -336,7 +338,8 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
           float acc = 0.f;
 #pragma unroll
           for (int r = 0; r < 16; ++r) acc = fmaf(uu[r], tsum[r], acc);
-          yacc[b] = fmaf(acc, esc, yacc[b]);
+          if (p.kfuse) yacc[0] = fmaf(acc, esc, yacc[0]);
+          else yacc[b] = fmaf(acc, esc, yacc[b]);
         }
         // the next block's first MMA (issued after this warpgroup's next tile-ready
         // barrier) overwrites the accumulator: order these tcgen05.ld before it

@@ -59,6 +59,7 @@ struct DecodeParams {
   const uint8_t* zq;              // e4m3 kernel: Zq units built by zq_kernel (else null)
   int* status;                    // sticky numeric-range flag (e4m3 kernel), may be null
   int ksh;                        // blocks are 16-rank halves: sign tile of block i is i >> ksh (k > 16: 1)
+  int kfuse;                      // e4m3 kernel, k > 16 at batch 1: NB = 2 columns are the two rank halves
 };
 
 // Split-K reduction, shared by every decode kernel.  Each CTA stores the
