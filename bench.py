@@ -954,6 +954,8 @@ def main():
             "roofline": {"bound": "hbm" if decode_path else "tensor", "achieved": achieved,
                          "peak": peak, "unit": "GB/s" if decode_path else "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         ("frac_of_spec_8000_gbs" if decode_path else "frac_of_nominal_2250_tflops"):
+                             achieved / (8000.0 if decode_path else 2250.0),
                          "kernel": dom_name, "kernel_us": kernel_ms * 1e3,
                          "kernel_launches_timed": nk,
                          ("bytes_per_launch" if decode_path else "flops_per_launch"):
