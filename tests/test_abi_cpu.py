@@ -105,3 +105,15 @@ def test_grouped_load_and_compress_validate_without_gpu(lib):
     with pytest.raises(ValueError):
         bsmod.Group([], [1], [])
     assert bsmod.matmul_grouped([], []) == []
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: pointing the binding at a missing library raises instead of computing."""
+    import subprocess
+    import sys
+    code = ("import os, sys; sys.path.insert(0, %r); os.environ['BITSTACK_LIB'] = %r\n"
+            "import paper_2410_23918_b200 as bs\n"
+            "try:\n    bs.Layer(64, 64)\nexcept FileNotFoundError as e:\n    print('LOUD', e)\n") % (
+        ROOT, str(tmp_path / "missing.so"))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert "LOUD" in out.stdout and "no CPU fallback" in out.stdout, out.stdout + out.stderr
