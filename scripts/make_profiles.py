@@ -127,8 +127,26 @@ def main(r, key="c2_n16_b1_g1"):
     print("\n".join(lines + out))
 
 
+def traffic_only(rep_name, key, regex):
+    """profiles/traffic.json[key] = DRAM read + write bytes per call of the kernels matching
+    `regex` in gpurun_out/<rep_name>.ncu-rep (one launch each)."""
+    rep = os.path.join(ROOT, "gpurun_out", rep_name + ".ncu-rep")
+    total, seen = 0.0, []
+    for name, m in full(rep):
+        if re.search(regex, name) and name not in seen:
+            seen.append(name)
+            total += to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    tj = json.load(open(tp)) if os.path.exists(tp) else {}
+    tj[key] = total
+    json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
+    print(key, total, seen)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[2] == "prefill":
         prefill(sys.argv[1])
+    elif len(sys.argv) > 1 and sys.argv[1] == "traffic":
+        traffic_only(sys.argv[2], sys.argv[3], sys.argv[4])
     else:
         main(*sys.argv[1:])
