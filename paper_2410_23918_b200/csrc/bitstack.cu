@@ -184,7 +184,10 @@ bool decode_issuer() {
 #endif
 template <int NB> struct F8Geom;   // OCC: resident decode CTAs per SM (each with 512/OCC TMEM columns)
 template <> struct F8Geom<1> { static constexpr int R = BS_F8_R1, P = BS_F8_P1, OCC = BS_F8_OCC1; };
-template <> struct F8Geom<2> { static constexpr int R = 2, P = BS_F8_P2, OCC = 1; };
+#ifndef BS_F8_R2
+#define BS_F8_R2 2
+#endif
+template <> struct F8Geom<2> { static constexpr int R = BS_F8_R2, P = BS_F8_P2, OCC = 1; };
 template <> struct F8Geom<4> { static constexpr int R = 2, P = 1, OCC = 1; };
 
 // Z workspace of layer L for `units` (block, 128-column chunk) pairs at batch class NB; grows
