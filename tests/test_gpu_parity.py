@@ -413,6 +413,38 @@ def test_rank_above_16_every_path(bs, k, dtype):
         assert O.relative_l2(ys[0].cpu().numpy().astype(np.float64), ref) <= 1e-3
 
 
+# ------------------------------------------------------------------ mixed groups / graph capture
+def test_grouped_mixed_ranks_and_graph_capture(bs):
+    """A group mixing k = 16 and k = 32 members and different levels, captured into a CUDA
+    graph and replayed: every member matches its individual call and the oracle."""
+    g1, s1, b1 = compress_case(384, 512, 3, "bf16", 901)
+    g2, s2, b2 = compress_case(256, 512, 2, "bf16", 902, k=32)
+    l1 = make_layer(bs, 384, 512, b1, s1, "bf16")
+    l2 = make_layer(bs, 256, 512, b2, s2, "bf16")
+    l1.set_num_blocks(2)
+    x = torch.from_numpy(make_x(2, g1, 3).astype(np.float32)).to(torch.bfloat16).cuda()
+    y1 = torch.empty((2, 384), device="cuda")
+    y2 = torch.empty((2, 256), device="cuda")
+    grp = bs.Group([l1, l2], [x.data_ptr(), x.data_ptr()], [y1.data_ptr(), y2.data_ptr()])
+    stream = torch.cuda.current_stream()
+    grp(bs.BF16, bs.F32, 2, stream.cuda_stream)          # first call outside capture (workspaces)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(stream)
+    with torch.cuda.graph(graph, stream=cap):
+        grp(bs.BF16, bs.F32, 2, cap.cuda_stream)
+    stream.wait_stream(cap)
+    y1.zero_()
+    y2.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    xr = x.float().cpu().numpy().astype(np.float64)
+    assert O.relative_l2(y1.cpu().numpy().astype(np.float64), oracle_y(b1, s1, 2, xr)) <= 1e-3
+    assert O.relative_l2(y2.cpu().numpy().astype(np.float64), oracle_y(b2, s2, 2, xr)) <= 1e-3
+    assert torch.equal(y1, l1.matmul(x)) or O.relative_l2(y1.cpu().numpy(), l1.matmul(x).cpu().numpy()) <= 1e-6
+
+
 # ------------------------------------------------------------------ H7: deterministic split-K
 @pytest.mark.parametrize("dtype,batch", [("bf16", 1), ("bf16", 3), ("f32", 1), ("f32", 5)])
 def test_split_k_reduction_is_deterministic(bs, dtype, batch):
