@@ -17,9 +17,12 @@
 //                      in (224, 448], and the three round-to-nearest e4m3 digits, written
 //                      as a ready-to-copy UMMA B tile (+16 B of metadata) -- built ONCE per
 //                      unit instead of once per row group;
-//   decode_f8_kernel<NB>  bulk-copies sign tiles + Zq tiles (TMA engine), expands signs to
+//   decode kernel      bulk-copies sign tiles + Zq tiles (TMA engine), expands signs to
 //                      e4m3 +-2^a_u in TMEM, a_u = E - e_u (E = the CTA's first unit's e_u),
 //                      so A*B = +-Z 2^E for every unit; the epilogue multiplies by 2^-E.
+//                      The production schedule is decode_f8i_kernel (decode_f8i.cuh: one MMA
+//                      issuer warp per warpgroup); decode_f8_kernel below (self-issuing
+//                      warpgroups) stays selectable with BS_DECODE_WG=1 for A/B runs.
 // The decode kernel is launched with programmatic dependent launch: its setup and first
 // sign loads overlap the Zq kernel; only the Zq copies wait (griddepcontrol.wait).
 #pragma once
