@@ -5,3 +5,4 @@ from .bitstack import (  # noqa: F401
     BF16, F16, F32, BitStackError, Group, Layer, block_size_bits, compress, launch_count, load_library, matmul_grouped,
     profile_begin, profile_end,
 )
+from . import budget  # noqa: F401,E402  (memory-budget level selection, host logic)

@@ -445,6 +445,29 @@ def test_grouped_mixed_ranks_and_graph_capture(bs):
     assert torch.equal(y1, l1.matmul(x)) or O.relative_l2(y1.cpu().numpy(), l1.matmul(x).cpu().numpy()) <= 1e-6
 
 
+# ------------------------------------------------------------------ memory budget
+def test_stackset_budget_walk(bs):
+    """A StackSet follows a shrinking then growing memory budget (Average ordering): levels
+    differ by at most one, fit the budget, and every layer's y matches the oracle at its level."""
+    from paper_2410_23918_b200.budget import StackSet
+    shapes = [(256, 384), (384, 256), (200, 384)]
+    cases = [compress_case(d_out, d_in, 4, "bf16", 1201 + j) for j, (d_out, d_in) in enumerate(shapes)]
+    lays = [make_layer(bs, d_out, d_in, blocks, s32, "bf16") for (d_out, d_in), (g, s32, blocks) in zip(shapes, cases)]
+    ss = StackSet(lays, order=[2, 0, 1])
+    full = sum(ss.sizes) * 4
+    for frac in (1.0, 0.6, 0.3, 0.05, 0.45, 0.9):
+        levels = ss.apply_budget(frac * full)
+        assert max(levels) - min(levels) <= 1
+        assert sum(l * sz for l, sz in zip(levels, ss.sizes)) <= frac * full + 1e-6
+        for lay, (g, s32, blocks), lv in zip(lays, cases, levels):
+            assert lay.info()["n_active"] == lv
+            y, xr = gpu_y(lay, make_x(1, g, 5))
+            if lv == 0:
+                assert not np.any(y)
+            else:
+                assert O.relative_l2(y, oracle_y(blocks, s32, lv, xr)) <= 1e-3
+
+
 # ------------------------------------------------------------------ H7: deterministic split-K
 @pytest.mark.parametrize("dtype,batch", [("bf16", 1), ("bf16", 3), ("f32", 1), ("f32", 5)])
 def test_split_k_reduction_is_deterministic(bs, dtype, batch):
