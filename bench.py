@@ -27,7 +27,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synthetic import (C4_LEVELS, CONFIGS, LLAMA31_8B_SHAPES, average_levels, channel_gains,  # noqa: E402
+from synthetic import (CONFIGS, LLAMA31_8B_SHAPES, channel_gains,  # noqa: E402
                        make_random_blocks, make_x, seed_for)
 
 L2_BYTES = 126 * 2 ** 20
@@ -40,7 +40,7 @@ WORKLOADS = {
                   label="c3: Llama-3.1-8B up/gate_proj 14336x4096, n=8 blocks, k=16, bf16 factors, prefill 2048 tokens"),
     "c4": dict(d_out=4096, d_in=4096, n=4, k=16, batch=1, factor_dtype="bf16", kind="stack",
                label="c4: full Llama-3.1-8B linear stack (32 layers x q,k,v,o,gate,up,down = 224 matrices), "
-                     "5541 MiB budget (average level 3.88: 3-4 blocks per matrix, seeded Average layering), "
+                     "5541 MiB budget (levels from the budget with the Average ordering: 3-4 blocks per matrix, 3.88 in model-size units), "
                      "decode, one token-step = the 224 matmuls as 128 grouped calls (bitstack_matmul_grouped per shared input)"),
     "load": dict(CONFIGS["c5"], kind="load",
                  label="block streaming: the 12 blocks of Llama-3.1-70B down_proj 8192x28672 (k=16, bf16 "
@@ -181,9 +181,17 @@ def run_stack(args, w, world, rank, local_rank):
     """Config C4: every linear of Llama-3.1-8B held as BitStack blocks at the
     paper's 5541 MiB memory point; one step = one decode token through all 224 matmuls
     (32 layers x 7), captured as one CUDA graph.  Row shards at N > 1 (outputs all-gathered)."""
-    level = C4_LEVELS[5541]
+    budget_mib = 5541
     names = list(LLAMA31_8B_SHAPES)
-    n_of = average_levels(32 * len(names), level, seed_for(4, 0, "blocks")).reshape(32, len(names))
+    # per-matrix levels from the memory budget with the Average ordering (budget.average_levels,
+    # P:142-146): Eq.9 block sizes, 2004.5 MiB of embeddings / head / norms outside the stacks
+    # (SURVEY Q15), a seeded permutation of the 224 matrices as the within-level order
+    from paper_2410_23918_b200.budget import average_levels as budget_levels
+    eq9 = [(d_out * d_in + 16 * 16 * (d_out + d_in)) / 8.0
+           for _ in range(32) for d_out, d_in in (LLAMA31_8B_SHAPES[nm] for nm in names)]
+    order = np.random.default_rng(seed_for(4, 0, "blocks")).permutation(len(eq9)).tolist()
+    n_of = np.array(budget_levels(eq9, (budget_mib - 2004.5) * 2 ** 20, order)).reshape(32, len(names))
+    level = float(np.dot(n_of.reshape(-1), eq9) / sum(eq9))   # loaded levels in model-size units
     batch = args.batch or 1
     def oracle_stack_sample(reps):
         """The oracle on a bounded sample: 64 rows of each of layer 0's 7 matrices -> GB/s."""
@@ -339,7 +347,8 @@ def run_stack(args, w, world, rank, local_rank):
             "dtype": "e4m3 MMA operands (S exact, Z as 3 e4m3 digits), fp32 accumulate",
             "data": "synthetic (stored-form random blocks + activations, synthetic/ recipe)",
             "config": {"workload": w["label"], "batch": batch, "matrices": len(layers),
-                       "blocks_per_matrix": {"3": int((n_of == 3).sum()), "4": int((n_of == 4).sum())},
+                       "blocks_per_matrix": {str(v): int((n_of == v).sum()) for v in sorted(set(n_of.reshape(-1).tolist()))},
+                       "budget_mib": budget_mib, "loaded_level": level,
                        "weight_bytes_per_token": all_bytes,
                        "parallelism": f"tp{world} (row shards + NCCL all-gather)" if world > 1 else "tp1",
                        "l2": "inputs larger than L2 (3.7 GB of blocks per token-step)",
