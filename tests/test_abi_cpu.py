@@ -117,3 +117,26 @@ def test_missing_library_fails_loudly(tmp_path):
         ROOT, str(tmp_path / "missing.so"))
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert "LOUD" in out.stdout and "no CPU fallback" in out.stdout, out.stdout + out.stderr
+
+
+def _build_c_demo(tmp_path):
+    import shutil
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    exe = tmp_path / "abi_demo"
+    lib_dir = os.path.join(ROOT, "paper_2410_23918_b200")
+    subprocess.run(["gcc", "-O2", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "abi_demo.c"), "-L", lib_dir, "-lbitstack", "-lm",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_c_demo_compiles_links_and_fails_cleanly_without_gpu(lib, tmp_path):
+    """The header is plain C99 and the library links from C; without a GPU the first call
+    returns an ABI status (no crash, no exception across the boundary)."""
+    exe = _build_c_demo(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    if out.returncode == 0:      # a GPU is present: the demo ran to completion
+        assert "OK" in out.stdout
+    else:
+        assert out.returncode == 2 and "bitstack_create: status" in out.stdout, out.stdout + out.stderr

@@ -468,6 +468,24 @@ def test_stackset_budget_walk(bs):
                 assert O.relative_l2(y, oracle_y(blocks, s32, lv, xr)) <= 1e-3
 
 
+# ------------------------------------------------------------------ plain C use of the ABI
+def test_c_demo_runs(bs, tmp_path):
+    """examples/abi_demo.c (C99, host buffers, every level) agrees with its host reference."""
+    import shutil
+    import subprocess
+    import os
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_2410_23918_b200")
+    exe = tmp_path / "abi_demo"
+    subprocess.run(["gcc", "-O2", "-std=c99", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "abi_demo.c"), "-L", lib_dir, "-lbitstack", "-lm",
+                    f"-Wl,-rpath,{lib_dir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout + out.stderr
+
+
 # ------------------------------------------------------------------ H7: deterministic split-K
 @pytest.mark.parametrize("dtype,batch", [("bf16", 1), ("bf16", 3), ("f32", 1), ("f32", 5)])
 def test_split_k_reduction_is_deterministic(bs, dtype, batch):
