@@ -798,7 +798,9 @@ def main():
         return ms, nsteps, launches
 
     use_graph = (not args.no_graph) and world == 1
-    for i in range(args.warmup):
+    # warm-up: at least one call per layer copy, so every copy's lazily sized workspaces exist
+    # before any CUDA-graph capture (a workspace allocation cannot happen while capturing)
+    for i in range(max(args.warmup, copies)):
         step(i)
     torch.cuda.synchronize()
     l0 = pkg.launch_count()
