@@ -199,23 +199,26 @@ def run_stack(args, w, world, rank, local_rank):
         for m, name in enumerate(names):
             d_out, d_in = LLAMA31_8B_SHAPES[name]
             ww = dict(d_out=d_out, d_in=d_in, k=16, kind="decode")
-            dt, by = oracle_sample_time(ww, int(n_of[0, m]), batch, 64, reps, 1, seed_for(4, m, "blocks"))
-            tot_bytes += by
-            tot_s += dt
-        return tot_bytes / tot_s, tot_s
+            nn = int(n_of[0, m])
+            dt, _ = oracle_sample_time(ww, nn, batch, 64, reps, 1, seed_for(4, m, "blocks"))
+            tot_bytes += step_units(ww, d_out, batch, nn) * 1e9     # the whole matrix ...
+            tot_s += dt * d_out / 64                                # ... at the sampled per-row time
+        return tot_bytes / 1e9 / tot_s, tot_s
 
     if args.impl == "reference":
         if rank != 0:
             return
-        val, tot_s = oracle_stack_sample(max(1, args.steps // 100))
+        reps = max(1, min(args.steps // 100, 20))
+        val, tot_s = oracle_stack_sample(reps)
         print(json.dumps({
             "impl": "reference", "metric": metric_name(dict(kind="decode")), "value": val, "unit": "GB/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s * 1e3,
+            "n_gpus": world, "steps": reps, "warmup": 1, "ms_per_step": tot_s * 32 * 1e3,   # 32 layers per token
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (stored-form random blocks, synthetic/ recipe)",
             "config": {"workload": w["label"], "batch": batch, "parallelism": "cpu", "sample_rows": 64},
             "cpu_baseline": {"value": val, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-                             "sample": "dense oracle (fp64 numpy) for 64 rows of each of layer 0's 7 matrices"},
+                             "sample": "dense oracle (fp64 numpy) for 64 rows of each of layer 0's 7 matrices, "
+                                       "scaled to whole matrices (x 32 layers for ms_per_step)"},
             "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
     import torch
@@ -700,17 +703,25 @@ def main():
         if rank != 0:
             return
         budget_s = 60.0
-        # bounded row sample: calibrate on 16 rows, then size the sample to the budget
+        # bounded row sample: calibrate on 16 rows, then size the per-step sample (>= 1 row) so
+        # that --steps K --warmup W fit the budget; with a very large K only as many steps as
+        # fit are timed (reported in "steps")
         t16, _ = oracle_sample_time(w, n, batch, 16, 1, 0, seed_for(2, 0, "blocks"))
-        rows = int(max(16, min(w["d_out"], 16 * budget_s / max(t16, 1e-6) / (args.steps + args.warmup))))
-        dt, by = oracle_sample_time(w, n, batch, rows, args.steps, args.warmup, seed_for(2, 0, "blocks"))
-        val = by / dt
+        t_row = max(t16 / 16.0, 1e-7)
+        rows = int(max(16, min(w["d_out"], budget_s / (t_row * (args.steps + args.warmup)))))
+        steps_run = int(min(args.steps, max(3, budget_s / (t_row * rows))))
+        warm_run = min(args.warmup, 3)
+        dt, _ = oracle_sample_time(w, n, batch, rows, steps_run, warm_run, seed_for(2, 0, "blocks"))
+        # the whole layer's work at the sampled per-row time (the per-block V / x terms of a
+        # row sample would otherwise inflate a small sample's throughput)
+        val = step_units(w, w["d_out"], batch, n) / (dt * w["d_out"] / rows)
         line = {
-            "impl": "reference", "metric": metric_name(w), "value": val, "unit": unit_name(w), "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (stored-form random blocks, synthetic/ recipe)",
+            "impl": "reference", "metric": metric_name(w), "value": val, "unit": unit_name(w), "n_gpus": world, "steps": steps_run, "warmup": warm_run,
+            "ms_per_step": dt * 1e3 * w["d_out"] / rows, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (stored-form random blocks, synthetic/ recipe)",
             "config": {"workload": w["label"], "d_out": w["d_out"], "d_in": w["d_in"], "n": n, "k": w["k"],
-                       "batch": batch, "parallelism": "cpu", "sample_rows": rows},
+                       "batch": batch, "parallelism": "cpu", "sample_rows": rows,
+                       "timing": "per-step row sample, scaled to the whole layer"},
             "cpu_baseline": {"value": val, "unit": unit_name(w), "cores": cpu_cores(), "kind": "oracle",
                              "sample": f"dense oracle (fp64 numpy) for {rows} of {w['d_out']} output rows, all {n} blocks"},
             "e2e": {"value": val, "unit": unit_name(w), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -923,10 +934,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rows_s = 256
-        dt, by = oracle_sample_time(w, n, batch, rows_s, 1, 0, seed_for(2, 0, "blocks"))
-        cpu = {"value": by / dt, "unit": unit_name(w), "cores": cpu_cores(), "kind": "oracle",
+        dt, _ = oracle_sample_time(w, n, batch, rows_s, 1, 0, seed_for(2, 0, "blocks"))
+        cpu = {"value": step_units(w, d_out, batch, n) / (dt * d_out / rows_s), "unit": unit_name(w),
+               "cores": cpu_cores(), "kind": "oracle",
                "sample": f"dense oracle (fp64 numpy, Eq.8+Eq.4) for {rows_s} of {d_out} output rows, "
-                         f"all {n} blocks, 1 call ({dt:.2f} s)"}
+                         f"all {n} blocks, 1 call ({dt:.2f} s), scaled to the whole layer"}
 
     # N > 1: the NCCL all-gather of the output slices timed alone (kernel,
     # collective and end-to-end reported separately); all ranks take part
