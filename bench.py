@@ -53,6 +53,17 @@ WORKLOADS = {
 }
 
 
+def traffic_key(key):
+    """DRAM read + write bytes of the roofline kernel(s) per launch (per token-step for C4) from
+    profiles/traffic.json (one ncu capture, scripts/gpu_traffic.sh / gpu_c4_traffic.sh), or None."""
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(tpath) as f:
+            return json.load(f).get(key)
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def peaks(kind="decode"):
     """Roofline denominator: HBM copy GB/s (decode), or dense bf16 TFLOP/s sustained (prefill
     GEMM with fp16 operands: same tensor rate as bf16, nominal ratio 1)."""
@@ -359,7 +370,9 @@ def run_stack(args, w, world, rank, local_rank):
                        "grouping": "per matrix" if args.no_group else "grouped per shared input: {q,k,v},{o},{gate,up},{down}",
                        "timing": "CUDA-graph replay of the token's calls" if graph is not None else "eager launches"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None, "peak_source": peak_src,
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": None if args.no_group else traffic_key(f"c4_b{batch}_g{world}"),
+                         "peak_source": peak_src,
                          "kernel": "zq + decode_f8i kernel pairs (sum over the token's calls)",
                          "kernel_us": kms * 1e3, "kernel_launches_timed": nk},
             "clocks": clocks,
@@ -849,15 +862,7 @@ def main():
         dom_name = "bs::prefill_gemm_kernel<BN> (BN = 128 or 256 by wave fill)"
     achieved = dom_units / (kernel_ms * 1e-3)
     peak, peak_src = peaks("decode" if decode_path else "prefill")
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                tj = json.load(f)
-            traffic = tj.get(f"{args.workload}_n{n}_b{batch}_g{world}")
-        except Exception:  # noqa: BLE001
-            traffic = None
+    traffic = traffic_key(f"{args.workload}_n{n}_b{batch}_g{world}")
 
     # ---- e2e: public API with host buffers (pinned), copies inside the timed region
     x_h = x.cpu().pin_memory()

@@ -143,10 +143,31 @@ def traffic_only(rep_name, key, regex):
     print(key, total, seen)
 
 
+def traffic_csv(csv_path, key):
+    """profiles/traffic.json[key] = DRAM read + write bytes summed over EVERY launch in an
+    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --csv` log (a whole step of
+    many launches, e.g. one C4 token-step)."""
+    import csv
+    total, launches = 0.0, set()
+    with open(csv_path) as f:
+        rows = [l for l in f if l.startswith('"')]
+    for r in csv.DictReader(rows):
+        if r.get("Metric Name") in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += to_bytes(r["Metric Value"].replace(",", ""), r["Metric Unit"])
+            launches.add(r["ID"])
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    tj = json.load(open(tp)) if os.path.exists(tp) else {}
+    tj[key] = total
+    json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
+    print(key, total, "bytes over", len(launches), "launches")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 2 and sys.argv[2] == "prefill":
         prefill(sys.argv[1])
     elif len(sys.argv) > 1 and sys.argv[1] == "traffic":
         traffic_only(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif len(sys.argv) > 1 and sys.argv[1] == "traffic_csv":
+        traffic_csv(sys.argv[2], sys.argv[3])
     else:
         main(*sys.argv[1:])
