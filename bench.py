@@ -197,11 +197,15 @@ def run_stack(args, w, world, rank, local_rank):
     # per-matrix levels from the memory budget with the Average ordering (budget.average_levels,
     # P:142-146): Eq.9 block sizes, 2004.5 MiB of embeddings / head / norms outside the stacks
     # (SURVEY Q15), a seeded permutation of the 224 matrices as the within-level order
-    from paper_2410_23918_b200.budget import average_levels as budget_levels
+    from paper_2410_23918_b200.budget import average_levels as budget_levels, prefix_levels, universal_stack
     eq9 = [(d_out * d_in + 16 * 16 * (d_out + d_in)) / 8.0
            for _ in range(32) for d_out, d_in in (LLAMA31_8B_SHAPES[nm] for nm in names)]
     order = np.random.default_rng(seed_for(4, 0, "blocks")).permutation(len(eq9)).tolist()
-    n_of = np.array(budget_levels(eq9, (budget_mib - 2004.5) * 2 ** 20, order)).reshape(32, len(names))
+    if args.order == "random":   # the paper's Random sorting over n = 16 blocks per stack
+        stack = universal_stack([16] * len(eq9), "random", seed=404)
+        n_of = np.array(prefix_levels(stack, eq9, (budget_mib - 2004.5) * 2 ** 20)).reshape(32, len(names))
+    else:
+        n_of = np.array(budget_levels(eq9, (budget_mib - 2004.5) * 2 ** 20, order)).reshape(32, len(names))
     level = float(np.dot(n_of.reshape(-1), eq9) / sum(eq9))   # loaded levels in model-size units
     batch = args.batch or 1
     def oracle_stack_sample(reps):
@@ -244,22 +248,25 @@ def run_stack(args, w, world, rank, local_rank):
         dist.barrier()
     import paper_2410_23918_b200 as pkg
     pkg.load_library()
-    # one set of stored-form blocks per matrix type (4 blocks: the maximum level), loaded into
-    # 32 independent handles each (every handle owns its device copy: 3.7 GB of weights)
+    # one set of stored-form blocks per matrix type (as many as the highest level), of which each
+    # of the 32 handles loads its own level's prefix (every handle owns its device copy: 3.7 GB
+    # of weights, the budget)
     layers, total_bytes = [], 0.0
     xs = {d: torch.from_numpy(make_x(batch, channel_gains(d, 5), 6).astype(np.float32)).to(torch.bfloat16).cuda()
           for d in (4096, 14336)}
     for m, name in enumerate(names):
         d_out, d_in = LLAMA31_8B_SHAPES[name]
-        signs, u32, v32, s = make_random_blocks(4, d_out, d_in, 16, seed=seed_for(4, m, "blocks"))
+        nmax = max(1, int(n_of[:, m].max()))
+        signs, u32, v32, s = make_random_blocks(nmax, d_out, d_in, 16, seed=seed_for(4, m, "blocks"))
         u_bf = torch.from_numpy(u32).to(torch.bfloat16)
         v_bf = torch.from_numpy(v32).to(torch.bfloat16)
         r0, r1 = d_out * rank // world, d_out * (rank + 1) // world
         for layer in range(32):
-            lay = pkg.Layer(d_out, d_in, k=16, n_capacity=4, factor_dtype="bf16", row_begin=r0, row_end=r1,
-                            device=local_rank)
-            lay.load_blocks(0, signs, u_bf, v_bf, s)
             nn = int(n_of[layer, m])
+            lay = pkg.Layer(d_out, d_in, k=16, n_capacity=max(nn, 1), factor_dtype="bf16", row_begin=r0,
+                            row_end=r1, device=local_rank)
+            if nn:
+                lay.load_blocks(0, signs[:nn], u_bf[:nn], v_bf[:nn], s)
             lay.set_num_blocks(nn)
             y = torch.empty((batch, r1 - r0), dtype=torch.float32, device="cuda")
             yf = torch.empty((world * batch, r1 - r0), dtype=torch.float32, device="cuda") if world > 1 else None
@@ -368,10 +375,12 @@ def run_stack(args, w, world, rank, local_rank):
                        "l2": "inputs larger than L2 (3.7 GB of blocks per token-step)",
                        "calls_per_token": len(groups),
                        "grouping": "per matrix" if args.no_group else "grouped per shared input: {q,k,v},{o},{gate,up},{down}",
+                       "sorting": args.order, "level_range": [int(n_of.min()), int(n_of.max())],
                        "timing": "CUDA-graph replay of the token's calls" if graph is not None else "eager launches"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
-                         "traffic": None if args.no_group else traffic_key(f"c4_b{batch}_g{world}"),
+                         "traffic": (None if args.no_group or args.order != "average"
+                                     else traffic_key(f"c4_b{batch}_g{world}")),
                          "peak_source": peak_src,
                          "kernel": "zq + decode_f8i kernel pairs (sum over the token's calls)",
                          "kernel_us": kms * 1e3, "kernel_launches_timed": nk},
@@ -694,6 +703,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-group", action="store_true",
                     help="c4: one bitstack_matmul per matrix instead of grouped calls per shared input")
+    ap.add_argument("--order", choices=["average", "random"], default="average",
+                    help="c4: the universal stack's sorting (P:351); Greedy needs measured perplexities")
     ap.add_argument("--sweep", action="store_true", help="also report us/layer for n = 1, 2, 4, 8, 16")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -167,10 +167,11 @@ BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x
  * Each member keeps its own level n_i, dtypes of x / y are shared, xs[i] / ys[i] follow
  * bitstack_matmul's layouts (xs[i] may be the same buffer for several members).
  * When count <= 8, 1 <= batch < 16, the members are distinct handles on one device on the
- * e4m3 decode path (bf16/f16 factors, d_in % 8 == 0, n_i >= 1, AUTO or TC kernel)
- * and all xs / ys are 16-byte aligned device buffers, the whole group runs as ONE Zq launch
- * and ONE decode launch per chunk of <= 4 tokens, whose CTAs are shared out among the members
- * in proportion to their work; otherwise the members run one after another through
+ * e4m3 decode path (bf16/f16 factors, d_in % 8 == 0, AUTO or TC kernel) and all xs / ys are
+ * 16-byte aligned device buffers, the whole group runs as ONE Zq launch and ONE decode launch
+ * per chunk of <= 4 tokens, whose CTAs are shared out among the members in proportion to their
+ * work; members at level n_i == 0 get ys[i] = 0 (a memset) and no share of the launches (no
+ * launch at all when every member is at level 0); otherwise the members run one after another through
  * bitstack_matmul (from 16 tokens that is the prefill path of each member).  Results are
  * identical to the individual calls either way.  With profiling enabled the fused pair is
  * bracketed once.  count == 0 or batch == 0 is a no-op.

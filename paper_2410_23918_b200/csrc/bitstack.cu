@@ -1110,14 +1110,29 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   // otherwise the members run one after another through bitstack_matmul (same results).
   bool fused = count <= bs::kMaxGroup && batch >= 1 && batch < kPrefillMinBatch && decode_issuer() &&
                valid_dtype(x_dtype) && (y_dtype == BITSTACK_F32 || y_dtype == BITSTACK_BF16);
+  // members at level 0 (possible under any budget below one level, and common under the Random
+  // and Greedy sortings) get y = 0 and stay out of the launches; the rest run fused
+  bitstack_layer fl[bs::kMaxGroup];
+  const void* fx[bs::kMaxGroup];
+  void* fy[bs::kMaxGroup];
+  int fc = 0, zero[bs::kMaxGroup], zc = 0;
   for (int i = 0; fused && i < count; ++i) {
     bitstack_layer L = layers[i];
-    fused = L && xs[i] && ys[i] && L->device == layers[0]->device && L->layout == 1 && L->n_res > 0 &&
-            L->n_act > 0 && L->n_act <= L->n_res && L->d_in % 8 == 0 &&
-            (L->kernel == BITSTACK_KERNEL_AUTO || L->kernel == BITSTACK_KERNEL_TC) &&
-            (reinterpret_cast<uintptr_t>(xs[i]) % 16) == 0 && mem_kind(xs[i]) == kMemDevice &&
-            mem_kind(ys[i]) == kMemDevice;
+    fused = L && xs[i] && ys[i] && L->device == layers[0]->device && mem_kind(ys[i]) == kMemDevice;
     for (int j = 0; fused && j < i; ++j) fused = layers[j] != L;   // each member owns its workspaces
+    if (fused && L->n_act == 0) {
+      zero[zc++] = i;
+      continue;
+    }
+    fused = fused && L->layout == 1 && L->n_res > 0 && L->n_act <= L->n_res && L->d_in % 8 == 0 &&
+            (L->kernel == BITSTACK_KERNEL_AUTO || L->kernel == BITSTACK_KERNEL_TC) &&
+            (reinterpret_cast<uintptr_t>(xs[i]) % 16) == 0 && mem_kind(xs[i]) == kMemDevice;
+    if (fused) {
+      fl[fc] = L;
+      fx[fc] = xs[i];
+      fy[fc] = ys[i];
+      ++fc;
+    }
   }
   if (!fused) {
     for (int i = 0; i < count; ++i) {
@@ -1131,19 +1146,21 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype), ysz = y_dtype == BITSTACK_F32 ? 4 : 2;
+  for (int z = 0; z < zc; ++z)
+    CK(cudaMemsetAsync(ys[zero[z]], 0, (size_t)(batch * layers[zero[z]]->rows_local * ysz), st));
   // batch chunks of <= 4 tokens (the decode kernels' widest batch class), one launch pair each
-  for (int64_t b0 = 0; b0 < batch; b0 += 4) {
+  for (int64_t b0 = 0; fc > 0 && b0 < batch; b0 += 4) {
     const int bc = (int)std::min<int64_t>(4, batch - b0);
     const void* xc[bs::kMaxGroup];
     void* yc[bs::kMaxGroup];
-    for (int i = 0; i < count; ++i) {
-      xc[i] = reinterpret_cast<const uint8_t*>(xs[i]) + b0 * layers[i]->d_in * xsz;
-      yc[i] = reinterpret_cast<uint8_t*>(ys[i]) + b0 * layers[i]->rows_local * ysz;
+    for (int i = 0; i < fc; ++i) {
+      xc[i] = reinterpret_cast<const uint8_t*>(fx[i]) + b0 * fl[i]->d_in * xsz;
+      yc[i] = reinterpret_cast<uint8_t*>(fy[i]) + b0 * fl[i]->rows_local * ysz;
     }
     bitstack_status rs;
-    if (bc == 1) rs = launch_grouped_f8<1>(layers, count, xc, xdt, xsz, yc, ydt, ysz, bc, st);
-    else if (bc == 2) rs = launch_grouped_f8<2>(layers, count, xc, xdt, xsz, yc, ydt, ysz, bc, st);
-    else rs = launch_grouped_f8<4>(layers, count, xc, xdt, xsz, yc, ydt, ysz, bc, st);
+    if (bc == 1) rs = launch_grouped_f8<1>(fl, fc, xc, xdt, xsz, yc, ydt, ysz, bc, st);
+    else if (bc == 2) rs = launch_grouped_f8<2>(fl, fc, xc, xdt, xsz, yc, ydt, ysz, bc, st);
+    else rs = launch_grouped_f8<4>(fl, fc, xc, xdt, xsz, yc, ydt, ysz, bc, st);
     if (rs) return rs;
   }
   return BITSTACK_OK;

@@ -576,6 +576,40 @@ def test_grouped_fallbacks(bs):
     assert bs.matmul_grouped([], []) == []
 
 
+@pytest.mark.parametrize("batch", [1, 3, 6])
+def test_grouped_level_zero_members(bs, batch):
+    """Members at level 0 (budgets below one level; the Random / Greedy sortings) get y = 0 and
+    stay out of the fused launches; the others still run as ONE launch pair per <= 4 tokens."""
+    case = _grouped_case(bs, [(512, 640, 3), (300, 200, 2), (1100, 264, 4), (128, 1000, 2)], 801)
+    levels = [0, 2, 0, 1]
+    for (_, _, _, lay), n in zip(case, levels):
+        lay.set_num_blocks(n)
+    lays = [c[3] for c in case]
+    xs = [torch.from_numpy(make_x(batch, g, 60 + j).astype(np.float32)).to(torch.bfloat16).cuda()
+          for j, (g, _, _, _) in enumerate(case)]
+    ys = [torch.full((batch, l.rows), float("nan"), dtype=torch.float32, device="cuda") for l in lays]
+    grp = bs.Group(lays, [x.data_ptr() for x in xs], [y.data_ptr() for y in ys])
+    c0 = bs.launch_count()
+    grp(bs.BF16, bs.F32, batch, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    if os.environ.get("BS_DECODE_WG") != "1":
+        assert bs.launch_count() - c0 == 2 * ((batch + 3) // 4)
+    for (g, s32, blocks, lay), n, x, y in zip(case, levels, xs, ys):
+        if n == 0:
+            assert torch.count_nonzero(y) == 0          # NaN prefill overwritten by zeros
+            continue
+        xr = x.float().cpu().numpy().astype(np.float64)
+        assert O.relative_l2(y.cpu().numpy().astype(np.float64), oracle_y(blocks, s32, n, xr)) <= 1e-3
+    for _, _, _, lay in case:
+        lay.set_num_blocks(0)
+    ys2 = [torch.full_like(y, 1.0) for y in ys]       # every member at level 0: no launches at all
+    c0 = bs.launch_count()
+    bs.Group(lays, [x.data_ptr() for x in xs], [y.data_ptr() for y in ys2])(
+        bs.BF16, bs.F32, batch, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert bs.launch_count() == c0 and all(torch.count_nonzero(y) == 0 for y in ys2)
+
+
 # ------------------------------------------------------------------ H8: large-batch path
 @pytest.mark.parametrize("shape", [(384, 640), (200, 296), (1100, 264), (128, 64)])
 def test_prefill_parity_ragged(bs, shape):
