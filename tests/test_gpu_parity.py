@@ -447,18 +447,22 @@ def test_grouped_mixed_ranks_and_graph_capture(bs):
 
 
 # ------------------------------------------------------------------ memory budget
-def test_stackset_budget_walk(bs):
-    """A StackSet follows a shrinking then growing memory budget (Average ordering): levels
-    differ by at most one, fit the budget, and every layer's y matches the oracle at its level."""
+@pytest.mark.parametrize("kind", ["average", "random", "greedy"])
+def test_stackset_budget_walk(bs, kind):
+    """A StackSet follows a shrinking then growing memory budget under each sorting:
+    levels fit the budget (Average: differ by at most one), and every layer's y matches the
+    oracle at its level."""
     from paper_2410_23918_b200.budget import StackSet
     shapes = [(256, 384), (384, 256), (200, 384)]
     cases = [compress_case(d_out, d_in, 4, "bf16", 1201 + j) for j, (d_out, d_in) in enumerate(shapes)]
     lays = [make_layer(bs, d_out, d_in, blocks, s32, "bf16") for (d_out, d_in), (g, s32, blocks) in zip(shapes, cases)]
-    ss = StackSet(lays, order=[2, 0, 1])
+    scores = [[0.3, 0.9, 0.2, 0.8], [0.1, 0.5, 0.6, 0.7], [0.4, 0.45, 0.95, 0.99]] if kind == "greedy" else None
+    ss = StackSet(lays, order=[2, 0, 1] if kind == "average" else None, kind=kind, scores=scores, seed=3)
     full = sum(ss.sizes) * 4
     for frac in (1.0, 0.6, 0.3, 0.05, 0.45, 0.9):
         levels = ss.apply_budget(frac * full)
-        assert max(levels) - min(levels) <= 1
+        if kind == "average":
+            assert max(levels) - min(levels) <= 1
         assert sum(l * sz for l, sz in zip(levels, ss.sizes)) <= frac * full + 1e-6
         for lay, (g, s32, blocks), lv in zip(lays, cases, levels):
             assert lay.info()["n_active"] == lv
