@@ -127,10 +127,14 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
       long long ui = (long long)(iv >> p.ksh) * p.nq;   // (sign block of block iv) * nq
       for (; gi < STAGES && k < nunits; ++gi) {
         const int cnt = group_count<P>(k, q, nunits, p.nq);
+#ifndef BS_EXP_NOSIGN   // timing experiment: no sign-tile copies (wrong results)
         mbar_arrive_expect_tx(&full[gi], (uint32_t)cnt * (sign_bytes + C::kZUnit));
         for (int u = 0; u < cnt; ++u)
           bulk_g2s(smem + gi * C::kStageBytes + u * C::kUnitSign, p.signs + (ui + q + u) * p.rows_pad + row0,
                    sign_bytes, &full[gi], pol_sign);
+#else
+        mbar_arrive_expect_tx(&full[gi], (uint32_t)cnt * C::kZUnit);
+#endif
         k += cnt;
         q += cnt;
         if (q == p.nq) { q = 0; ++iv; ui = (long long)(iv >> p.ksh) * p.nq; }
@@ -154,9 +158,13 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
         const int cnt = group_count<P>(k, q, nunits, p.nq);
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + s * C::kStageBytes;
+#ifndef BS_EXP_NOSIGN
         mbar_arrive_expect_tx(&full[s], (uint32_t)cnt * (sign_bytes + C::kZUnit));
         for (int u = 0; u < cnt; ++u)
           bulk_g2s(st + u * C::kUnitSign, p.signs + (ui + q + u) * p.rows_pad + row0, sign_bytes, &full[s], pol_sign);
+#else
+        mbar_arrive_expect_tx(&full[s], (uint32_t)cnt * C::kZUnit);
+#endif
         bulk_g2s(st + C::kOffZ, p.zq + (u0 + k) * C::kZUnit, (uint32_t)cnt * C::kZUnit, &full[s], pol_keep);
         k += cnt;
         q += cnt;
@@ -203,10 +211,13 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
           for (int u = 0; u < P; ++u) {
             if (u < cnt) {
 #pragma unroll
-              for (int m = 0; m < kSubK / 32; ++m)
+              for (int m = 0; m < kSubK / 32; ++m) {
+#ifndef BS_EXP_SKEL   // timing experiment (scripts/exp_skeleton.sh): no MMAs
                 mma_f8_ts(d_acc, a_col + (uint32_t)(C::kACols * u + 8 * m),
                           bdesc0 + (uint64_t)((u * C::kZUnit + m * 2 * C::LBO) >> 4), idesc,
                           (m > 0 || u > 0 || !first) ? 1u : 0u);
+#endif
+              }
             }
           }
           mma_commit(&a_empty[t * NSLOT + slot]);
@@ -271,11 +282,16 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
           if (a_exp != a_raw && lane == 0 && p.status) atomicOr(p.status, 1);   // beyond the e4m3 A range
           const uint32_t e8 = (uint32_t)((7 + a_exp) << 3) * 0x01010101u;
           uint32_t o[32];
+#ifndef BS_EXP_SKEL   // timing experiment: no expansion / TMEM stores (wrong results)
           expand_e4m3(sw.x, e8, o);
           expand_e4m3(sw.y, e8, o + 8);
           expand_e4m3(sw.z, e8, o + 16);
           expand_e4m3(sw.w, e8, o + 24);
           tmem_st32(a_addr + (uint32_t)(C::kACols * u), o);
+#else
+          (void)o;
+          if ((sw.x ^ sw.y ^ sw.z ^ sw.w ^ e8) == 0x12345u && p.status) p.status[1] = 1;
+#endif
         }
       }
       if (warp == 5) BS_ITRACE(gk, 2);
