@@ -16,6 +16,13 @@
 
 namespace bs {
 
+#ifndef BS_F8_STAGES
+#define BS_F8_STAGES 6      // ring depth cap (scripts/exp_stages.sh: 6 beats 4, 8, 10, 12, 14, 15)
+#endif
+#ifndef BS_F8_SMEM_KB
+#define BS_F8_SMEM_KB 200   // shared memory the ring may use per SM
+#endif
+
 template <int NB, int R_, int P_ = 1, int OCC_ = 1>
 struct DecodeF8ICfg {
   static constexpr int OCC = OCC_;                           // resident CTAs per SM (TMEM / smem split)
@@ -29,8 +36,8 @@ struct DecodeF8ICfg {
   static constexpr int kUnitSign = R * kTileRows * 16;       // sign bytes of one unit (R row tiles)
   static constexpr int kOffZ = P * kUnitSign;                // Zq of unit u at kOffZ + u kZUnit
   static constexpr int kStageBytes = (kOffZ + P * kZUnit + 127) / 128 * 128;
-  static constexpr int S0 = (200 * 1024 / OCC_) / kStageBytes;
-  static constexpr int STAGES = S0 > 12 ? 12 : (S0 < 2 ? 2 : S0);
+  static constexpr int S0 = (BS_F8_SMEM_KB * 1024 / OCC_) / kStageBytes;
+  static constexpr int STAGES = S0 > BS_F8_STAGES ? BS_F8_STAGES : (S0 < 2 ? 2 : S0);
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes;
   static constexpr uint32_t kTmemCols = 512 / OCC_;

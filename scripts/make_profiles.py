@@ -121,8 +121,10 @@ def main(r, key="c2_n16_b1_g1"):
     tj = json.load(open(tp)) if os.path.exists(tp) else {}
     tj[key] = traffic
     tj["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per call of the roofline's dominant kernel, "
-                   "from one ncu --set full capture: decode keys = the zq_kernel + decode_f8_kernel pair, "
-                   "prefill (c3_*) keys = prefill_gemm_kernel; keys <workload>_n<n>_b<batch>_g<world>")
+                   "from one ncu capture: decode keys = the zq_kernel + decode_f8i_kernel pair, "
+                   "prefill (c3_*) keys = prefill_gemm_kernel; keys <workload>_n<n>_b<batch>_g<world>; "
+                   "c4_b<batch>_g<world> = summed over the 256 launches of one C4 token-step "
+                   "(scripts/gpu_c4_traffic.sh)")
     json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
     print("\n".join(lines + out))
 
@@ -141,6 +143,39 @@ def traffic_only(rep_name, key, regex):
     tj[key] = total
     json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
     print(key, total, seen)
+
+
+def c4_launches(r):
+    """profiles/<r>_c4_launches.txt from gpurun_out/c4_launches.csv (scripts/gpu_sweeps.sh): the
+    launches of one eager C4 token-step in order, zq then decode per group, 4 groups per layer."""
+    rows = list(csv.reader(open(os.path.join(ROOT, "gpurun_out", "c4_launches.csv"))))
+    i = next(k for k, x in enumerate(rows) if x and x[0] == "ID")
+    hdr = rows[i]
+    us = []
+    for x in rows[i + 1:]:
+        d = dict(zip(hdr, x))
+        if d.get("Metric Name") == "gpu__time_duration.sum":
+            us.append((d["Kernel Name"], float(d["Metric Value"].replace(",", "")) *
+                       {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(d["Metric Unit"], 1.0)))
+    assert len(us) == 256, len(us)
+    groups = ["{q,k,v}", "{o}", "{gate,up}", "{down}"]
+    zq = {g: [] for g in groups}
+    dec = {g: [] for g in groups}
+    for j in range(128):
+        g = groups[j % 4]
+        (n0, t0), (n1, t1) = us[2 * j], us[2 * j + 1]
+        assert "zq" in n0 and "decode" in n1
+        zq[g].append(t0)
+        dec[g].append(t1)
+    tot = sum(t for _, t in us)
+    lines = ["# ncu launch list of `python bench.py --workload c4 --steps 3 --warmup 3 --no-cpu-baseline --no-graph`",
+             "# (-k regex:'zq_grouped|decode_f8i_grouped', 128 launch pairs = 32 layers x 4 groups; --clock-control none,",
+             "#  cold-cache and serialised: compare shares). Per group type, average over the layers:",
+             f"{'group':14s} {'zq_us':>6s} {'decode_us':>10s} {'share':>7s}"]
+    for g in groups:
+        lines.append(f"{g:14s} {sum(zq[g]) / 32:6.2f} {sum(dec[g]) / 32:10.2f} {(sum(zq[g]) + sum(dec[g])) / tot:7.3f}")
+    lines.append(f"# zq share of the token's kernel time: {sum(sum(v) for v in zq.values()) / tot:.3f}")
+    open(os.path.join(ROOT, "profiles", f"{r}_c4_launches.txt"), "w").write("\n".join(lines) + "\n")
 
 
 def traffic_csv(csv_path, key):
@@ -167,6 +202,8 @@ if __name__ == "__main__":
         prefill(sys.argv[1])
     elif len(sys.argv) > 1 and sys.argv[1] == "traffic":
         traffic_only(sys.argv[2], sys.argv[3], sys.argv[4])
+    elif len(sys.argv) > 2 and sys.argv[2] == "c4":
+        c4_launches(sys.argv[1])
     elif len(sys.argv) > 1 and sys.argv[1] == "traffic_csv":
         traffic_csv(sys.argv[2], sys.argv[3])
     else:
