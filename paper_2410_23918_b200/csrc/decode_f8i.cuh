@@ -19,6 +19,9 @@ namespace bs {
 #ifndef BS_F8_STAGES
 #define BS_F8_STAGES 6      // ring depth cap (scripts/exp_stages.sh: 6 beats 4, 8, 10, 12, 14, 15)
 #endif
+#ifndef BS_F8_PRE
+#define BS_F8_PRE 2         // ring stages whose sign tiles are requested before griddepcontrol.wait
+#endif
 #ifndef BS_F8_SMEM_KB
 #define BS_F8_SMEM_KB 200   // shared memory the ring may use per SM
 #endif
@@ -132,7 +135,7 @@ __device__ __forceinline__ void decode_f8i_body(const DecodeParams& p, const int
       // first STAGES groups: sign tiles before the dependency wait, then their Zq
       int k = 0, q = q_start, gi = 0, iv = i_start;
       long long ui = (long long)(iv >> p.ksh) * p.nq;   // (sign block of block iv) * nq
-      for (; gi < STAGES && k < nunits; ++gi) {
+      for (; gi < (BS_F8_PRE < STAGES ? BS_F8_PRE : STAGES) && k < nunits; ++gi) {
         const int cnt = group_count<P>(k, q, nunits, p.nq);
 #ifndef BS_EXP_NOSIGN   // timing experiment: no sign-tile copies (wrong results)
         mbar_arrive_expect_tx(&full[gi], (uint32_t)cnt * (sign_bytes + C::kZUnit));
