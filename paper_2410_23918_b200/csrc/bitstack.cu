@@ -19,8 +19,7 @@
 
 #include "aux_kernels.cuh"
 #include "compress.cuh"
-#include "decode_f8.cuh"
-#include "decode_f8i.cuh"
+#include "decode_mx.cuh"
 #include "decode_tc.cuh"
 #include "prefill.cuh"
 
@@ -46,7 +45,6 @@ struct bitstack_layer_s {
   float* y_part = nullptr; // [max(2 sm_count, row_tiles)][kPartStride] split-K partial slots (<= 2 CTAs/SM)
   uint8_t* zq = nullptr;   // e4m3 path: Zq units of the current call (grown on demand)
   int64_t zq_bytes = 0;
-  int* status = nullptr;   // sticky device-side numeric-range flag
   int* counters = nullptr; // [row_tiles]
   uint8_t* pf_w = nullptr; // prefill path: W' operand image (transient workspace, grown on demand)
   uint8_t* pf_x = nullptr; // prefill path: X' operand image
@@ -161,53 +159,23 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
 // e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
 constexpr int64_t kPrefillMinBatch = 16;   // AUTO: restored-tile GEMM path from this batch on
 
-// Decode kernel choice: the per-warpgroup-issuer kernel (decode_f8i.cuh) by default;
-// BS_DECODE_WG=1 selects the previous self-issuing warpgroup kernel (A/B measurements).
-bool decode_issuer() {
-  static const bool v = [] { const char* e = getenv("BS_DECODE_WG"); return !(e && e[0] == '1'); }();
-  return v;
-}
-
-// e4m3 decode geometry per batch class: R row tiles per CTA, P units per hand-off
-// (decode_f8i.cuh).  TMEM: R x 2 x P x 32 A columns + R x 48 NB accumulator columns <= 512.
-#ifndef BS_F8_R1
-#define BS_F8_R1 4
-#endif
-#ifndef BS_F8_P1
-#define BS_F8_P1 1
-#endif
-#ifndef BS_F8_P2
-#define BS_F8_P2 2
-#endif
-#ifndef BS_F8_OCC1
-#define BS_F8_OCC1 1
-#endif
-template <int NB> struct F8Geom;   // OCC: resident decode CTAs per SM (each with 512/OCC TMEM columns)
-template <> struct F8Geom<1> { static constexpr int R = BS_F8_R1, P = BS_F8_P1, OCC = BS_F8_OCC1; };
-#ifndef BS_F8_R2
-#define BS_F8_R2 2
-#endif
-template <> struct F8Geom<2> { static constexpr int R = BS_F8_R2, P = BS_F8_P2, OCC = 1; };
-template <> struct F8Geom<4> { static constexpr int R = 2, P = 1, OCC = 1; };
-
-// Z workspace of layer L for `units` (block, 128-column chunk) pairs at batch class NB; grows
-// once per larger batch class (a stream sync + cudaMalloc), never inside steady state.
+// ------------------------------------------------------------------ MX e4m3 decode (decode_mx.cuh)
+// Zq workspace for batch class NB: one unit per (block half, 128-column chunk) of the capacity.
 template <int NB>
-bitstack_status ensure_zq(bitstack_layer L, int64_t units, cudaStream_t st) {
-  using C = bs::DecodeF8Cfg<NB, F8Geom<NB>::R>;
-  if (units * C::kZUnit <= L->zq_bytes) return BITSTACK_OK;
+bitstack_status ensure_zq_mx(bitstack_layer L, cudaStream_t st) {
+  const int64_t cap = (int64_t)L->n_cap * L->kh * L->nq * bs::MxCfg<NB>::kUnit;
+  if (cap <= L->zq_bytes) return BITSTACK_OK;
   CK(cudaStreamSynchronize(st));
   cudaFree(L->zq);
   L->zq = nullptr;
-  const int64_t cap = (int64_t)L->n_cap * L->kh * L->nq * C::kZUnit;
   CK(cudaMalloc((void**)&L->zq, (size_t)cap));
   L->bytes += cap - L->zq_bytes;
   L->zq_bytes = cap;
   return BITSTACK_OK;
 }
 
-bs::ZqParams zq_params(bitstack_layer L, const bs::DecodeParams& p) {
-  bs::ZqParams zp;
+bs::ZqMxParams zq_mx_params(bitstack_layer L, const bs::DecodeParams& p) {
+  bs::ZqMxParams zp;
   zp.v = p.v;
   zp.inv_s = p.inv_s;
   zp.x = p.x;
@@ -215,7 +183,6 @@ bs::ZqParams zq_params(bitstack_layer L, const bs::DecodeParams& p) {
   zp.x_stride = p.x_stride;
   zp.nq = p.nq;
   zp.d_in = p.d_in;
-  zp.d_in_pad = p.d_in_pad;
   zp.batch = p.batch;
   zp.x_dtype = p.x_dtype;
   zp.f_dtype = p.f_dtype;
@@ -224,44 +191,75 @@ bs::ZqParams zq_params(bitstack_layer L, const bs::DecodeParams& p) {
 }
 
 template <int NB>
-bitstack_status launch_decode_f8(bitstack_layer L, const bs::DecodeParams& prm_in, int grid, cudaStream_t st) {
-  using G = F8Geom<NB>;
-  using C = bs::DecodeF8Cfg<NB, G::R>;
-  using CI = bs::DecodeF8ICfg<NB, G::R, G::P, G::OCC>;
-  static std::atomic<unsigned long long> attr_done{0};
-  bitstack_status attr_rs = once_per_device(attr_done, [&]() -> bitstack_status {
-    CK(cudaFuncSetAttribute(bs::decode_f8_kernel<NB, G::R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+bitstack_status mx_attrs() {
+  static std::atomic<unsigned long long> done{0};
+  return once_per_device(done, [&]() -> bitstack_status {
+    using C = bs::DecodeMxCfg<NB>;
+    constexpr int zs = bs::MxCfg<NB>::kUnit;
+    CK(cudaFuncSetAttribute(bs::zq_mx_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zs));
+    CK(cudaFuncSetAttribute(bs::zq_mx_grouped_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zs));
+    CK(cudaFuncSetAttribute(bs::decode_mx_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
+    CK(cudaFuncSetAttribute(bs::decode_mx_grouped_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             C::kSmemBytes));
-    CK(cudaFuncSetAttribute(bs::decode_f8i_kernel<NB, G::R, G::P, G::OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            CI::kSmemBytes));
     return BITSTACK_OK;
   });
-  if (attr_rs) return attr_rs;
-  const bool iss = decode_issuer();
-  const int64_t units = (int64_t)prm_in.n * prm_in.nq;
-  bitstack_status zs = ensure_zq<NB>(L, units, st);
-  if (zs) return zs;
-  const bs::ZqParams zp = zq_params(L, prm_in);
-  bs::zq_kernel<NB><<<(unsigned)units, 128, 0, st>>>(zp);
-  count_launch();
-  CK(cudaGetLastError());
-  bs::DecodeParams prm = prm_in;
-  prm.zq = L->zq;
-  prm.status = L->status;
+}
+
+cudaLaunchConfig_t pdl_config(int grid, int threads, int smem, cudaStream_t st, cudaLaunchAttribute* attr) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(iss ? CI::kThreads : C::kThreads);
-  cfg.dynamicSmemBytes = iss ? CI::kSmemBytes : C::kSmemBytes;
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = (size_t)smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (iss) CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_kernel<NB, G::R, G::P, G::OCC>, prm));
-  else CK(cudaLaunchKernelEx(&cfg, bs::decode_f8_kernel<NB, G::R>, prm));
+  return cfg;
+}
+
+// One zq_mx + one decode_mx (PDL) launch for one layer and one batch chunk of NB tokens.
+template <int NB>
+bitstack_status launch_decode_mx(bitstack_layer L, const bs::DecodeParams& prm_in, int grid, cudaStream_t st) {
+  using C = bs::DecodeMxCfg<NB>;
+  bitstack_status rs = mx_attrs<NB>();
+  if (rs) return rs;
+  rs = ensure_zq_mx<NB>(L, st);
+  if (rs) return rs;
+  const int64_t units = (int64_t)prm_in.n * prm_in.nq;
+  bs::zq_mx_kernel<NB><<<(unsigned)units, 128, bs::MxCfg<NB>::kUnit, st>>>(zq_mx_params(L, prm_in));
+  count_launch();
+  CK(cudaGetLastError());
+  bs::DecodeParams prm = prm_in;
+  prm.zq = L->zq;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = pdl_config(grid, C::kThreads, C::kSmemBytes, st, attr);
+  CK(cudaLaunchKernelEx(&cfg, bs::decode_mx_kernel<NB>, prm));
   count_launch();
   return BITSTACK_OK;
+}
+
+int mx_rows(int nb) {
+  switch (nb) {
+    case 1: return bs::MxGeom<1>::R;
+    case 2: return bs::MxGeom<2>::R;
+    case 3: return bs::MxGeom<3>::R;
+    default: return bs::MxGeom<4>::R;
+  }
+}
+
+bitstack_status dispatch_mx(int nb, bitstack_layer L, const bs::DecodeParams& prm, int grid, cudaStream_t st) {
+  switch (nb) {
+    case 1: return launch_decode_mx<1>(L, prm, grid, st);
+    case 2: return launch_decode_mx<2>(L, prm, grid, st);
+    case 3: return launch_decode_mx<3>(L, prm, grid, st);
+    case 4: return launch_decode_mx<4>(L, prm, grid, st);
+    case 5: return launch_decode_mx<5>(L, prm, grid, st);
+    case 6: return launch_decode_mx<6>(L, prm, grid, st);
+    case 7: return launch_decode_mx<7>(L, prm, grid, st);
+    case 8: return launch_decode_mx<8>(L, prm, grid, st);
+    default: return fail(BITSTACK_E_INVALID_ARG, "internal: batch chunk %d", nb);
+  }
 }
 
 bitstack_status record_prof(cudaStream_t st, bool begin, int* slot) {
@@ -467,30 +465,24 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
   prm.dbg_acc = g_dbg_acc;
   prm.dbg_z = g_dbg_z;
   prm.zq = nullptr;
-  prm.status = nullptr;
   prm.kfuse = 0;
   return prm;
 }
 
-// One zq_grouped_kernel + one decode_f8i_grouped_kernel (PDL) for `count` layers at batch
-// class NB.  The SMs are shared out in proportion to work: every layer starts at one CTA per
-// row group, then CTAs go one row group's worth at a time to the layer with the most work per
-// CTA while the total stays within one wave (sm_count CTAs, one resident per SM).
+// One zq_mx_grouped + one decode_mx_grouped launch (PDL) for `count` layers sharing a batch
+// chunk of NB tokens.  SMs are shared out in proportion to work: every layer starts at one CTA
+// per row group, then CTAs go one row group's worth at a time to the layer with the most work
+// per CTA while the total stays within one wave (one resident CTA per SM).
 template <int NB>
-bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const void* const* xs, int xdt,
-                                         int xsz, void* const* ys, int ydt, int ysz, int bc, cudaStream_t st) {
-  constexpr int R = F8Geom<NB>::R, P = F8Geom<NB>::P, OCC = F8Geom<NB>::OCC;
-  using CI = bs::DecodeF8ICfg<NB, R, P, OCC>;
-  static std::atomic<unsigned long long> attr_done{0};
-  bitstack_status attr_rs = once_per_device(attr_done, [&]() -> bitstack_status {
-    CK(cudaFuncSetAttribute(bs::decode_f8i_grouped_kernel<NB, R, P, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            CI::kSmemBytes));
-    return BITSTACK_OK;
-  });
-  if (attr_rs) return attr_rs;
-  int n_groups[bs::kMaxGroup], cpg[bs::kMaxGroup];
-  int64_t units[bs::kMaxGroup];
-  double work[bs::kMaxGroup];
+bitstack_status launch_grouped_mx(const bitstack_layer* layers, int count, const void* const* xs, int xdt, int xsz,
+                                  void* const* ys, int ydt, int ysz, int bc, cudaStream_t st) {
+  using C = bs::DecodeMxCfg<NB>;
+  constexpr int R = C::R;
+  bitstack_status rs = mx_attrs<NB>();
+  if (rs) return rs;
+  int n_groups[bs::kMaxMxGroup], cpg[bs::kMaxMxGroup];
+  int64_t units[bs::kMaxMxGroup];
+  double work[bs::kMaxMxGroup];
   int total = 0;
   for (int i = 0; i < count; ++i) {
     bitstack_layer L = layers[i];
@@ -500,7 +492,7 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
     cpg[i] = 1;
     total += n_groups[i];
   }
-  const int budget = layers[0]->sm_count * OCC;
+  const int budget = layers[0]->sm_count;
   for (;;) {
     int best = -1;
     double best_w = 0.0;
@@ -513,42 +505,48 @@ bitstack_status launch_grouped_f8(const bitstack_layer* layers, int count, const
     ++cpg[best];
     total += n_groups[best];
   }
-  bs::ZqGroup zg;
-  bs::DecodeGroup dg;
+  bs::ZqMxGroup zg;
+  bs::DecodeMxGroup dg;
   zg.count = dg.count = count;
   zg.unit_start[0] = dg.cta_start[0] = 0;
   for (int i = 0; i < count; ++i) {
     bitstack_layer L = layers[i];
-    bitstack_status zs = ensure_zq<NB>(L, units[i], st);
-    if (zs) return zs;
+    rs = ensure_zq_mx<NB>(L, st);
+    if (rs) return rs;
     bs::DecodeParams prm = decode_params(L, xs[i], xdt, xsz, ys[i], ydt, ysz, 0, bc, n_groups[i], cpg[i]);
     prm.zq = L->zq;
-    prm.status = L->status;
-    zg.prm[i] = zq_params(L, prm);
+    zg.prm[i] = zq_mx_params(L, prm);
     dg.prm[i] = prm;
     zg.unit_start[i + 1] = zg.unit_start[i] + (int)units[i];
     dg.cta_start[i + 1] = dg.cta_start[i] + n_groups[i] * cpg[i];
   }
-  for (int i = count; i < bs::kMaxGroup; ++i) zg.unit_start[i + 1] = dg.cta_start[i + 1] = 0;
+  for (int i = count; i < bs::kMaxMxGroup; ++i) zg.unit_start[i + 1] = dg.cta_start[i + 1] = 0;
   int slot = -1;
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
-  bs::zq_grouped_kernel<NB><<<(unsigned)zg.unit_start[count], 128, 0, st>>>(zg);
+  bs::zq_mx_grouped_kernel<NB><<<(unsigned)zg.unit_start[count], 128, bs::MxCfg<NB>::kUnit, st>>>(zg);
   count_launch();
   CK(cudaGetLastError());
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)dg.cta_start[count]);
-  cfg.blockDim = dim3(CI::kThreads);
-  cfg.dynamicSmemBytes = CI::kSmemBytes;
-  cfg.stream = st;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, bs::decode_f8i_grouped_kernel<NB, R, P, OCC>, dg));
+  cudaLaunchConfig_t cfg = pdl_config(dg.cta_start[count], C::kThreads, C::kSmemBytes, st, attr);
+  CK(cudaLaunchKernelEx(&cfg, bs::decode_mx_grouped_kernel<NB>, dg));
   count_launch();
   return record_prof(st, false, &slot);
+}
+
+bitstack_status dispatch_grouped_mx(int nb, const bitstack_layer* layers, int count, const void* const* xs, int xdt,
+                                    int xsz, void* const* ys, int ydt, int ysz, cudaStream_t st) {
+  switch (nb) {
+    case 1: return launch_grouped_mx<1>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    case 2: return launch_grouped_mx<2>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    case 3: return launch_grouped_mx<3>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    case 4: return launch_grouped_mx<4>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    case 5: return launch_grouped_mx<5>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    case 6: return launch_grouped_mx<6>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    case 7: return launch_grouped_mx<7>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    case 8: return launch_grouped_mx<8>(layers, count, xs, xdt, xsz, ys, ydt, ysz, nb, st);
+    default: return fail(BITSTACK_E_INVALID_ARG, "internal: batch chunk %d", nb);
+  }
 }
 
 // Per-device cuBLAS handles (created on first use).
@@ -656,7 +654,6 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * L->kh * 16 * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->y_part, (int64_t)std::max(2 * L->sm_count, L->row_tiles) * bs::kPartStride * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
-  if (e == cudaSuccess) e = alloc((void**)&L->status, 16);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     bitstack_destroy(L);
@@ -681,7 +678,6 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   if (L->pf_join) cudaEventDestroy(L->pf_join);
   cudaFree(L->y_part);
   cudaFree(L->counters);
-  cudaFree(L->status);
   cudaFree(L->zq);
   cudaFree(L->pf_w);
   cudaFree(L->pf_x);
@@ -989,52 +985,46 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
     return BITSTACK_OK;
   }
 
-  const bool f8 = L->layout == 1;          // e4m3 kernel (bf16/f16 factors); fp16 kernel for fp32 factors
-  const int nbmax = f8 ? 4 : 8;
+  const bool f8 = L->layout == 1;          // MX e4m3 kernel (bf16/f16 factors); fp16 kernel for fp32 factors
+  const int nbmax = 8;
   for (int64_t b0 = 0; b0 < batch; b0 += nbmax) {
     const int bc = (int)std::min<int64_t>(nbmax, batch - b0);
-    // k > 16 with one token: both 16-rank halves of a block in ONE N = 96 contraction (the
-    // batch-2 kernel geometry, column b = rank half b), so each sign tile is streamed once
-    if (f8 && L->kh == 2 && bc == 1 && decode_issuer()) {
-      const int R = F8Geom<2>::R;
+    int slot = -1;
+    bitstack_status ps;
+    if (f8) {
+      // k > 16 with one token: both 16-rank halves of a block in ONE N = 96 contraction (the
+      // batch-2 geometry, column group b = rank half b), so each sign tile is streamed once
+      const bool kfuse = L->kh == 2 && bc == 1;
+      const int nb = kfuse ? 2 : bc;
+      const int R = mx_rows(nb);
       const int n_groups = (L->row_tiles + R - 1) / R;
-      const int64_t units = (int64_t)L->n_act * L->nq;
-      int cpg = std::max(1, F8Geom<2>::OCC * L->sm_count / n_groups);
+      const int64_t units = (int64_t)L->n_act * (kfuse ? 1 : L->kh) * L->nq;
+      int cpg = std::max(1, L->sm_count / n_groups);
       cpg = (int)std::min<int64_t>(cpg, units);
       bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
-      prm.n = L->n_act;
-      prm.ksh = 0;
-      prm.kfuse = 1;
-      int slot = -1;
-      bitstack_status ps = record_prof(st, true, &slot);
+      if (kfuse) {
+        prm.n = L->n_act;
+        prm.ksh = 0;
+        prm.kfuse = 1;
+      }
+      ps = record_prof(st, true, &slot);
       if (ps) return ps;
-      bitstack_status rs = launch_decode_f8<2>(L, prm, n_groups * cpg, st);
+      bitstack_status rs = dispatch_mx(nb, L, prm, n_groups * cpg, st);
       if (rs) return rs;
-      ps = record_prof(st, false, &slot);
-      if (ps) return ps;
-      continue;
-    }
-    int nb = 1;
-    while (nb < bc) nb <<= 1;
-    const int R = f8 ? (nb == 1 ? F8Geom<1>::R : (nb == 2 ? F8Geom<2>::R : F8Geom<4>::R)) : r_tiles_for(nb, 2);
-    const int occ = f8 ? (nb == 1 ? F8Geom<1>::OCC : (nb == 2 ? F8Geom<2>::OCC : F8Geom<4>::OCC)) : 1;
-    const int n_groups = (L->row_tiles + R - 1) / R;
-    const int64_t units = (int64_t)L->n_act * L->kh * L->nq;
-    int cpg = std::max(1, occ * L->sm_count / n_groups);
-    cpg = (int)std::min<int64_t>(cpg, units);
-    const bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
-    int slot = -1;
-    bitstack_status ps = record_prof(st, true, &slot);
-    if (ps) return ps;
-    const int grid = n_groups * cpg;
-    bitstack_status rs;
-    if (f8) {
-      rs = nb == 1 ? launch_decode_f8<1>(L, prm, grid, st)
-                   : (nb == 2 ? launch_decode_f8<2>(L, prm, grid, st) : launch_decode_f8<4>(L, prm, grid, st));
     } else {
-      rs = dispatch_decode<2>(nb, prm, grid, st);
+      int nb = 1;
+      while (nb < bc) nb <<= 1;
+      const int R = r_tiles_for(nb, 2);
+      const int n_groups = (L->row_tiles + R - 1) / R;
+      const int64_t units = (int64_t)L->n_act * L->kh * L->nq;
+      int cpg = std::max(1, L->sm_count / n_groups);
+      cpg = (int)std::min<int64_t>(cpg, units);
+      const bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
+      ps = record_prof(st, true, &slot);
+      if (ps) return ps;
+      bitstack_status rs = dispatch_decode<2>(nb, prm, n_groups * cpg, st);
+      if (rs) return rs;
     }
-    if (rs) return rs;
     ps = record_prof(st, false, &slot);
     if (ps) return ps;
   }
@@ -1108,14 +1098,14 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   if (count == 0 || batch == 0) return BITSTACK_OK;
   // One launch pair when every member can take the e4m3 decode kernel on device buffers;
   // otherwise the members run one after another through bitstack_matmul (same results).
-  bool fused = count <= bs::kMaxGroup && batch >= 1 && batch < kPrefillMinBatch && decode_issuer() &&
+  bool fused = count <= bs::kMaxMxGroup && batch >= 1 && batch < kPrefillMinBatch &&
                valid_dtype(x_dtype) && (y_dtype == BITSTACK_F32 || y_dtype == BITSTACK_BF16);
   // members at level 0 (possible under any budget below one level, and common under the Random
   // and Greedy sortings) get y = 0 and stay out of the launches; the rest run fused
-  bitstack_layer fl[bs::kMaxGroup];
-  const void* fx[bs::kMaxGroup];
-  void* fy[bs::kMaxGroup];
-  int fc = 0, zero[bs::kMaxGroup], zc = 0;
+  bitstack_layer fl[bs::kMaxMxGroup];
+  const void* fx[bs::kMaxMxGroup];
+  void* fy[bs::kMaxMxGroup];
+  int fc = 0, zero[bs::kMaxMxGroup], zc = 0;
   for (int i = 0; fused && i < count; ++i) {
     bitstack_layer L = layers[i];
     fused = L && xs[i] && ys[i] && L->device == layers[0]->device && mem_kind(ys[i]) == kMemDevice;
@@ -1148,19 +1138,16 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   const int xsz = dsize(x_dtype), ysz = y_dtype == BITSTACK_F32 ? 4 : 2;
   for (int z = 0; z < zc; ++z)
     CK(cudaMemsetAsync(ys[zero[z]], 0, (size_t)(batch * layers[zero[z]]->rows_local * ysz), st));
-  // batch chunks of <= 4 tokens (the decode kernels' widest batch class), one launch pair each
-  for (int64_t b0 = 0; fc > 0 && b0 < batch; b0 += 4) {
-    const int bc = (int)std::min<int64_t>(4, batch - b0);
-    const void* xc[bs::kMaxGroup];
-    void* yc[bs::kMaxGroup];
+  // batch chunks of <= 8 tokens (the decode kernel's widest batch class), one launch pair each
+  for (int64_t b0 = 0; fc > 0 && b0 < batch; b0 += 8) {
+    const int bc = (int)std::min<int64_t>(8, batch - b0);
+    const void* xc[bs::kMaxMxGroup];
+    void* yc[bs::kMaxMxGroup];
     for (int i = 0; i < fc; ++i) {
       xc[i] = reinterpret_cast<const uint8_t*>(fx[i]) + b0 * fl[i]->d_in * xsz;
       yc[i] = reinterpret_cast<uint8_t*>(fy[i]) + b0 * fl[i]->rows_local * ysz;
     }
-    bitstack_status rs;
-    if (bc == 1) rs = launch_grouped_f8<1>(fl, fc, xc, xdt, xsz, yc, ydt, ysz, bc, st);
-    else if (bc == 2) rs = launch_grouped_f8<2>(fl, fc, xc, xdt, xsz, yc, ydt, ysz, bc, st);
-    else rs = launch_grouped_f8<4>(fl, fc, xc, xdt, xsz, yc, ydt, ysz, bc, st);
+    bitstack_status rs = dispatch_grouped_mx(bc, fl, fc, xc, xdt, xsz, yc, ydt, ysz, st);
     if (rs) return rs;
   }
   return BITSTACK_OK;

@@ -1,0 +1,510 @@
+// Block-scaled (MX) e4m3 decode: the production decode path for bf16 / fp16 factors.
+//
+// Computes y[b, j] = sum_i sum_r U'_i[j, r] (S_i (V'_i[:, r] (.) x_b / s))[j]   (Eq.4 P:111,
+// Eq.7-8; the factored form of W_hat_n x) with
+// tcgen05.mma.kind::mxf8f6f4.block_scale, A read from TMEM:
+//   * A = S_i as e4m3 +-1.0 (a pure function of the sign bits: LOP3 + IMAD per 4 signs,
+//     expand_e4m3 with the exponent fixed at 0), so the sign stream never waits for Z;
+//   * B = Z = V' (.) x/s as THREE e4m3 digits per (rank, token) column, each digit with its own
+//     UE8M0 scale per 32-channel K-block (the MX block scale).  Z ~= sum_d q_d 2^sigma_d, the
+//     scales are chosen per (K-block, column, digit) from that K-block's own maximum, so there is
+//     no shared exponent across units, tokens or channels: any finite x (tokens 2^12 apart,
+//     single outlier channels, ...) keeps ~12 significant bits per element
+//     (round 1's per-unit exponent / A = +-2^a scheme had a silent clamp).
+//   * scale_A = 1.0 for every row (constant UE8M0 127), scale_B from the Zq unit via tcgen05.cp.
+// The MX semantics on sm_100a (TS form, CUTLASS SF chunk layout through tcgen05.cp
+// 32x128b.warpx4) were pinned on a B200 before use: scripts/mx_probe.cu, max error 2.4e-7 of
+// sum |products| against an fp64 host reference over 4 K-blocks with random scales.
+//
+// Two kernels per call:
+//   zq_mx_kernel<NB>   one CTA per (block i, 128-channel subchunk q) unit: Z in fp32, then per
+//                      warp (= one 32-channel K-block) and column: redux.max -> sigma ->
+//                      e4m3 RNE digit -> exact residual -> next digit.  Writes the unit as a
+//                      ready-to-copy UMMA B image + its SFB chunks (MxCfg::kUnit bytes).
+//   decode_mx_kernel   warp-specialised, one CTA per SM: a producer thread streams sign tiles
+//                      (R row tiles x 128 rows x 16 B) and Zq units into a stage ring with the
+//                      bulk-copy (TMA) engine; 4R expander warps turn signs into e4m3 +-1 in a
+//                      TMEM A slot (one slot = the unit's R tiles, 32 columns each); one MMA
+//                      thread issues tcgen05.cp (SFB) + 4 R x (MMAs per 48 NB columns) per unit
+//                      (16 MMAs per hand-off at batch 1) into R fp32 TMEM accumulators; 4
+//                      epilogue warps drain the accumulators at each block end
+//                      (y += sum_r U'[j, r] sum_d T[j, (b, d, r)]) while the expanders keep
+//                      filling the other slot; split-K partials reduced deterministically by
+//                      the last CTA of each row group (decode_tc.cuh finalize_group).
+// Launch: zq_mx (PDL trigger at entry) then decode_mx with programmatic stream
+// serialization; only the producer's Zq copies wait (griddepcontrol.wait).
+#pragma once
+#include <cuda_fp8.h>
+
+#include "decode_tc.cuh"
+
+namespace bs {
+
+// ------------------------------------------------------------------ operand geometry
+// Column n of a Zq unit = b * 48 + d * 16 + r (token b, digit d, rank r).
+// B image: (n, k) at ((k / 16) (N / 8) + n / 8) 128 + (n % 8) 16 + k % 16 (K-major, no swizzle).
+// SFB chunk h (columns [128 h, 128 h + 128)): (n, kb) at 512 h + 16 (n % 32) + 4 ((n % 128) / 32) + kb.
+template <int NB>
+struct MxCfg {
+  static constexpr int N = 48 * NB;
+  static constexpr int NCH = (N + 127) / 128;
+  static constexpr int kB = kSubK * N;
+  static constexpr int kUnit = kB + 512 * NCH;
+  static constexpr uint32_t LBO = (N / 8) * 128;   // K-adjacent core matrices
+  static constexpr uint32_t SBO = 128;             // N-adjacent core matrices
+  // MMA split of the N columns: first 256, then the rest (each start a multiple of 128 so that
+  // its SFB chunks line up with the MMA's local columns)
+  static constexpr int NM = N > 256 ? 2 : 1;
+  static constexpr int N0 = N > 256 ? 256 : N;
+  static constexpr int N1 = N - N0;
+  static_assert(N0 % 16 == 0 && N1 % 16 == 0 && N1 <= 256, "MMA N");
+};
+
+// kind::mxf8f6f4 instruction descriptor: e4m3 x e4m3 -> f32, K-major, UE8M0 scales, M = 128,
+// scale-factor byte ids (the K-block inside the 4-byte TMEM scale cell).
+__host__ __device__ constexpr uint32_t idesc_mx(uint32_t N, uint32_t sf_id) {
+  return (sf_id << 4) | ((N >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24) | (sf_id << 29);
+}
+__device__ __forceinline__ void mma_mx_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t sfa,
+                                          uint32_t sfb, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], [%1], %2, %3, [%4], [%5], p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb), "r"(acc)
+      : "memory");
+}
+// 32 lanes x 16 B from shared memory, broadcast to the 4 lane quadrants of TMEM columns [c, c + 4).
+__device__ __forceinline__ void utccp_sf(uint32_t taddr, uint32_t saddr) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr),
+               "l"(smem_desc_kmajor(saddr, 128, 128))
+               : "memory");
+}
+
+// 16 consecutive factor entries (bf16 / f16 / f32 storage) as fp32.
+__device__ __forceinline__ void load_f16x(const void* base, int fdt, long long row, float (&f)[16]) {
+  if (fdt == 0) {
+    const float4* p = reinterpret_cast<const float4*>(base) + row * 4;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 v = __ldg(p + e);
+      f[4 * e] = v.x; f[4 * e + 1] = v.y; f[4 * e + 2] = v.z; f[4 * e + 3] = v.w;
+    }
+    return;
+  }
+  const uint4* p = reinterpret_cast<const uint4*>(base) + row * 2;
+  const uint4 a = __ldg(p), b = __ldg(p + 1);
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float2 v;
+    if (fdt == 1) v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+    else v = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
+    f[2 * e] = v.x;
+    f[2 * e + 1] = v.y;
+  }
+}
+
+// 32 device-layout sign bits (F8 layout, aux_kernels.cuh: bit p of word w = column 32 w + 4 (p & 7)
+// + (p >> 3)) -> 8 TMEM columns of e4m3 +-1.0 (byte = 0x38 | !bit << 7): per column one LOP3
+// (alu pipe) isolates bits t, t+8, t+16, t+24 (inverted) and one IMAD (fma pipe) moves them to
+// the byte sign bits and adds the exponent of 1.0.
+__device__ __forceinline__ void expand_pm1(uint32_t w, uint32_t* o /*8*/) {
+  const uint32_t e8 = 0x38383838u;
+#pragma unroll
+  for (int t = 0; t < 7; ++t) o[t] = mad_lo(lop3_andnot(w, 0x01010101u << t), 1u << (7 - t), e8);
+  o[7] = lop3_andnot_or(w, 0x80808080u, e8);
+}
+
+__device__ __forceinline__ float pow2f(int e) { return __uint_as_float((uint32_t)(e + 127) << 23); }  // |e| <= 126
+
+// ------------------------------------------------------------------ Zq (prologue, H3)
+struct ZqMxParams {
+  const void* v;        // [n_cap x kh][d_in_pad][16] V'
+  const float* inv_s;   // [d_in_pad]
+  const void* x;        // [batch][x_stride]
+  uint8_t* zq;          // [n x kh][nq] units of MxCfg<NB>::kUnit bytes
+  long long x_stride;
+  int nq, d_in, batch, x_dtype, f_dtype;
+  int kfuse;            // k > 16 at batch 1: token slot b = rank half b of block i (x row 0)
+};
+
+template <int NB>
+__device__ __forceinline__ void zq_mx_body(const ZqMxParams& p, const int unit) {
+  using C = MxCfg<NB>;
+  constexpr int N = C::N;
+  extern __shared__ __align__(128) uint8_t tile[];   // C::kUnit bytes (dynamic: > 48 KB at NB = 8)
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int i = unit / p.nq, q = unit % p.nq;
+  const int c = threadIdx.x, lane = c & 31, kb = c >> 5;
+  const int col = q * kSubK + c;
+  const long long dpad = (long long)p.nq * kSubK;
+  float vv[16];
+  if (!p.kfuse) load_f16x(p.v, p.f_dtype, (long long)i * dpad + col, vv);
+  const float is = col < p.d_in ? __ldg(p.inv_s + col) : 0.f;
+  const int kc = (c >> 4) * (N / 8) * 128 + (c & 15);   // this channel's byte offset in the B image
+#pragma unroll 1
+  for (int b = 0; b < NB; ++b) {
+    if (p.kfuse) load_f16x(p.v, p.f_dtype, (long long)(2 * i + b) * dpad + col, vv);
+    const bool on = p.kfuse || b < p.batch;
+    const long long xi = (long long)(p.kfuse ? 0 : b) * p.x_stride + col;
+    const float xs = (on && col < p.d_in) ? __fmul_rn(load_act(p.x, xi, p.x_dtype), is) : 0.f;
+#pragma unroll 4
+    for (int r = 0; r < 16; ++r) {
+      float val = __fmul_rn(vv[r], xs);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int n = b * 48 + d * 16 + r;
+        const uint32_t amax = __reduce_max_sync(0xffffffffu, __float_as_uint(val) & 0x7fffffffu);
+        uint8_t q8 = 0;
+        int sf = 0;                                    // UE8M0 byte (0 = 2^-127: an empty digit)
+        if (amax >= 0x7f800000u) {                     // inf / nan in this K-block: propagate
+          q8 = __nv_cvt_float_to_fp8(val, __NV_NOSAT, __NV_E4M3);
+          sf = 127;
+        } else if (amax >= 0x0a800000u) {              // max >= 2^-106: scale it into [128, 256)
+          const int sig = (int)(amax >> 23) - 127 - 7;  // in [-113, 120]
+          const float scaled = __fmul_rn(val, pow2f(-sig));
+          q8 = __nv_cvt_float_to_fp8(scaled, __NV_SATFINITE, __NV_E4M3);
+          const float back = __half2float(__half(__nv_cvt_fp8_to_halfraw(q8, __NV_E4M3)));
+          val = __fmul_rn(__fsub_rn(scaled, back), pow2f(sig));   // exact residual, absolute units
+          sf = sig + 127;
+        } else {                                       // below 2^-106: flushed (negligible)
+          val = 0.f;
+        }
+        tile[kc + (n / 8) * 128 + (n % 8) * 16] = q8;
+        if (lane == (n & 31)) tile[C::kB + 512 * (n / 128) + 16 * (n & 31) + 4 * ((n & 127) >> 5) + kb] = (uint8_t)sf;
+      }
+    }
+  }
+  // SFB bytes of columns >= N in the last chunk: defined (never used by an MMA)
+  for (int e = N + c; e < 128 * C::NCH; e += 128)
+    for (int k4 = 0; k4 < 4; ++k4) tile[C::kB + 512 * (e / 128) + 16 * (e & 31) + 4 * ((e & 127) >> 5) + k4] = 0;
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(p.zq + (long long)unit * C::kUnit);
+  for (int e = c; e < C::kUnit / 16; e += 128) dst[e] = reinterpret_cast<const uint4*>(tile)[e];
+}
+
+template <int NB>
+__global__ void __launch_bounds__(128) zq_mx_kernel(const ZqMxParams p) {
+  zq_mx_body<NB>(p, (int)blockIdx.x);
+}
+
+constexpr int kMaxMxGroup = 8;
+struct ZqMxGroup {
+  int count;
+  int unit_start[kMaxMxGroup + 1];
+  ZqMxParams prm[kMaxMxGroup];
+};
+template <int NB>
+__global__ void __launch_bounds__(128) zq_mx_grouped_kernel(const __grid_constant__ ZqMxGroup grp) {
+  int i = 0;
+  while (i + 1 < grp.count && (int)blockIdx.x >= grp.unit_start[i + 1]) ++i;
+  zq_mx_body<NB>(grp.prm[i], (int)blockIdx.x - grp.unit_start[i]);
+}
+
+// ------------------------------------------------------------------ decode kernel (H4-H7)
+template <int NB> struct MxGeom;                        // row tiles per CTA by batch class
+template <> struct MxGeom<1> { static constexpr int R = 4; };
+template <> struct MxGeom<2> { static constexpr int R = 3; };
+template <> struct MxGeom<3> { static constexpr int R = 2; };
+template <> struct MxGeom<4> { static constexpr int R = 1; };
+template <> struct MxGeom<5> { static constexpr int R = 1; };
+template <> struct MxGeom<6> { static constexpr int R = 1; };
+template <> struct MxGeom<7> { static constexpr int R = 1; };
+template <> struct MxGeom<8> { static constexpr int R = 1; };
+
+#ifndef BS_MX_SMEM_KB
+#define BS_MX_SMEM_KB 200
+#endif
+#ifndef BS_MX_STAGES
+#define BS_MX_STAGES 8
+#endif
+
+template <int NB>
+struct DecodeMxCfg {
+  using Z = MxCfg<NB>;
+  static constexpr int N = Z::N, R = MxGeom<NB>::R;
+  static constexpr int kWarpEpi = 4 * R;               // 4 epilogue warps (lane quadrants)
+  static constexpr int kWarpProd = 4 * R + 4;
+  static constexpr int kWarpMma = 4 * R + 5;
+  static constexpr int kThreads = 32 * (4 * R + 6);
+  static constexpr int kSignBytes = R * kTileRows * 16;
+  static constexpr int kStageBytes = (kSignBytes + Z::kUnit + 1023) / 1024 * 1024;
+  static constexpr int S0 = BS_MX_SMEM_KB * 1024 / kStageBytes;
+  static constexpr int STAGES = S0 > BS_MX_STAGES ? BS_MX_STAGES : (S0 < 2 ? 2 : S0);
+  static constexpr int kBarBytes = 1024;
+  static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes + 1024;   // + alignment slack
+  // TMEM columns: A slots | accumulators | SFA | SFB slots
+  static constexpr int kACols = R * 32;                // one slot = the unit's R sign tiles
+  static constexpr int kSfCols = 4 * Z::NCH;
+  static constexpr int NS0 = (512 - R * N - 4) / (kACols + kSfCols);
+  static constexpr int NSLOT = NS0 > 4 ? 4 : NS0;
+  static constexpr uint32_t kColAcc = NSLOT * kACols;
+  static constexpr uint32_t kColSfa = kColAcc + R * N;
+  static constexpr uint32_t kColSfb = kColSfa + 4;
+  static_assert(NSLOT >= 2, "need a double-buffered A slot");
+  static_assert(kColSfb + NSLOT * kSfCols <= 512, "TMEM overflow");
+  static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
+  static_assert(R * kTileRows * NB <= kPartStride, "split-K slot");
+};
+
+template <int NB>
+__device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int cta) {
+  using C = DecodeMxCfg<NB>;
+  using Z = MxCfg<NB>;
+  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
+  uint64_t* sfull = bars;                    // [STAGES] sign tiles landed (tx)
+  uint64_t* zfull = sfull + STAGES;          // [STAGES] Zq unit landed (tx)
+  uint64_t* sempty = zfull + STAGES;         // [STAGES] 4R expander warps + 1 MMA commit
+  uint64_t* afull = sempty + STAGES;         // [NSLOT] 4R expander warps
+  uint64_t* aempty = afull + NSLOT;          // [NSLOT] MMA commit
+  uint64_t* accfull = aempty + NSLOT;        // MMA commit at a block's last unit
+  uint64_t* accempty = accfull + 1;          // 4 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = cta / p.ctas_per_group;
+  const int jc = cta % p.ctas_per_group;
+  const long long L = (long long)p.n * p.nq;
+  const long long u0 = L * jc / p.ctas_per_group;
+  const int nunits = (int)(L * (jc + 1) / p.ctas_per_group - u0);
+  const int i_start = (int)(u0 / p.nq), q_start = (int)(u0 % p.nq);
+  const int tiles_left = p.row_tiles - g * R;
+  const int Rg = tiles_left < R ? tiles_left : R;
+  const int row0 = g * R * kTileRows;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&zfull[s], 1);
+      mbar_init(&sempty[s], 4 * Rg + 1);
+    }
+    for (int a = 0; a < NSLOT; ++a) {
+      mbar_init(&afull[a], 4 * Rg);
+      mbar_init(&aempty[a], 1);
+    }
+    mbar_init(accfull, 1);
+    mbar_init(accempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == C::kWarpMma) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  if (warp >= C::kWarpEpi && warp < C::kWarpEpi + 4) {
+    // scale_A = 1.0 (UE8M0 127) in every byte of the 4 SFA columns, lane quadrant warp % 4
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(
+                     tbase + ((uint32_t)((warp & 3) * 32) << 16) + C::kColSfa),
+                 "r"(0x7f7f7f7fu)
+                 : "memory");
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == C::kWarpProd) {
+    // ================= producer: sign tiles now, Zq units after the Zq grid completed
+    if (lane == 0) {
+      const uint64_t pol_sign = policy_evict_first();
+      const uint64_t pol_zq = policy_evict_last();
+      const uint32_t sign_bytes = (uint32_t)Rg * kTileRows * 16;
+      int q = q_start, iv = i_start;
+      const int pre = nunits < STAGES ? nunits : STAGES;
+      // sign tiles of the first `pre` units before the dependency wait
+      for (int k = 0; k < pre; ++k) {
+        mbar_arrive_expect_tx(&sfull[k], sign_bytes);
+        bulk_g2s(smem + k * C::kStageBytes, p.signs + ((long long)(iv >> p.ksh) * p.nq + q) * p.rows_pad + row0,
+                 sign_bytes, &sfull[k], pol_sign);
+        if (++q == p.nq) { q = 0; ++iv; }
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");   // this call's Zq units are complete
+      for (int k = 0; k < pre; ++k) {
+        mbar_arrive_expect_tx(&zfull[k], Z::kUnit);
+        bulk_g2s(smem + k * C::kStageBytes + C::kSignBytes, p.zq + (u0 + k) * Z::kUnit, Z::kUnit, &zfull[k], pol_zq);
+      }
+      int s = pre % STAGES;
+      uint32_t ph = pre == STAGES ? 1u : 0u;
+      for (int k = pre; k < nunits; ++k) {
+        mbar_wait(&sempty[s], ph ^ 1);
+        uint8_t* st = smem + s * C::kStageBytes;
+        mbar_arrive_expect_tx(&sfull[s], sign_bytes);
+        bulk_g2s(st, p.signs + ((long long)(iv >> p.ksh) * p.nq + q) * p.rows_pad + row0, sign_bytes, &sfull[s],
+                 pol_sign);
+        mbar_arrive_expect_tx(&zfull[s], Z::kUnit);
+        bulk_g2s(st + C::kSignBytes, p.zq + (u0 + k) * Z::kUnit, Z::kUnit, &zfull[s], pol_zq);
+        if (++q == p.nq) { q = 0; ++iv; }
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == C::kWarpMma) {
+    // ================= MMA issuer: one thread
+    if (lane == 0 && nunits > 0) {
+      const uint32_t sfa = tbase + C::kColSfa;
+      int s = 0, a = 0, q = q_start, seg = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int k = 0; k < nunits; ++k) {
+        const bool first = (k == 0) || (q == 0);
+        const bool last = (k + 1 == nunits) || (q + 1 == p.nq);
+        mbar_wait(&afull[a], aph);
+        mbar_wait(&zfull[s], ph);
+        if (first && seg > 0) mbar_wait(accempty, (seg - 1) & 1);
+        tc_fence_after();
+        const uint32_t zs = smem_u32(smem + s * C::kStageBytes + C::kSignBytes);
+        const uint32_t sfb = tbase + C::kColSfb + (uint32_t)(a * C::kSfCols);
+#pragma unroll
+        for (int h = 0; h < Z::NCH; ++h) utccp_sf(sfb + 4 * h, zs + Z::kB + 512 * h);
+        const uint64_t bdesc = smem_desc_kmajor(zs, Z::LBO, Z::SBO);
+        const uint32_t acol = tbase + (uint32_t)(a * C::kACols);
+        for (int t = 0; t < Rg; ++t) {
+          const uint32_t d = tbase + C::kColAcc + (uint32_t)(t * N);
+#pragma unroll
+          for (int kb = 0; kb < 4; ++kb) {
+            const uint32_t acc = (first && kb == 0) ? 0u : 1u;
+            const uint64_t bk = bdesc + (uint64_t)((kb * 2 * Z::LBO) >> 4);
+            mma_mx_ts(d, acol + (uint32_t)(t * 32 + kb * 8), bk, idesc_mx(Z::N0, kb), sfa | ((uint32_t)kb << 30),
+                      sfb | ((uint32_t)kb << 30), acc);
+            if constexpr (Z::NM == 2)
+              mma_mx_ts(d + Z::N0, acol + (uint32_t)(t * 32 + kb * 8), bk + (uint64_t)(((Z::N0 / 8) * 128) >> 4),
+                        idesc_mx(Z::N1, kb), sfa | ((uint32_t)kb << 30), (sfb + 8) | ((uint32_t)kb << 30), acc);
+          }
+        }
+        mma_commit(&aempty[a]);
+        mma_commit(&sempty[s]);
+        if (last) {
+          mma_commit(accfull);
+          ++seg;
+        }
+        if (++q == p.nq) q = 0;
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (++a == NSLOT) { a = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp < C::kWarpEpi) {
+    // ================= expanders: warp w -> tile w / 4, TMEM lane quadrant w % 4
+    const int t = warp >> 2, qd = warp & 3;
+    if (t < Rg) {
+      const uint32_t sw0 = smem_u32(smem) + (uint32_t)((t * kTileRows + qd * 32 + lane) * 16);
+      const uint32_t a0 = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(t * 32);
+      int s = 0, a = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int k = 0; k < nunits; ++k) {
+        mbar_wait(&sfull[s], ph);
+        uint4 w;
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                     : "r"(sw0 + (uint32_t)(s * C::kStageBytes)));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[s]);
+        if (k >= NSLOT) mbar_wait(&aempty[a], aph ^ 1);
+        tc_fence_after();
+        uint32_t o[32];
+        expand_pm1(w.x, o);
+        expand_pm1(w.y, o + 8);
+        expand_pm1(w.z, o + 16);
+        expand_pm1(w.w, o + 24);
+        tmem_st32(a0 + (uint32_t)(a * C::kACols), o);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[a]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (++a == NSLOT) { a = 0; aph ^= 1; }
+      }
+    }
+  } else {
+    // ================= epilogue warps: lane quadrant e, all R tiles
+    const int e = warp - C::kWarpEpi;   // == warp % 4
+    const uint32_t lq = (uint32_t)(e * 32) << 16;
+    float yacc[R][NB];
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) yacc[t][b] = 0.f;
+    int k = 0, q = q_start, i = i_start, seg = 0;
+    while (k < nunits) {
+      const int cnt = (nunits - k) < (p.nq - q) ? (nunits - k) : (p.nq - q);   // units of block i here
+      mbar_wait(accfull, seg & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        if (t < Rg) {
+          const long long row = row0 + t * kTileRows + e * 32 + lane;
+          float uu[16];
+          if (!p.kfuse) load_f16x(p.u, p.f_dtype, (long long)i * p.rows_pad + row, uu);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            if (p.kfuse) load_f16x(p.u, p.f_dtype, (long long)(2 * i + b) * p.rows_pad + row, uu);
+            uint32_t v0[16], v1[16], v2[16];
+            const uint32_t base = tbase + lq + C::kColAcc + (uint32_t)(t * N + b * 48);
+            tmem_ld16(base, v0);
+            tmem_ld16(base + 16, v1);
+            tmem_ld16(base + 32, v2);
+            tmem_ld_wait();
+            float acc = 0.f;
+#pragma unroll
+            for (int r = 0; r < 16; ++r)
+              acc = fmaf(uu[r], __uint_as_float(v0[r]) + __uint_as_float(v1[r]) + __uint_as_float(v2[r]), acc);
+            if (p.kfuse) yacc[t][0] += acc;
+            else yacc[t][b] += acc;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty);
+      ++seg;
+      k += cnt;
+      q += cnt;
+      if (q == p.nq) { q = 0; ++i; }
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      if (t < Rg)
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          if (b < p.batch) store_partial(p, cta, R * kTileRows, t * kTileRows + e * 32 + lane, b, yacc[t][b]);
+  }
+
+  // ---- teardown + last-CTA-of-group finalisation (deterministic split-K, H7)
+  __threadfence();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == C::kWarpMma) tmem_dealloc<512>(tbase);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(p.counters + g, 1);
+    *last_flag = (prev == p.ctas_per_group - 1);
+  }
+  __syncthreads();
+  if (*last_flag) {
+    __threadfence();
+    finalize_group(p, g, R * kTileRows, Rg, row0);
+    if (threadIdx.x == 0) p.counters[g] = 0;
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(DecodeMxCfg<NB>::kThreads, 1) decode_mx_kernel(const DecodeParams p) {
+  decode_mx_body<NB>(p, (int)blockIdx.x);
+}
+
+struct DecodeMxGroup {
+  int count;
+  int cta_start[kMaxMxGroup + 1];
+  DecodeParams prm[kMaxMxGroup];
+};
+template <int NB>
+__global__ void __launch_bounds__(DecodeMxCfg<NB>::kThreads, 1) decode_mx_grouped_kernel(
+    const __grid_constant__ DecodeMxGroup grp) {
+  int i = 0;
+  while (i + 1 < grp.count && (int)blockIdx.x >= grp.cta_start[i + 1]) ++i;
+  decode_mx_body<NB>(grp.prm[i], (int)blockIdx.x - grp.cta_start[i]);
+}
+
+}  // namespace bs

@@ -56,10 +56,9 @@ struct DecodeParams {
   uint32_t one2;                  // 0x3C003C00 (fp16x2 {1, 1}), see expand_f16
   float* dbg_acc;                 // test hook: raw accumulators of CTA 0's first drain (or null)
   uint32_t* dbg_z;                // test hook: CTA 0's first Z tile as stored in SMEM (or null)
-  const uint8_t* zq;              // e4m3 kernel: Zq units built by zq_kernel (else null)
-  int* status;                    // sticky numeric-range flag (e4m3 kernel), may be null
+  const uint8_t* zq;              // MX e4m3 kernel: Zq units built by zq_mx_kernel (else null)
   int ksh;                        // blocks are 16-rank halves: sign tile of block i is i >> ksh (k > 16: 1)
-  int kfuse;                      // e4m3 kernel, k > 16 at batch 1: NB = 2 columns are the two rank halves
+  int kfuse;                      // MX kernel, k > 16 at batch 1: NB = 2 column groups are the two rank halves
 };
 
 // Split-K reduction, shared by every decode kernel.  Each CTA stores the

@@ -531,8 +531,7 @@ def test_grouped_matches_individual_and_oracle(bs, batch):
     c0 = bs.launch_count()
     ys = bs.matmul_grouped(lays, xs)
     torch.cuda.synchronize()
-    if os.environ.get("BS_DECODE_WG") != "1":   # grouping is a property of the decode_f8i schedule
-        assert bs.launch_count() - c0 == 2 * ((batch + 3) // 4)   # zq_grouped + decode_f8i_grouped per 4 tokens
+    assert bs.launch_count() - c0 == 2 * ((batch + 7) // 8)   # zq_mx_grouped + decode_mx_grouped per 8 tokens
     for (g, s32, blocks, lay), n, x, y in zip(case, levels, xs, ys):
         y1 = lay.matmul(x)
         torch.cuda.synchronize()
@@ -583,7 +582,7 @@ def test_grouped_fallbacks(bs):
 @pytest.mark.parametrize("batch", [1, 3, 6])
 def test_grouped_level_zero_members(bs, batch):
     """Members at level 0 (budgets below one level; the Random / Greedy sortings) get y = 0 and
-    stay out of the fused launches; the others still run as ONE launch pair per <= 4 tokens."""
+    stay out of the fused launches; the others still run as ONE launch pair per <= 8 tokens."""
     case = _grouped_case(bs, [(512, 640, 3), (300, 200, 2), (1100, 264, 4), (128, 1000, 2)], 801)
     levels = [0, 2, 0, 1]
     for (_, _, _, lay), n in zip(case, levels):
@@ -596,8 +595,7 @@ def test_grouped_level_zero_members(bs, batch):
     c0 = bs.launch_count()
     grp(bs.BF16, bs.F32, batch, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    if os.environ.get("BS_DECODE_WG") != "1":
-        assert bs.launch_count() - c0 == 2 * ((batch + 3) // 4)
+    assert bs.launch_count() - c0 == 2 * ((batch + 7) // 8)
     for (g, s32, blocks, lay), n, x, y in zip(case, levels, xs, ys):
         if n == 0:
             assert torch.count_nonzero(y) == 0          # NaN prefill overwritten by zeros
