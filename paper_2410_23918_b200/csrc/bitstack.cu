@@ -462,6 +462,7 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
   prm.y_dtype = ydt;
   prm.f_dtype = L->dev_fdt;
   prm.one2 = 0x3C003C00u;
+  prm.one = 1u;
   prm.dbg_acc = g_dbg_acc;
   prm.dbg_z = g_dbg_z;
   prm.zq = nullptr;

@@ -108,10 +108,12 @@ __device__ __forceinline__ void load_f16x(const void* base, int fdt, long long r
 // + (p >> 3)) -> 8 TMEM columns of e4m3 +-1.0 (byte = 0x38 | !bit << 7): per column one LOP3
 // (alu pipe) isolates bits t, t+8, t+16, t+24 (inverted) and one IMAD (fma pipe) moves them to
 // the byte sign bits and adds the exponent of 1.0.
-__device__ __forceinline__ void expand_pm1(uint32_t w, uint32_t* o /*8*/) {
+// `one` = 1 arrives at run time (DecodeParams::one) so that ptxas keeps IMAD (fma pipe) instead
+// of turning a constant power-of-two multiply-add into LEA (alu pipe, shared with the LOP3s).
+__device__ __forceinline__ void expand_pm1(uint32_t w, uint32_t one, uint32_t* o /*8*/) {
   const uint32_t e8 = 0x38383838u;
 #pragma unroll
-  for (int t = 0; t < 7; ++t) o[t] = mad_lo(lop3_andnot(w, 0x01010101u << t), 1u << (7 - t), e8);
+  for (int t = 0; t < 7; ++t) o[t] = mad_lo(lop3_andnot(w, 0x01010101u << t), one << (7 - t), e8);
   o[7] = lop3_andnot_or(w, 0x80808080u, e8);
 }
 
@@ -148,30 +150,40 @@ __device__ __forceinline__ void zq_mx_body(const ZqMxParams& p, const int unit) 
     const bool on = p.kfuse || b < p.batch;
     const long long xi = (long long)(p.kfuse ? 0 : b) * p.x_stride + col;
     const float xs = (on && col < p.d_in) ? __fmul_rn(load_act(p.x, xi, p.x_dtype), is) : 0.f;
-#pragma unroll 4
-    for (int r = 0; r < 16; ++r) {
-      float val = __fmul_rn(vv[r], xs);
+    float val[16];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
+    for (int r = 0; r < 16; ++r) val[r] = __fmul_rn(vv[r], xs);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      // the 16 K-block maxima of this digit first (independent reductions, pipelined)
+      uint32_t amax[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) amax[r] = __reduce_max_sync(0xffffffffu, __float_as_uint(val[r]) & 0x7fffffffu);
+      int my_sf = 0;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
         const int n = b * 48 + d * 16 + r;
-        const uint32_t amax = __reduce_max_sync(0xffffffffu, __float_as_uint(val) & 0x7fffffffu);
         uint8_t q8 = 0;
         int sf = 0;                                    // UE8M0 byte (0 = 2^-127: an empty digit)
-        if (amax >= 0x7f800000u) {                     // inf / nan in this K-block: propagate
-          q8 = __nv_cvt_float_to_fp8(val, __NV_NOSAT, __NV_E4M3);
+        if (amax[r] >= 0x7f800000u) {                  // inf / nan in this K-block: propagate
+          q8 = __nv_cvt_float_to_fp8(val[r], __NV_NOSAT, __NV_E4M3);
           sf = 127;
-        } else if (amax >= 0x0a800000u) {              // max >= 2^-106: scale it into [128, 256)
-          const int sig = (int)(amax >> 23) - 127 - 7;  // in [-113, 120]
-          const float scaled = __fmul_rn(val, pow2f(-sig));
+        } else if (amax[r] >= 0x0a800000u) {           // max >= 2^-106: scale it into [128, 256)
+          const int sig = (int)(amax[r] >> 23) - 127 - 7;   // in [-113, 120]
+          const float scaled = __fmul_rn(val[r], pow2f(-sig));
           q8 = __nv_cvt_float_to_fp8(scaled, __NV_SATFINITE, __NV_E4M3);
           const float back = __half2float(__half(__nv_cvt_fp8_to_halfraw(q8, __NV_E4M3)));
-          val = __fmul_rn(__fsub_rn(scaled, back), pow2f(sig));   // exact residual, absolute units
+          val[r] = __fmul_rn(__fsub_rn(scaled, back), pow2f(sig));   // exact residual, absolute units
           sf = sig + 127;
         } else {                                       // below 2^-106: flushed (negligible)
-          val = 0.f;
+          val[r] = 0.f;
         }
         tile[kc + (n / 8) * 128 + (n % 8) * 16] = q8;
-        if (lane == (n & 31)) tile[C::kB + 512 * (n / 128) + 16 * (n & 31) + 4 * ((n & 127) >> 5) + kb] = (uint8_t)sf;
+        if (lane == r) my_sf = sf;
+      }
+      if (lane < 16) {   // lane r writes the scale byte of column (b, d, r) for this warp's K-block
+        const int n = b * 48 + d * 16 + lane;
+        tile[C::kB + 512 * (n / 128) + 16 * (n & 31) + 4 * ((n & 127) >> 5) + kb] = (uint8_t)my_sf;
       }
     }
   }
@@ -203,8 +215,11 @@ __global__ void __launch_bounds__(128) zq_mx_grouped_kernel(const __grid_constan
 
 // ------------------------------------------------------------------ decode kernel (H4-H7)
 template <int NB> struct MxGeom;                        // row tiles per CTA by batch class
-template <> struct MxGeom<1> { static constexpr int R = 4; };
-template <> struct MxGeom<2> { static constexpr int R = 3; };
+#ifndef BS_MX_R1
+#define BS_MX_R1 4
+#endif
+template <> struct MxGeom<1> { static constexpr int R = BS_MX_R1; };
+template <> struct MxGeom<2> { static constexpr int R = 2; };
 template <> struct MxGeom<3> { static constexpr int R = 2; };
 template <> struct MxGeom<4> { static constexpr int R = 1; };
 template <> struct MxGeom<5> { static constexpr int R = 1; };
@@ -219,30 +234,46 @@ template <> struct MxGeom<8> { static constexpr int R = 1; };
 #define BS_MX_STAGES 8
 #endif
 
+// Warp roles (R row tiles per CTA).  Synchronisation operations per unit are the cost that
+// bounds this kernel (scripts/sync_probe.cu, mbar_tput.cu: a completed-phase wait ~90 cycles of
+// latency, an arrive ~7 cycles of the SM's synchronisation unit), so few, fat warps hand off
+// large pieces of work:
+//   warps 0 .. 4NI-1   expanders: warp w owns TMEM lane quadrant w % 4 of the TPI tiles of
+//                      issuer group w / 4; per unit it expands its 32 rows of those tiles and
+//                      arrives once (two warps per SMSP keep the LOP3 -> IMAD chains busy)
+//   next NI warps      issuers: issuer i owns TPI consecutive tiles (their accumulators, A slots
+//                      and SFB copies); per unit one wait, one tcgen05.cp, 4 TPI MMAs, 2 commits
+//   next 4 warps       epilogue (lane quadrant warp % 4, all tiles)
+//   last warp          producer (bulk copies; allocates TMEM)
 template <int NB>
 struct DecodeMxCfg {
   using Z = MxCfg<NB>;
   static constexpr int N = Z::N, R = MxGeom<NB>::R;
-  static constexpr int kWarpEpi = 4 * R;               // 4 epilogue warps (lane quadrants)
-  static constexpr int kWarpProd = 4 * R + 4;
-  static constexpr int kWarpMma = 4 * R + 5;
-  static constexpr int kThreads = 32 * (4 * R + 6);
+#ifndef BS_MX_TPI
+#define BS_MX_TPI 1
+#endif
+  static constexpr int TPI = R >= BS_MX_TPI ? BS_MX_TPI : 1;   // tiles per issuer
+  static constexpr int NI = R / TPI;                   // issuers
+  static_assert(R % TPI == 0, "tiles per issuer");
+  static constexpr int kWarpIss = 4 * NI;
+  static constexpr int kWarpEpi = 5 * NI;
+  static constexpr int kWarpProd = 5 * NI + 4;
+  static constexpr int kThreads = 32 * (5 * NI + 5);
   static constexpr int kSignBytes = R * kTileRows * 16;
   static constexpr int kStageBytes = (kSignBytes + Z::kUnit + 1023) / 1024 * 1024;
   static constexpr int S0 = BS_MX_SMEM_KB * 1024 / kStageBytes;
   static constexpr int STAGES = S0 > BS_MX_STAGES ? BS_MX_STAGES : (S0 < 2 ? 2 : S0);
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes + 1024;   // + alignment slack
-  // TMEM columns: A slots | accumulators | SFA | SFB slots
-  static constexpr int kACols = R * 32;                // one slot = the unit's R sign tiles
+  // TMEM columns: A slots [slot][tile] (32 each) | accumulators [t] (N each) | SFA (4) | SFB [i][slot]
   static constexpr int kSfCols = 4 * Z::NCH;
-  static constexpr int NS0 = (512 - R * N - 4) / (kACols + kSfCols);
+  static constexpr int NS0 = (512 - R * N - 4) / (R * 32 + NI * kSfCols);
   static constexpr int NSLOT = NS0 > 4 ? 4 : NS0;
-  static constexpr uint32_t kColAcc = NSLOT * kACols;
+  static constexpr uint32_t kColAcc = NSLOT * R * 32;
   static constexpr uint32_t kColSfa = kColAcc + R * N;
   static constexpr uint32_t kColSfb = kColSfa + 4;
   static_assert(NSLOT >= 2, "need a double-buffered A slot");
-  static_assert(kColSfb + NSLOT * kSfCols <= 512, "TMEM overflow");
+  static_assert(kColSfb + NI * NSLOT * kSfCols <= 512, "TMEM overflow");
   static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
   static_assert(R * kTileRows * NB <= kPartStride, "split-K slot");
 };
@@ -251,18 +282,17 @@ template <int NB>
 __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int cta) {
   using C = DecodeMxCfg<NB>;
   using Z = MxCfg<NB>;
-  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT;
+  constexpr int N = C::N, R = C::R, STAGES = C::STAGES, NSLOT = C::NSLOT, TPI = C::TPI, NI = C::NI;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::kStageBytes);
-  uint64_t* sfull = bars;                    // [STAGES] sign tiles landed (tx)
-  uint64_t* zfull = sfull + STAGES;          // [STAGES] Zq unit landed (tx)
-  uint64_t* sempty = zfull + STAGES;         // [STAGES] 4R expander warps + 1 MMA commit
-  uint64_t* afull = sempty + STAGES;         // [NSLOT] 4R expander warps
-  uint64_t* aempty = afull + NSLOT;          // [NSLOT] MMA commit
-  uint64_t* accfull = aempty + NSLOT;        // MMA commit at a block's last unit
-  uint64_t* accempty = accfull + 1;          // 4 epilogue warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
+  uint64_t* full = bars;                     // [STAGES] sign tiles + Zq unit landed (tx)
+  uint64_t* sempty = full + STAGES;          // [STAGES] one commit per active issuer
+  uint64_t* aempty = sempty + STAGES;        // [NI][NSLOT] commit after the group's MMAs on the slot
+  uint64_t* afull = aempty + NI * NSLOT;     // [NI][NSLOT] the 4 expander warps stored the group's tiles
+  uint64_t* accfull = afull + NI * NSLOT;    // [R] commit at a block's last unit
+  uint64_t* accempty = accfull + R;          // [R] 4 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + R);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -274,23 +304,41 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
   const int i_start = (int)(u0 / p.nq), q_start = (int)(u0 % p.nq);
   const int tiles_left = p.row_tiles - g * R;
   const int Rg = tiles_left < R ? tiles_left : R;
+  const int NIg = (Rg + TPI - 1) / TPI;              // active issuers
   const int row0 = g * R * kTileRows;
+#ifdef BS_MX_TRACE   // timing build (scripts/mx_trace.py): per-unit clock64 stamps of CTA 0
+  long long* trace = (p.dbg_acc && cta == 0) ? reinterpret_cast<long long*>(p.dbg_acc) : nullptr;
+  __shared__ long long tstart_sh;
+  if (threadIdx.x == 0) tstart_sh = clock64();
+  __syncthreads();
+  const long long tstart = tstart_sh;
+#define BS_TR(k_, c_) do { if (trace && (k_) < 4000) trace[(k_) * 16 + (c_)] = clock64() - tstart; } while (0)
+  if (p.dbg_acc && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * cta] = (long long)gt;
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * cta + 2] = nunits;
+  }
+#else
+#define BS_TR(k_, c_) do { } while (0)
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&sfull[s], 1);
-      mbar_init(&zfull[s], 1);
-      mbar_init(&sempty[s], 4 * Rg + 1);
+      mbar_init(&full[s], 1);
+      mbar_init(&sempty[s], NIg);
     }
-    for (int a = 0; a < NSLOT; ++a) {
-      mbar_init(&afull[a], 4 * Rg);
+    for (int a = 0; a < NI * NSLOT; ++a) {
       mbar_init(&aempty[a], 1);
+      mbar_init(&afull[a], 4);
     }
-    mbar_init(accfull, 1);
-    mbar_init(accempty, 4);
+    for (int t = 0; t < R; ++t) {
+      mbar_init(&accfull[t], 1);
+      mbar_init(&accempty[t], 4);
+    }
     fence_mbar_init();
   }
-  if (warp == C::kWarpMma) tmem_alloc<512>(tmem_slot);
+  if (warp == C::kWarpProd) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -315,110 +363,161 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
       const uint32_t sign_bytes = (uint32_t)Rg * kTileRows * 16;
       int q = q_start, iv = i_start;
       const int pre = nunits < STAGES ? nunits : STAGES;
-      // sign tiles of the first `pre` units before the dependency wait
-      for (int k = 0; k < pre; ++k) {
-        mbar_arrive_expect_tx(&sfull[k], sign_bytes);
-        bulk_g2s(smem + k * C::kStageBytes, p.signs + ((long long)(iv >> p.ksh) * p.nq + q) * p.rows_pad + row0,
-                 sign_bytes, &sfull[k], pol_sign);
+#define SIGN_ADDR (p.signs + ((long long)(iv >> p.ksh) * p.nq + q) * p.rows_pad + row0)
+      for (int k = 0; k < pre; ++k) {   // sign tiles of the first units before the dependency wait
+        mbar_arrive_expect_tx(&full[k], sign_bytes + Z::kUnit);
+        bulk_g2s(smem + k * C::kStageBytes, SIGN_ADDR, sign_bytes, &full[k], pol_sign);
         if (++q == p.nq) { q = 0; ++iv; }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");   // this call's Zq units are complete
-      for (int k = 0; k < pre; ++k) {
-        mbar_arrive_expect_tx(&zfull[k], Z::kUnit);
-        bulk_g2s(smem + k * C::kStageBytes + C::kSignBytes, p.zq + (u0 + k) * Z::kUnit, Z::kUnit, &zfull[k], pol_zq);
-      }
+      for (int k = 0; k < pre; ++k)
+        bulk_g2s(smem + k * C::kStageBytes + C::kSignBytes, p.zq + (u0 + k) * Z::kUnit, Z::kUnit, &full[k], pol_zq);
       int s = pre % STAGES;
       uint32_t ph = pre == STAGES ? 1u : 0u;
       for (int k = pre; k < nunits; ++k) {
         mbar_wait(&sempty[s], ph ^ 1);
+        BS_TR(k, 0);
         uint8_t* st = smem + s * C::kStageBytes;
-        mbar_arrive_expect_tx(&sfull[s], sign_bytes);
-        bulk_g2s(st, p.signs + ((long long)(iv >> p.ksh) * p.nq + q) * p.rows_pad + row0, sign_bytes, &sfull[s],
-                 pol_sign);
-        mbar_arrive_expect_tx(&zfull[s], Z::kUnit);
-        bulk_g2s(st + C::kSignBytes, p.zq + (u0 + k) * Z::kUnit, Z::kUnit, &zfull[s], pol_zq);
+#if defined(BS_MX_EXP_NODATA)   // timing experiment: no copies after the first ring fill (wrong values)
+        mbar_arrive(&full[s]);
+#else
+        mbar_arrive_expect_tx(&full[s], sign_bytes + Z::kUnit);
+        bulk_g2s(st + C::kSignBytes, p.zq + (u0 + k) * Z::kUnit, Z::kUnit, &full[s], pol_zq);
+        bulk_g2s(st, SIGN_ADDR, sign_bytes, &full[s], pol_sign);
+#endif
         if (++q == p.nq) { q = 0; ++iv; }
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
+#undef SIGN_ADDR
     }
-  } else if (warp == C::kWarpMma) {
-    // ================= MMA issuer: one thread
-    if (lane == 0 && nunits > 0) {
-      const uint32_t sfa = tbase + C::kColSfa;
-      int s = 0, a = 0, q = q_start, seg = 0;
+  } else if (warp < C::kWarpIss) {
+    // ================= expander warp: TMEM lane quadrant qd of the tiles of issuer group gi
+    const int qd = warp & 3, gi = warp >> 2;
+    if (gi < NIg) {
+      const uint32_t sw0 = smem_u32(smem) + (uint32_t)((qd * 32 + lane) * 16);
+      const uint32_t one = p.one;
+      const uint32_t a0 = tbase + ((uint32_t)(qd * 32) << 16);
+      int s = 0, a = 0;
       uint32_t ph = 0, aph = 0;
       for (int k = 0; k < nunits; ++k) {
-        const bool first = (k == 0) || (q == 0);
-        const bool last = (k + 1 == nunits) || (q + 1 == p.nq);
-        mbar_wait(&afull[a], aph);
-        mbar_wait(&zfull[s], ph);
-        if (first && seg > 0) mbar_wait(accempty, (seg - 1) & 1);
-        tc_fence_after();
-        const uint32_t zs = smem_u32(smem + s * C::kStageBytes + C::kSignBytes);
-        const uint32_t sfb = tbase + C::kColSfb + (uint32_t)(a * C::kSfCols);
+        // the try_waits go out first so that their latency overlaps the loads and the expansion
+        const bool landed = mbar_try_wait(&full[s], ph);
+        const bool sfree = k < NSLOT || mbar_try_wait(&aempty[gi * NSLOT + a], aph ^ 1);
+        if (!landed) mbar_wait(&full[s], ph);
+        if (warp == 0 && lane == 0) BS_TR(k, 1);
+        const uint32_t sw = sw0 + (uint32_t)(s * C::kStageBytes);
+        uint4 w[TPI];
 #pragma unroll
-        for (int h = 0; h < Z::NCH; ++h) utccp_sf(sfb + 4 * h, zs + Z::kB + 512 * h);
-        const uint64_t bdesc = smem_desc_kmajor(zs, Z::LBO, Z::SBO);
-        const uint32_t acol = tbase + (uint32_t)(a * C::kACols);
-        for (int t = 0; t < Rg; ++t) {
-          const uint32_t d = tbase + C::kColAcc + (uint32_t)(t * N);
+        for (int tt = 0; tt < TPI; ++tt)
+          if (gi * TPI + tt < Rg)
+            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(w[tt].x), "=r"(w[tt].y), "=r"(w[tt].z), "=r"(w[tt].w)
+                         : "r"(sw + (uint32_t)((gi * TPI + tt) * kTileRows * 16)));
 #pragma unroll
-          for (int kb = 0; kb < 4; ++kb) {
-            const uint32_t acc = (first && kb == 0) ? 0u : 1u;
-            const uint64_t bk = bdesc + (uint64_t)((kb * 2 * Z::LBO) >> 4);
-            mma_mx_ts(d, acol + (uint32_t)(t * 32 + kb * 8), bk, idesc_mx(Z::N0, kb), sfa | ((uint32_t)kb << 30),
-                      sfb | ((uint32_t)kb << 30), acc);
-            if constexpr (Z::NM == 2)
-              mma_mx_ts(d + Z::N0, acol + (uint32_t)(t * 32 + kb * 8), bk + (uint64_t)(((Z::N0 / 8) * 128) >> 4),
-                        idesc_mx(Z::N1, kb), sfa | ((uint32_t)kb << 30), (sfb + 8) | ((uint32_t)kb << 30), acc);
+        for (int tt = 0; tt < TPI; ++tt) {
+          const int t = gi * TPI + tt;
+          if (t < Rg) {
+            uint32_t o[32];
+#ifndef BS_MX_EXP_NOEXP
+            expand_pm1(w[tt].x, one, o);
+            expand_pm1(w[tt].y, one, o + 8);
+            expand_pm1(w[tt].z, one, o + 16);
+            expand_pm1(w[tt].w, one, o + 24);
+#else
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o[j] = w[tt].x;
+#endif
+            if (tt == 0) {
+              if (!sfree) mbar_wait(&aempty[gi * NSLOT + a], aph ^ 1);
+              tc_fence_after();
+            }
+#ifndef BS_MX_EXP_NOST
+            tmem_st32(a0 + (uint32_t)((a * R + t) * 32), o);
+#else
+            if ((o[0] ^ o[31]) == 0x12345u) p.y_part[0] = 1.f;
+#endif
           }
         }
-        mma_commit(&aempty[a]);
-        mma_commit(&sempty[s]);
-        if (last) {
-          mma_commit(accfull);
-          ++seg;
-        }
-        if (++q == p.nq) q = 0;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[gi * NSLOT + a]);
+        if (warp == 0 && lane == 0) BS_TR(k, 3);
         if (++s == STAGES) { s = 0; ph ^= 1; }
         if (++a == NSLOT) { a = 0; aph ^= 1; }
       }
     }
   } else if (warp < C::kWarpEpi) {
-    // ================= expanders: warp w -> tile w / 4, TMEM lane quadrant w % 4
-    const int t = warp >> 2, qd = warp & 3;
-    if (t < Rg) {
-      const uint32_t sw0 = smem_u32(smem) + (uint32_t)((t * kTileRows + qd * 32 + lane) * 16);
-      const uint32_t a0 = tbase + ((uint32_t)(qd * 32) << 16) + (uint32_t)(t * 32);
-      int s = 0, a = 0;
-      uint32_t ph = 0, aph = 0;
+    // ================= issuer i: tiles [i TPI, (i+1) TPI); per unit one wait for the group's
+    // A slot, then tcgen05.cp (SFB) + 4 TPI MMAs from one elected lane and the commits that
+    // release the slot, the stage and (at a block end) the accumulators
+    const int i = warp - C::kWarpIss;
+    if (i < NIg) {
+      const uint32_t sfa = tbase + C::kColSfa;
+      int s = 0, a = 0, q = q_start, seg = 0;
+      uint32_t aph = 0;
       for (int k = 0; k < nunits; ++k) {
-        mbar_wait(&sfull[s], ph);
-        uint4 w;
-        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                     : "r"(sw0 + (uint32_t)(s * C::kStageBytes)));
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[s]);
-        if (k >= NSLOT) mbar_wait(&aempty[a], aph ^ 1);
+        const bool first = (k == 0) || (q == 0);
+        const bool last = (k + 1 == nunits) || (q + 1 == p.nq);
+        if (i == 0 && lane == 0) BS_TR(k, 8);
+        const bool ready = mbar_try_wait(&afull[i * NSLOT + a], aph);
+        if (first && seg > 0) {
+#pragma unroll
+          for (int tt = 0; tt < TPI; ++tt)
+            if (i * TPI + tt < Rg) mbar_wait(&accempty[i * TPI + tt], (seg - 1) & 1);
+        }
+        if (!ready) mbar_wait(&afull[i * NSLOT + a], aph);
+        if (i == 0 && lane == 0) BS_TR(k, 5);
         tc_fence_after();
-        uint32_t o[32];
-        expand_pm1(w.x, o);
-        expand_pm1(w.y, o + 8);
-        expand_pm1(w.z, o + 16);
-        expand_pm1(w.w, o + 24);
-        tmem_st32(a0 + (uint32_t)(a * C::kACols), o);
-        tmem_st_wait();
-        tc_fence_before();
+        if (elect_one()) {
+          const uint32_t zs = smem_u32(smem + s * C::kStageBytes + C::kSignBytes);
+          const uint32_t sfb = tbase + C::kColSfb + (uint32_t)((i * NSLOT + a) * C::kSfCols);
+#ifndef BS_MX_EXP_NOCP
+#pragma unroll
+          for (int h = 0; h < Z::NCH; ++h) utccp_sf(sfb + 4 * h, zs + Z::kB + 512 * h);
+#endif
+          const uint64_t bdesc = smem_desc_kmajor(zs, Z::LBO, Z::SBO);
+#pragma unroll
+          for (int tt = 0; tt < TPI; ++tt) {
+            const int t = i * TPI + tt;
+            if (t < Rg) {
+              const uint32_t dacc = tbase + C::kColAcc + (uint32_t)(t * N);
+              const uint32_t acol = tbase + (uint32_t)((a * R + t) * 32);
+#pragma unroll
+              for (int kb = 0; kb < 4; ++kb) {
+                const uint32_t acc = (first && kb == 0) ? 0u : 1u;
+                const uint64_t bk = bdesc + (uint64_t)((kb * 2 * Z::LBO) >> 4);
+#ifndef BS_MX_EXP_NOMMA
+                mma_mx_ts(dacc, acol + (uint32_t)(kb * 8), bk, idesc_mx(Z::N0, kb), sfa | ((uint32_t)kb << 30),
+                          sfb | ((uint32_t)kb << 30), acc);
+                if constexpr (Z::NM == 2)
+                  mma_mx_ts(dacc + Z::N0, acol + (uint32_t)(kb * 8), bk + (uint64_t)(((Z::N0 / 8) * 128) >> 4),
+                            idesc_mx(Z::N1, kb), sfa | ((uint32_t)kb << 30), (sfb + 8) | ((uint32_t)kb << 30), acc);
+#else
+                (void)acc; (void)bk; (void)dacc; (void)acol;
+#endif
+              }
+            }
+          }
+          mma_commit(&aempty[i * NSLOT + a]);
+          mma_commit(&sempty[s]);
+          if (last) {
+#pragma unroll
+            for (int tt = 0; tt < TPI; ++tt)
+              if (i * TPI + tt < Rg) mma_commit(&accfull[i * TPI + tt]);
+          }
+          if (i == 0) BS_TR(k, 7);
+        }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[a]);
-        if (++s == STAGES) { s = 0; ph ^= 1; }
+        if (last) ++seg;
+        if (++q == p.nq) q = 0;
+        if (++s == STAGES) s = 0;
         if (++a == NSLOT) { a = 0; aph ^= 1; }
       }
     }
-  } else {
+  } else if (warp < C::kWarpProd) {
     // ================= epilogue warps: lane quadrant e, all R tiles
-    const int e = warp - C::kWarpEpi;   // == warp % 4
+    const int e = warp & 3;
     const uint32_t lq = (uint32_t)(e * 32) << 16;
     float yacc[R][NB];
 #pragma unroll
@@ -428,14 +527,14 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
     int k = 0, q = q_start, i = i_start, seg = 0;
     while (k < nunits) {
       const int cnt = (nunits - k) < (p.nq - q) ? (nunits - k) : (p.nq - q);   // units of block i here
-      mbar_wait(accfull, seg & 1);
-      tc_fence_after();
 #pragma unroll
       for (int t = 0; t < R; ++t) {
         if (t < Rg) {
           const long long row = row0 + t * kTileRows + e * 32 + lane;
           float uu[16];
           if (!p.kfuse) load_f16x(p.u, p.f_dtype, (long long)i * p.rows_pad + row, uu);
+          mbar_wait(&accfull[t], seg & 1);
+          tc_fence_after();
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             if (p.kfuse) load_f16x(p.u, p.f_dtype, (long long)(2 * i + b) * p.rows_pad + row, uu);
@@ -452,11 +551,11 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
             if (p.kfuse) yacc[t][0] += acc;
             else yacc[t][b] += acc;
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&accempty[t]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(accempty);
       ++seg;
       k += cnt;
       q += cnt;
@@ -471,11 +570,19 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
   }
 
   // ---- teardown + last-CTA-of-group finalisation (deterministic split-K, H7)
+#ifdef BS_MX_TRACE
+  if (p.dbg_acc && threadIdx.x == 0) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    reinterpret_cast<long long*>(p.dbg_acc)[65536 + 4 * cta + 1] = (long long)gt;
+  }
+#endif
+#undef BS_TR
   __threadfence();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == C::kWarpMma) tmem_dealloc<512>(tbase);
+  if (warp == C::kWarpProd) tmem_dealloc<512>(tbase);
   if (threadIdx.x == 0) {
     __threadfence();
     const int prev = atomicAdd(p.counters + g, 1);

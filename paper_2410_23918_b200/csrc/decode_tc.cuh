@@ -54,6 +54,7 @@ struct DecodeParams {
   int batch;            // valid batch columns in this launch (<= NB)
   int x_dtype, y_dtype, f_dtype;  // 0 f32, 1 bf16, 2 f16 (f_dtype: 0 f32, 1 bf16)
   uint32_t one2;                  // 0x3C003C00 (fp16x2 {1, 1}), see expand_f16
+  uint32_t one;                   // 1 (MX kernel expansion multiplier base, see expand_pm1)
   float* dbg_acc;                 // test hook: raw accumulators of CTA 0's first drain (or null)
   uint32_t* dbg_z;                // test hook: CTA 0's first Z tile as stored in SMEM (or null)
   const uint8_t* zq;              // MX e4m3 kernel: Zq units built by zq_mx_kernel (else null)

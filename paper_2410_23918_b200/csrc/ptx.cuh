@@ -40,11 +40,28 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 #ifndef BS_WATCHDOG_SPINS
 #define BS_WATCHDOG_SPINS (1u << 26)
 #endif
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// The first try_wait is straight-line code: a phase that has already completed costs ~13
+// cycles this way, against ~122 through the loop (the compiler puts a YIELD in the loop body;
+// scripts/sync_probe.cu).  Most waits on the decode hot path find their phase complete.
+__device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (++spins > BS_WATCHDOG_SPINS) __trap();
   }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
+}
+// Warp-collective variants: ONE lane touches the barrier (an mbarrier operation issued by all 32
+// lanes costs the SM's shared synchronisation unit up to 32 requests), the result is broadcast.
+__device__ __forceinline__ bool mbar_try_wait_warp(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  if ((threadIdx.x & 31) == 0) ok = mbar_try_wait(bar, parity) ? 1u : 0u;
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
 }
 
 // ------------------------------------------------------------------ bulk copy (TMA, non-tensor)

@@ -1,0 +1,26 @@
+"""Build timing-experiment variants of libbitstack.so (wrong values, timing only) into
+scripts/variants/lib_<name>.so; scripts/run_variants.sh swaps each in and runs bench.py."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2410_23918_b200 import build as B  # noqa: E402
+
+VARIANTS = {
+    "base": [],
+    "r2": ["-DBS_MX_R1=2"],
+    "tpi2": ["-DBS_MX_TPI=2"],
+    "nomma": ["-DBS_MX_EXP_NOMMA"],
+    "noexp": ["-DBS_MX_EXP_NOEXP"],
+    "skel": ["-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
+    "skelnodata": ["-DBS_MX_EXP_NODATA", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
+    "nodata": ["-DBS_MX_EXP_NODATA"],
+}
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    os.makedirs(os.path.join(ROOT, "scripts", "variants"), exist_ok=True)
+    for n in names:
+        out = os.path.join(ROOT, "scripts", "variants", f"lib_{n}.so")
+        B.build(force=True, extra=VARIANTS[n], out=out)
+        print(out)
