@@ -46,6 +46,9 @@ struct bitstack_layer_s {
   uint8_t* zq = nullptr;   // e4m3 path: Zq units of the current call (grown on demand)
   int64_t zq_bytes = 0;
   int* counters = nullptr; // [row_tiles]
+  unsigned* xmax = nullptr; // fp16 paths: [batch] bits of max_c |x_bc / s_c| of the call (absmax_xs_kernel)
+  int64_t xmax_cap = 0;
+  int* pf_rowexp = nullptr; // prefill: W' row scale exponents [rows_pad]
   uint8_t* pf_w = nullptr; // prefill path: W' operand image (transient workspace, grown on demand)
   uint8_t* pf_x = nullptr; // prefill path: X' operand image
   int64_t pf_w_bytes = 0, pf_x_bytes = 0;
@@ -158,6 +161,26 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
 
 // e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
 constexpr int64_t kPrefillMinBatch = 16;   // AUTO: restored-tile GEMM path from this batch on
+
+// Per-token max_c |x_bc / s_c| of a call into L->xmax (the power-of-two operand scales of the
+// fp16 paths); the buffer grows with the largest batch seen.
+bitstack_status launch_absmax(bitstack_layer L, const void* x, int xdt, int64_t batch, cudaStream_t st) {
+  if (batch > L->xmax_cap) {
+    CK(cudaStreamSynchronize(st));
+    cudaFree(L->xmax);
+    L->xmax = nullptr;
+    const int64_t cap = std::max<int64_t>(batch, 64);
+    CK(cudaMalloc((void**)&L->xmax, (size_t)cap * 4));
+    L->bytes += (cap - L->xmax_cap) * 4;
+    L->xmax_cap = cap;
+  }
+  const int grid = (int)std::min<int64_t>(batch, (int64_t)L->sm_count * 8);
+  const bool vec = L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  bs::absmax_xs_kernel<<<grid, 256, 0, st>>>(x, xdt, L->d_in, L->inv_s, (int)batch, (int)L->d_in, L->xmax, vec);
+  count_launch();
+  CK(cudaGetLastError());
+  return BITSTACK_OK;
+}
 
 // ------------------------------------------------------------------ MX e4m3 decode (decode_mx.cuh)
 // Zq workspace for batch class NB: one unit per (block half, 128-column chunk) of the capacity.
@@ -347,8 +370,10 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   const long long pieces = (long long)nt * kc * BN * 8;
   const int xgrid = (int)std::min<long long>((pieces + 255) / 256, (long long)L->sm_count * 16);
   const bool xvec = L->d_in % 8 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  rs = launch_absmax(L, x, xdt, batch, L->pf_side);
+  if (rs) return rs;
   bs::xprep_kernel<<<xgrid, 256, 0, L->pf_side>>>(x, xdt, L->d_in, L->inv_s, (int)batch, (int)L->d_in, kc, BN,
-                                                  pieces, reinterpret_cast<uint4*>(L->pf_x), xvec);
+                                                  pieces, reinterpret_cast<uint4*>(L->pf_x), xvec, L->xmax);
   count_launch();
   CK(cudaGetLastError());
   CK(cudaEventRecord(L->pf_join, L->pf_side));
@@ -358,6 +383,7 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   wp.u = reinterpret_cast<const __nv_bfloat16*>(L->u);
   wp.v = reinterpret_cast<const __nv_bfloat16*>(L->v);
   wp.img = L->pf_w;
+  wp.rowexp = L->pf_rowexp;
   wp.n = L->n_act * L->kh;
   wp.ksh = L->kh == 2 ? 1 : 0;
   wp.nq = L->nq;
@@ -376,6 +402,8 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   gp.a_img = L->pf_w;
   gp.b_img = L->pf_x;
   gp.y = y;
+  gp.rowexp = L->pf_rowexp;
+  gp.xmax = L->xmax;
   gp.y_dtype = ydt;
   gp.y_stride = L->rows_local;
   gp.batch = (int)batch;
@@ -463,6 +491,7 @@ bs::DecodeParams decode_params(bitstack_layer L, const void* x, int xdt, int xsz
   prm.f_dtype = L->dev_fdt;
   prm.one2 = 0x3C003C00u;
   prm.one = 1u;
+  prm.xmax = L->xmax ? L->xmax + b0 : nullptr;
   prm.dbg_acc = g_dbg_acc;
   prm.dbg_z = g_dbg_z;
   prm.zq = nullptr;
@@ -655,6 +684,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * L->kh * 16 * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->y_part, (int64_t)std::max(2 * L->sm_count, L->row_tiles) * bs::kPartStride * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->pf_rowexp, (int64_t)L->rows_pad * 4);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     bitstack_destroy(L);
@@ -679,6 +709,8 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   if (L->pf_join) cudaEventDestroy(L->pf_join);
   cudaFree(L->y_part);
   cudaFree(L->counters);
+  cudaFree(L->xmax);
+  cudaFree(L->pf_rowexp);
   cudaFree(L->zq);
   cudaFree(L->pf_w);
   cudaFree(L->pf_x);
@@ -988,6 +1020,10 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
 
   const bool f8 = L->layout == 1;          // MX e4m3 kernel (bf16/f16 factors); fp16 kernel for fp32 factors
   const int nbmax = 8;
+  if (!f8) {   // fp16 digits: the call's x / s scale first
+    bitstack_status rs = launch_absmax(L, x, xdt, batch, st);
+    if (rs) return rs;
+  }
   for (int64_t b0 = 0; b0 < batch; b0 += nbmax) {
     const int bc = (int)std::min<int64_t>(nbmax, batch - b0);
     int slot = -1;

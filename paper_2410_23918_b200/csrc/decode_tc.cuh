@@ -55,12 +55,90 @@ struct DecodeParams {
   int x_dtype, y_dtype, f_dtype;  // 0 f32, 1 bf16, 2 f16 (f_dtype: 0 f32, 1 bf16)
   uint32_t one2;                  // 0x3C003C00 (fp16x2 {1, 1}), see expand_f16
   uint32_t one;                   // 1 (MX kernel expansion multiplier base, see expand_pm1)
+  const unsigned* xmax;           // fp16 decode: [batch] bits of max_c |x_bc / s_c| (absmax_xs_kernel)
   float* dbg_acc;                 // test hook: raw accumulators of CTA 0's first drain (or null)
   uint32_t* dbg_z;                // test hook: CTA 0's first Z tile as stored in SMEM (or null)
   const uint8_t* zq;              // MX e4m3 kernel: Zq units built by zq_mx_kernel (else null)
   int ksh;                        // blocks are 16-rank halves: sign tile of block i is i >> ksh (k > 16: 1)
   int kfuse;                      // MX kernel, k > 16 at batch 1: NB = 2 column groups are the two rank halves
 };
+
+// ------------------------------------------------------------------ operand range (fp16 paths)
+// fp16 operands have 11 significant bits but only the range 2^-24 .. 65504, so the fp16 decode
+// (fp32 factors) and the prefill GEMM scale x / s by a power of two 2^-e per call, with e
+// chosen from the call's max |x_bc / s_c| (absmax_xs_kernel); the epilogues multiply by 2^e.
+// Power-of-two scaling is exact, so the result does not depend on the scale of x or s.
+__device__ __forceinline__ float load_act(const void* p, long long idx, int dt);
+
+__global__ void __launch_bounds__(256) absmax_xs_kernel(const void* __restrict__ x, int x_dtype, long long x_stride,
+                                                        const float* __restrict__ inv_s, int batch, int d_in,
+                                                        unsigned* __restrict__ out, bool vec) {
+  // out[b] = bits of max_c |x_bc / s_c| (one CTA per token; NaN counts as inf).  vec: 16-byte
+  // aligned rows with d_in % 8 == 0 -> 8 channels per load, 4 loads in flight per thread.
+  __shared__ float red[8];
+  for (int b = blockIdx.x; b < batch; b += gridDim.x) {
+    float m = 0.f;
+    auto take = [&](float v) { v = fabsf(v); m = fmaxf(m, v != v ? __int_as_float(0x7f800000) : v); };
+    if (vec) {
+      const int groups = d_in / 8;
+      for (int g0 = threadIdx.x; g0 < groups; g0 += 4 * blockDim.x) {
+        float xv[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int g = g0 + u * blockDim.x;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) xv[u][t] = 0.f;
+          if (g < groups) {
+            const long long o = (long long)b * x_stride + g * 8;
+            if (x_dtype == 0) {
+              const float4 a = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + o));
+              const float4 c = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + o) + 1);
+              xv[u][0] = a.x; xv[u][1] = a.y; xv[u][2] = a.z; xv[u][3] = a.w;
+              xv[u][4] = c.x; xv[u][5] = c.y; xv[u][6] = c.z; xv[u][7] = c.w;
+            } else {
+              const uint4 a = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + o));
+              const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float2 f = x_dtype == 1 ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[t]))
+                                              : __half22float2(*reinterpret_cast<const __half2*>(&w[t]));
+                xv[u][2 * t] = f.x;
+                xv[u][2 * t + 1] = f.y;
+              }
+            }
+            const float4 s0 = __ldg(reinterpret_cast<const float4*>(inv_s + g * 8));
+            const float4 s1 = __ldg(reinterpret_cast<const float4*>(inv_s + g * 8) + 1);
+            xv[u][0] *= s0.x; xv[u][1] *= s0.y; xv[u][2] *= s0.z; xv[u][3] *= s0.w;
+            xv[u][4] *= s1.x; xv[u][5] *= s1.y; xv[u][6] *= s1.z; xv[u][7] *= s1.w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int t = 0; t < 8; ++t) take(xv[u][t]);
+      }
+    } else {
+      for (int c = threadIdx.x; c < d_in; c += blockDim.x) take(load_act(x, (long long)b * x_stride + c, x_dtype) * __ldg(inv_s + c));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+      out[b] = __float_as_uint(m);
+    }
+    __syncthreads();
+  }
+}
+
+// e such that max * 2^-e < 2^target (0 for an all-zero or non-finite x: those propagate as is).
+__device__ __forceinline__ int xs_exp(unsigned maxbits, int target) {
+  if (maxbits == 0u || maxbits >= 0x7f800000u) return 0;
+  const int e = (int)(maxbits >> 23) - 127 + 1 - target;   // subnormal max: (bits >> 23) = 0
+  return e < -100 ? -100 : (e > 100 ? 100 : e);
+}
+__device__ __forceinline__ float exp2i(int e) { return __uint_as_float((uint32_t)(e + 127) << 23); }   // |e| <= 126
 
 // Split-K reduction, shared by every decode kernel.  Each CTA stores the
 // partial y of its row group (R*128 rows x batch) into its own slot; the last CTA of the group
@@ -321,6 +399,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const Deco
   } else if (warp >= kWarpBuilder0) {
     // ================= Z builders: Z = V' (.) x' -> fp16 UMMA B tiles =================
     const int bt = threadIdx.x - 32 * kWarpBuilder0;  // 0..63
+    // x'_b = x_b / s scaled by 2^-e_b so that |Z| = |V' x'| < 2^15 (|V'| <= 2^8): fp16 digits in range
+    float xsc[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) xsc[b] = exp2i(-xs_exp(b < p.batch ? p.xmax[b] : 0u, 7));
     constexpr int kTasks = 16 * (N / 8);  // (k-group, n-group) core matrices
     int s = 0;
     uint32_t ph = 0;
@@ -342,7 +424,10 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const Deco
             if (p.x_dtype == 0) xv = reinterpret_cast<const float*>(xr)[b * kSubK + c];
             else if (p.x_dtype == 1) xv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(xr)[b * kSubK + c]);
             else xv = __half2float(reinterpret_cast<const __half*>(xr)[b * kSubK + c]);
-            xv *= isv[c];
+            float sb = xsc[0];
+#pragma unroll
+            for (int bb = 1; bb < NB; ++bb) sb = b == bb ? xsc[bb] : sb;
+            xv *= isv[c] * sb;
           }
           xsm[e] = xv;
         }
@@ -446,6 +531,9 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const Deco
     const int row_in_tile = qd * 32 + lane;
     const uint32_t lane_base = (uint32_t)(qd * 32) << 16;
     constexpr int kMyTiles = (R + 1) / 2;
+    float yunsc[NB];                                       // undo the x' scales (builders)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) yunsc[b] = exp2i(xs_exp(b < p.batch ? p.xmax[b] : 0u, 7));
     float yacc[kMyTiles][NB];
 #pragma unroll
     for (int a = 0; a < kMyTiles; ++a)
@@ -567,7 +655,8 @@ __global__ void __launch_bounds__(kDecodeThreads, 1) decode_tc_kernel(const Deco
       if (t < Rg) {
 #pragma unroll
         for (int b = 0; b < NB; ++b)
-          if (b < p.batch) store_partial(p, blockIdx.x, R * kTileRows, t * kTileRows + row_in_tile, b, yacc[a][b]);
+          if (b < p.batch)
+            store_partial(p, blockIdx.x, R * kTileRows, t * kTileRows + row_in_tile, b, yacc[a][b] * yunsc[b]);
       }
     }
   }

@@ -46,7 +46,9 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 // dense in image order.  Tokens >= batch and columns >= d_in are zero.
 __global__ void __launch_bounds__(256) xprep_kernel(const void* __restrict__ x, int x_dtype, long long x_stride,
                                                    const float* __restrict__ inv_s, int batch, int d_in,
-                                                   int kc, int bn, long long pieces, uint4* __restrict__ img, bool vec) {
+                                                   int kc, int bn, long long pieces, uint4* __restrict__ img, bool vec,
+                                                   const unsigned* __restrict__ xmax) {
+  // X'_t = x_t / s scaled by 2^-e_t per token (|X'| < 2^14: fp16 in range for any scale of x, s)
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < pieces;
        e += (long long)gridDim.x * blockDim.x) {
     const long long tile = e / (bn * 8);
@@ -87,6 +89,9 @@ __global__ void __launch_bounds__(256) xprep_kernel(const void* __restrict__ x, 
         v[t] = (tok < batch && col < d_in) ? load_act(x, (long long)tok * x_stride + col, x_dtype) * __ldg(inv_s + col) : 0.f;
       }
     }
+    const float xsc = tok < batch ? exp2i(-xs_exp(xmax[tok], 14)) : 0.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] *= xsc;
     img[e] = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
   }
 }
@@ -97,6 +102,7 @@ struct WtileParams {
   const __nv_bfloat16* u; // [n_cap][rows_pad][16] U'
   const __nv_bfloat16* v; // [n_cap][d_in_pad][16] V'
   uint8_t* img;           // [row_tiles_img][kc] tiles of kImgTileA bytes
+  int* rowexp;            // [rows_pad] W' row j is stored as W'[j,:] 2^-rowexp[j] (fp16 range)
   int n, nq, rows_pad, row_tiles, row_tiles_img, kc;
   int ksh;                // sign tile of block i is i >> ksh (16-rank halves of a k > 16 block)
 };
@@ -233,6 +239,27 @@ __global__ void __launch_bounds__(256, (2 * G * kPK <= 256) ? 2 : 1) wtile_kerne
     fence_proxy_async_smem();
     __syncthreads();                 // U' and V'(0) in SMEM (the previous segment's MMAs all waited)
     if (tid == 0) issue(vb0, sbase & 1, g_0);
+    // |W'[row, c]| <= 2^8 sum_i sum_r |U'_i[row, r]| (|V'| <= 2^8 after the load-time rebalancing):
+    // the row's fp16 image is W' 2^-re with that bound below 2^15
+    int re = 0;
+    {
+      float bound = 0.f;
+      for (int i = 0; i < p.n; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(su + i * C::kUBytes + ((j >> 3) * 2 + kk) * 128 + (j & 7) * 16);
+          const __nv_bfloat162* bp = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2) {
+            const float2 f = __bfloat1622float2(bp[e2]);
+            bound += fabsf(f.x) + fabsf(f.y);
+          }
+        }
+      bound *= 256.f;
+      if (bound > 0.f && bound < __int_as_float(0x7f800000)) re = xs_exp(__float_as_uint(bound), 15);
+      if (h == 0 && c0 == 0) p.rowexp[row] = re;
+    }
+    const float wsc = exp2i(-re);
     float acc[32];
 #pragma unroll
     for (int l = 0; l < 32; ++l) acc[l] = 0.f;
@@ -278,8 +305,10 @@ __global__ void __launch_bounds__(256, (2 * G * kPK <= 256) ? 2 : 1) wtile_kerne
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           *reinterpret_cast<uint4*>(dst + img_off(j, h * 32 + t * 8)) =
-              make_uint4(pack_half2(acc[8 * t + 0], acc[8 * t + 1]), pack_half2(acc[8 * t + 2], acc[8 * t + 3]),
-                         pack_half2(acc[8 * t + 4], acc[8 * t + 5]), pack_half2(acc[8 * t + 6], acc[8 * t + 7]));
+              make_uint4(pack_half2(acc[8 * t + 0] * wsc, acc[8 * t + 1] * wsc),
+                         pack_half2(acc[8 * t + 2] * wsc, acc[8 * t + 3] * wsc),
+                         pack_half2(acc[8 * t + 4] * wsc, acc[8 * t + 5] * wsc),
+                         pack_half2(acc[8 * t + 6] * wsc, acc[8 * t + 7] * wsc));
         }
 #pragma unroll
         for (int l = 0; l < 32; ++l) acc[l] = 0.f;
@@ -301,6 +330,8 @@ struct GemmParams {
   const uint8_t* a_img;   // W' image [row_tiles_img][kc] x 16 KB
   const uint8_t* b_img;   // X' image [nt_count][kc] x (BN x 128 B)
   void* y;                // [batch][y_stride]
+  const int* rowexp;      // [rows_pad] W' row scale exponents (wtile_kernel)
+  const unsigned* xmax;   // [batch] max_c |x_bc / s_c| (absmax_xs_kernel): the X' token scales
   int y_dtype;            // 0 f32, 1 bf16
   long long y_stride;
   int batch, rows_local, row_tiles, m2_count, nt_count, kc;   // m2_count: row-tile groups of MH
@@ -418,11 +449,17 @@ __global__ void __launch_bounds__(192, 1) prefill_gemm_kernel(const GemmParams p
       tc_fence_after();
       for (int hh = 0; hh < nh; ++hh) {
         const int j = (MH * mt + hh) * 128 + q * 32 + lane;
+        const float sc = j < p.rows_local ? exp2i(p.rowexp[j]) : 0.f;   // undo the W' row scale
         for (int cc = 0; cc < BN / 32; ++cc) {
           uint32_t v[32];
           tmem_ld32(tbase + lane_base + (uint32_t)(ab * MH * BN + hh * BN + cc * 32), v);
           tmem_ld_wait();
           const int b0 = nt * BN + cc * 32;
+          // and the X' token scales: lane l fetches token b0 + l's, the loop broadcasts them
+          const float tf = exp2i(xs_exp(b0 + lane < p.batch ? __ldg(p.xmax + b0 + lane) : 0u, 14));
+#pragma unroll
+          for (int l = 0; l < 32; ++l)
+            v[l] = __float_as_uint(__uint_as_float(v[l]) * (sc * __shfl_sync(0xffffffffu, tf, l)));
           if (j < p.rows_local) {
             if (p.y_dtype == 0) {
               float* yp = reinterpret_cast<float*>(p.y) + (long long)b0 * p.y_stride + j;
