@@ -20,8 +20,12 @@
  *   - no exception or abort crosses the ABI.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *   - the library owns the device block store; the caller owns x, y, w.
- *   - a handle is not safe for concurrent mutation; matmul calls on different
- *     streams may overlap if no load/set call runs in between.
+ *   - calls on one handle never overlap: each handle reuses its workspaces (Zq
+ *     units, split-K slots, staging), so a call arriving on a different stream
+ *     than the handle's previous call first makes its stream wait for everything
+ *     already submitted to the previous one (an event; no host blocking).  Under
+ *     CUDA-graph capture that ordering is the caller's (capture one stream per
+ *     handle).  Handles are not safe for concurrent mutation from host threads.
  *   - a CUDA fault inside an asynchronous kernel surfaces at a later call (or
  *     cudaStreamSynchronize) as BITSTACK_E_CUDA.
  */
@@ -154,9 +158,17 @@ BITSTACK_API bitstack_status bitstack_set_num_blocks(bitstack_layer layer, int32
  * the first call that needs them (which therefore must not be under CUDA-graph capture).
  * x and y must not alias.  batch == 0 is a no-op; n == 0 writes y = 0.
  * Asynchronous on `stream`; argument errors are reported synchronously.
- * Numerics: factors and the activation product V (.) (x/s) are
- * rounded once to fp16 (one digit for BF16/F16 factors, two digits for F32
- * factors) on the tensor-core path, accumulation in fp32.
+ * Numerics, tensor-core paths, accumulation in fp32 throughout:
+ *   - BF16/F16 factors, decode (batch < 16): S as exact e4m3 +-1, the product
+ *     Z = V (.) (x/s) as three e4m3 digits per (rank, token), each digit with its
+ *     own power-of-two scale per 32-channel block (MX block scaling): ~12
+ *     significant bits per element whatever the range of x, s or the batch.
+ *   - F32 factors: Z as two fp16 digits after a per-token power-of-two scale of
+ *     x/s (~22 bits).
+ *   - BF16/F16 factors, batch >= 16 (prefill): the restored tile W' = W diag(s)
+ *     and x/s as fp16 GEMM operands, each with power-of-two scales (per row of W',
+ *     per token of x/s) so that neither overflows nor underflows.
+ *   Every scale is exact; non-finite x propagates to y.
  * Errors: E_INVALID_ARG, E_UNSUPPORTED (forced TC kernel not possible), E_CUDA. */
 BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x, bitstack_dtype x_dtype,
                                 void* y, bitstack_dtype y_dtype, int64_t batch, void* stream);
@@ -167,9 +179,9 @@ BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x
  * Each member keeps its own level n_i, dtypes of x / y are shared, xs[i] / ys[i] follow
  * bitstack_matmul's layouts (xs[i] may be the same buffer for several members).
  * When count <= 8, 1 <= batch < 16, the members are distinct handles on one device on the
- * e4m3 decode path (bf16/f16 factors, d_in % 8 == 0, AUTO or TC kernel) and all xs / ys are
+ * MX e4m3 decode path (bf16/f16 factors, d_in % 8 == 0, AUTO or TC kernel) and all xs / ys are
  * 16-byte aligned device buffers, the whole group runs as ONE Zq launch and ONE decode launch
- * per chunk of <= 4 tokens, whose CTAs are shared out among the members in proportion to their
+ * per chunk of <= 8 tokens, whose CTAs are shared out among the members in proportion to their
  * work; members at level n_i == 0 get ys[i] = 0 (a memset) and no share of the launches (no
  * launch at all when every member is at level 0); otherwise the members run one after another through
  * bitstack_matmul (from 16 tokens that is the prefill path of each member).  Results are

@@ -114,59 +114,6 @@ __device__ __forceinline__ float ld_factor(const void* p, long long idx, int dt)
   return __half2float(reinterpret_cast<const __half*>(p)[idx]);
 }
 
-// One CTA per block. Input u:[d_out][k], v:[d_in][k] in the user's dtype (staging);
-// output U' [rows_pad][16], V' [d_in_pad][16] in the device dtype (0 f32, 1 bf16),
-// columns r >= k and pad rows zero.  e_r = floor(log2(256 / max_c |V[c, r]|)).
-__global__ void prep_factors_kernel(const void* __restrict__ u_in, const void* __restrict__ v_in,
-                                    int in_dt, int k, long long d_out, long long d_in,
-                                    long long row_begin, long long rows_local, int rows_pad,
-                                    long long d_in_pad, void* u_out, void* v_out, int out_dt,
-                                    float* zscale_out) {
-  const int blk = blockIdx.x;
-  __shared__ float red[16][32];
-  __shared__ float scale[16];
-  const int tid = threadIdx.x;
-  const long long ub = (long long)blk * d_out * k, vb = (long long)blk * d_in * k;
-  // per-r max |V|
-  for (int r = 0; r < 16; ++r) {
-    float m = 0.f;
-    if (r < k)
-      for (long long c = tid; c < d_in; c += blockDim.x) m = fmaxf(m, fabsf(ld_factor(v_in, vb + c * k + r, in_dt)));
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((tid & 31) == 0) red[r][tid >> 5] = m;
-  }
-  __syncthreads();
-  if (tid < 16) {
-    float m = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[tid][w]);
-    int e = 0;
-    if (m > 0.f && isfinite(m)) {
-      e = (int)floorf(log2f(256.0f / m));
-      e = e > 60 ? 60 : (e < -60 ? -60 : e);
-    }
-    scale[tid] = ldexpf(1.0f, e);
-    if (zscale_out) zscale_out[blk * 16 + tid] = scale[tid];
-  }
-  __syncthreads();
-  const long long ou = (long long)blk * rows_pad * 16, ov = (long long)blk * d_in_pad * 16;
-  for (long long e = tid; e < (long long)rows_pad * 16; e += blockDim.x) {
-    const long long j = e / 16;
-    const int r = (int)(e % 16);
-    float val = 0.f;
-    if (j < rows_local && r < k) val = ld_factor(u_in, ub + (row_begin + j) * k + r, in_dt) / scale[r];
-    if (out_dt == 0) reinterpret_cast<float*>(u_out)[ou + e] = val;
-    else reinterpret_cast<__nv_bfloat16*>(u_out)[ou + e] = __float2bfloat16_rn(val);
-  }
-  for (long long e = tid; e < d_in_pad * 16; e += blockDim.x) {
-    const long long c = e / 16;
-    const int r = (int)(e % 16);
-    float val = 0.f;
-    if (c < d_in && r < k) val = ld_factor(v_in, vb + c * k + r, in_dt) * scale[r];
-    if (out_dt == 0) reinterpret_cast<float*>(v_out)[ov + e] = val;
-    else reinterpret_cast<__nv_bfloat16*>(v_out)[ov + e] = __float2bfloat16_rn(val);
-  }
-}
-
 // Parallel form of prep_factors_kernel for one block (the block loads): factor_max_kernel
 // reduces max_c |V[c, r]| into vmax[16] (float bits as uint: |v| >= 0 orders like its bits;
 // vmax zeroed before), factor_scale_kernel derives the same power-of-two e_r and writes
@@ -205,14 +152,21 @@ __device__ __forceinline__ float factor_scale(const unsigned int* vmax, int r) {
   return ldexpf(1.0f, e);
 }
 
+// U' = U / 2^e_r, V' = V 2^e_r (exact power-of-two rebalancing, U'V'^T == UV^T) into the device
+// dtype out_dt (0 f32, 1 bf16, 2 f16).  fp16 storage is NOT rebalanced (e_r = 0): fp16's range is
+// too small for U / 2^e_r, and the stored fp16 values are kept bit for bit (Eq.9's 16-bit
+// factors); the MX decode's per-K-block scales do not need max |V'| near 2^8.
+// vmaxr_out[r] = max_c |V'[c, r]| (the prefill restore's per-row fp16 range bound).
 __global__ void factor_scale_kernel(const void* __restrict__ u_in, const void* __restrict__ v_in, int in_dt, int ld,
                                     int col0, int k, long long rows_local, int rows_pad, long long d_in, long long d_in_pad,
                                     const unsigned int* __restrict__ vmax, void* u_out, void* v_out, int out_dt,
-                                    float* zscale_out) {
+                                    float* zscale_out, float* vmaxr_out) {
   __shared__ float scale[16];
-  if (threadIdx.x < 16) scale[threadIdx.x] = factor_scale(vmax, threadIdx.x);
+  if (threadIdx.x < 16) scale[threadIdx.x] = out_dt == 2 ? 1.f : factor_scale(vmax, threadIdx.x);
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x < 16 && zscale_out) zscale_out[threadIdx.x] = scale[threadIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x < 16 && vmaxr_out)
+    vmaxr_out[threadIdx.x] = __uint_as_float(vmax[threadIdx.x]) * scale[threadIdx.x];
   const long long nu = (long long)rows_pad * 16, nv = d_in_pad * 16;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nu + nv;
        e += (long long)gridDim.x * blockDim.x) {
@@ -222,14 +176,16 @@ __global__ void factor_scale_kernel(const void* __restrict__ u_in, const void* _
       const int r = (int)(e % 16);
       if (j < rows_local && r < k) val = ld_factor(u_in, j * ld + col0 + r, in_dt) / scale[r];
       if (out_dt == 0) reinterpret_cast<float*>(u_out)[e] = val;
-      else reinterpret_cast<__nv_bfloat16*>(u_out)[e] = __float2bfloat16_rn(val);
+      else if (out_dt == 1) reinterpret_cast<__nv_bfloat16*>(u_out)[e] = __float2bfloat16_rn(val);
+      else reinterpret_cast<__half*>(u_out)[e] = __float2half_rn(val);
     } else {
       const long long ev = e - nu;
       const long long c = ev / 16;
       const int r = (int)(ev % 16);
       if (c < d_in && r < k) val = ld_factor(v_in, c * ld + col0 + r, in_dt) * scale[r];
       if (out_dt == 0) reinterpret_cast<float*>(v_out)[ev] = val;
-      else reinterpret_cast<__nv_bfloat16*>(v_out)[ev] = __float2bfloat16_rn(val);
+      else if (out_dt == 1) reinterpret_cast<__nv_bfloat16*>(v_out)[ev] = __float2bfloat16_rn(val);
+      else reinterpret_cast<__half*>(v_out)[ev] = __float2half_rn(val);
     }
   }
 }
@@ -241,9 +197,10 @@ __global__ void inv_s_kernel(const float* __restrict__ s, float* __restrict__ in
     inv_s[c] = c < d_in ? 1.0f / s[c] : 0.0f;
 }
 
-__device__ __forceinline__ float ld_dev_factor(const void* p, long long idx, int dt) {
-  return dt == 0 ? reinterpret_cast<const float*>(p)[idx]
-                 : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
+__device__ __forceinline__ float ld_dev_factor(const void* p, long long idx, int dt) {   // 0 f32, 1 bf16, 2 f16
+  if (dt == 0) return reinterpret_cast<const float*>(p)[idx];
+  if (dt == 1) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[idx]);
+  return __half2float(reinterpret_cast<const __half*>(p)[idx]);
 }
 __device__ __forceinline__ float ld_act(const void* p, long long idx, int dt) {
   if (dt == 0) return reinterpret_cast<const float*>(p)[idx];

@@ -32,7 +32,7 @@ struct bitstack_layer_s {
   cudaStream_t pf_side = nullptr;              // prefill: xprep runs here, concurrent with wtile
   cudaEvent_t pf_fork = nullptr, pf_join = nullptr;
   bitstack_dtype fdt = BITSTACK_BF16;
-  int dev_fdt = 1;  // device factor storage: 0 f32, 1 bf16
+  int dev_fdt = 1;  // device factor storage: 0 f32, 1 bf16, 2 f16 (the user's 16-bit dtype, kept as is)
   int layout = 1;   // device sign layout: 0 = F16 (fp32 factors, fp16 MMA), 1 = F8 (e4m3 MMA)
   int device = 0;
   int sm_count = 148;
@@ -42,6 +42,7 @@ struct bitstack_layer_s {
   void* v = nullptr;
   float* inv_s = nullptr;
   float* zscale = nullptr;
+  float* vmaxr = nullptr;  // [n_cap x kh][16] max_c |V'[c, r]| (prefill W' range bound)
   float* y_part = nullptr; // [max(2 sm_count, row_tiles)][kPartStride] split-K partial slots (<= 2 CTAs/SM)
   uint8_t* zq = nullptr;   // e4m3 path: Zq units of the current call (grown on demand)
   int64_t zq_bytes = 0;
@@ -57,6 +58,9 @@ struct bitstack_layer_s {
   int64_t stage_x_bytes = 0, stage_y_bytes = 0;
   int64_t bytes = 0;
   int64_t block_bytes = 0;
+  cudaStream_t last_stream = nullptr;   // stream of the previous call (order_after_last)
+  bool has_last = false;
+  cudaEvent_t order_ev = nullptr;
 };
 
 namespace {
@@ -162,6 +166,34 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
 // e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
 constexpr int64_t kPrefillMinBatch = 16;   // AUTO: restored-tile GEMM path from this batch on
 
+// AUTO takes the restored-tile GEMM (fp16 operands, ~3e-4 relative error) from kPrefillMinBatch
+// tokens on, for shards of at least one full 128-row tile; tiny shards stay on the decode path
+// (one tile of GEMM work is not worth the restore, and y over a handful of rows is where the fp16
+// operand rounding shows most).
+bool prefill_auto(bitstack_layer L, int64_t batch) { return batch >= kPrefillMinBatch && L->rows_local >= 128; }
+
+// A handle's workspaces (Zq units, split-K slots and counters, staging, prefill images) are
+// reused by every call.  Calls on one stream are ordered by the stream; when a call arrives on a
+// different stream than the handle's previous call, the new stream first waits for everything
+// submitted to the old one (an event recorded now on the old stream), so calls on one handle never
+// overlap.  Under CUDA-graph capture the capture order is the caller's to keep (an event recorded
+// outside a capture cannot be waited on inside it).
+bitstack_status order_after_last(bitstack_layer L, cudaStream_t st) {
+  if (L->has_last && L->last_stream != st) {
+    cudaStreamCaptureStatus a = cudaStreamCaptureStatusNone, b = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(st, &a));
+    CK(cudaStreamIsCapturing(L->last_stream, &b));
+    if (a == cudaStreamCaptureStatusNone && b == cudaStreamCaptureStatusNone) {
+      if (!L->order_ev) CK(cudaEventCreateWithFlags(&L->order_ev, cudaEventDisableTiming));
+      CK(cudaEventRecord(L->order_ev, L->last_stream));
+      CK(cudaStreamWaitEvent(st, L->order_ev, 0));
+    }
+  }
+  L->last_stream = st;
+  L->has_last = true;
+  return BITSTACK_OK;
+}
+
 // Per-token max_c |x_bc / s_c| of a call into L->xmax (the power-of-two operand scales of the
 // fp16 paths); the buffer grows with the largest batch seen.
 bitstack_status launch_absmax(bitstack_layer L, const void* x, int xdt, int64_t batch, cudaStream_t st) {
@@ -250,7 +282,7 @@ bitstack_status launch_decode_mx(bitstack_layer L, const bs::DecodeParams& prm_i
   rs = ensure_zq_mx<NB>(L, st);
   if (rs) return rs;
   const int64_t units = (int64_t)prm_in.n * prm_in.nq;
-  bs::zq_mx_kernel<NB><<<(unsigned)units, 128, bs::MxCfg<NB>::kUnit, st>>>(zq_mx_params(L, prm_in));
+  bs::zq_mx_kernel<NB><<<(unsigned)units, bs::kZqThreads, bs::MxCfg<NB>::kUnit, st>>>(zq_mx_params(L, prm_in));
   count_launch();
   CK(cudaGetLastError());
   bs::DecodeParams prm = prm_in;
@@ -380,8 +412,10 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
 
   bs::WtileParams wp;
   wp.signs = L->signs;
-  wp.u = reinterpret_cast<const __nv_bfloat16*>(L->u);
-  wp.v = reinterpret_cast<const __nv_bfloat16*>(L->v);
+  wp.u = reinterpret_cast<const uint16_t*>(L->u);
+  wp.v = reinterpret_cast<const uint16_t*>(L->v);
+  wp.vmaxr = L->vmaxr;
+  wp.f16 = L->dev_fdt == 2 ? 1 : 0;
   wp.img = L->pf_w;
   wp.rowexp = L->pf_rowexp;
   wp.n = L->n_act * L->kh;
@@ -554,7 +588,7 @@ bitstack_status launch_grouped_mx(const bitstack_layer* layers, int count, const
   int slot = -1;
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
-  bs::zq_mx_grouped_kernel<NB><<<(unsigned)zg.unit_start[count], 128, bs::MxCfg<NB>::kUnit, st>>>(zg);
+  bs::zq_mx_grouped_kernel<NB><<<(unsigned)zg.unit_start[count], bs::kZqThreads, bs::MxCfg<NB>::kUnit, st>>>(zg);
   count_launch();
   CK(cudaGetLastError());
   cudaLaunchAttribute attr[1];
@@ -658,7 +692,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   L->kh = k > 16 ? 2 : 1;
   L->n_cap = n_capacity;
   L->fdt = factor_dtype;
-  L->dev_fdt = factor_dtype == BITSTACK_BF16 ? 1 : 0;
+  L->dev_fdt = factor_dtype == BITSTACK_BF16 ? 1 : (factor_dtype == BITSTACK_F16 ? 2 : 0);
   L->layout = factor_dtype == BITSTACK_F32 ? 0 : 1;
   L->device = device;
   L->sm_count = prop.multiProcessorCount;
@@ -682,6 +716,7 @@ bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t 
   if (e == cudaSuccess) e = alloc(&L->v, v_bytes * n_capacity * L->kh);
   if (e == cudaSuccess) e = alloc((void**)&L->inv_s, L->d_in_pad * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->zscale, (int64_t)n_capacity * L->kh * 16 * 4);
+  if (e == cudaSuccess) e = alloc((void**)&L->vmaxr, (int64_t)n_capacity * L->kh * 16 * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->y_part, (int64_t)std::max(2 * L->sm_count, L->row_tiles) * bs::kPartStride * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->counters, (int64_t)L->row_tiles * 4);
   if (e == cudaSuccess) e = alloc((void**)&L->pf_rowexp, (int64_t)L->rows_pad * 4);
@@ -704,9 +739,11 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   cudaFree(L->v);
   cudaFree(L->inv_s);
   cudaFree(L->zscale);
+  cudaFree(L->vmaxr);
   if (L->pf_side) cudaStreamDestroy(L->pf_side);
   if (L->pf_fork) cudaEventDestroy(L->pf_fork);
   if (L->pf_join) cudaEventDestroy(L->pf_join);
+  if (L->order_ev) cudaEventDestroy(L->order_ev);
   cudaFree(L->y_part);
   cudaFree(L->counters);
   cudaFree(L->xmax);
@@ -755,8 +792,11 @@ bitstack_status bitstack_set_num_blocks(bitstack_layer L, int32_t n) {
 }
 
 // Validation shared by the two load entry points (before any device state changes).
+// Argument checks of a block load.  Device-resident buffers are read back on `st` (ordered after
+// whatever produced them there, e.g. bitstack_compress on a side stream), then `st` is synchronised
+// for those few bytes.
 static bitstack_status check_load_args(bitstack_layer L, int32_t first_block, int32_t count, const uint8_t* signs,
-                                       const void* u, const void* v, const float* s) {
+                                       const void* u, const void* v, const float* s, cudaStream_t st) {
   if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
   if (count < 0) return fail(BITSTACK_E_INVALID_ARG, "count < 0");
   if (first_block < 0 || first_block > L->n_res)
@@ -778,7 +818,8 @@ static bitstack_status check_load_args(bitstack_layer L, int32_t first_block, in
     for (int b = 0; b < count; ++b) {
       uint8_t last = 0;
       if (dev) {
-        CK(cudaMemcpy(&last, signs + (int64_t)b * cbytes + cbytes - 1, 1, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(&last, signs + (int64_t)b * cbytes + cbytes - 1, 1, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
       } else {
         last = signs[(int64_t)b * cbytes + cbytes - 1];
       }
@@ -790,7 +831,8 @@ static bitstack_status check_load_args(bitstack_layer L, int32_t first_block, in
     const float* sp = s;
     if (is_device_ptr(s)) {
       hs.resize(L->d_in);
-      CK(cudaMemcpy(hs.data(), s, L->d_in * 4, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpyAsync(hs.data(), s, L->d_in * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
       sp = hs.data();
     }
     for (int64_t c = 0; c < L->d_in; ++c)
@@ -912,7 +954,7 @@ static bitstack_status enqueue_blocks(bitstack_layer L, int32_t first_block, int
       const int sgrid = (int)std::min<int64_t>((elems + threads - 1) / threads, cap);
       bs::factor_scale_kernel<<<sgrid, threads, 0, st>>>(st_u, st_v, in_dt, L->k, 16 * h, kc, L->rows_local,
                                                           L->rows_pad, L->d_in, L->d_in_pad, vmax + 16 * h, u_dst,
-                                                          v_dst, L->dev_fdt ? 1 : 0, L->zscale + vb * 16);
+                                                          v_dst, L->dev_fdt, L->zscale + vb * 16, L->vmaxr + vb * 16);
       count_launch();
       CK(cudaGetLastError());
     }
@@ -941,10 +983,12 @@ static bitstack_status enqueue_scale(bitstack_layer L, const float* s, cudaStrea
 
 static bitstack_status load_blocks_impl(bitstack_layer L, int32_t first_block, int32_t count, const uint8_t* signs,
                                         const void* u, const void* v, const float* s, void* stream, bool wait) {
-  bitstack_status rs = check_load_args(L, first_block, count, signs, u, v, s);
-  if (rs) return rs;
-  DeviceGuard guard(L->device);
+  DeviceGuard guard(L ? L->device : 0);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bitstack_status rs = check_load_args(L, first_block, count, signs, u, v, s, st);
+  if (rs) return rs;
+  rs = order_after_last(L, st);
+  if (rs) return rs;
   if (count > 0) {
     rs = enqueue_blocks(L, first_block, count, signs, u, v, st);
     if (rs) return rs;
@@ -985,10 +1029,10 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype);
   // large batch: restored-tile GEMM path (bf16 factors); forced with BITSTACK_KERNEL_PREFILL
-  const bool pf_ok = L->dev_fdt == 1 && L->layout == 1 && L->n_act * L->kh <= 16;
+  const bool pf_ok = L->dev_fdt != 0 && L->layout == 1 && L->n_act * L->kh <= 16;
   if (L->kernel == BITSTACK_KERNEL_PREFILL && !pf_ok)
     return fail(BITSTACK_E_UNSUPPORTED, "prefill path needs bf16 factors and n <= 16");
-  if (L->kernel == BITSTACK_KERNEL_PREFILL || (L->kernel == BITSTACK_KERNEL_AUTO && pf_ok && batch >= kPrefillMinBatch))
+  if (L->kernel == BITSTACK_KERNEL_PREFILL || (L->kernel == BITSTACK_KERNEL_AUTO && pf_ok && prefill_auto(L, batch)))
     return launch_prefill(L, x, xdt, y, ydt, batch, st);
 
   // tcgen05 path: k <= 16 (zero-padded columns of U', V'), x rows bulk-copied by the
@@ -1081,6 +1125,8 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
     return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "no resident blocks (load_blocks first)");
   DeviceGuard guard(L->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bitstack_status ors = order_after_last(L, st);
+  if (ors) return ors;
   const int64_t xbytes = batch * L->d_in * dsize(x_dtype);
   const int64_t ybytes = batch * L->rows_local * (y_dtype == BITSTACK_F32 ? 4 : 2);
   const MemKind kx = mem_kind(x), ky = mem_kind(y);
@@ -1091,8 +1137,8 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
   // is the kernels' own PCIe traffic.  Everything else is staged through device memory with
   // cudaMemcpyAsync on `stream` (synchronous with respect to pageable host memory).
   const bool pf = L->kernel == BITSTACK_KERNEL_PREFILL ||
-                  (L->kernel == BITSTACK_KERNEL_AUTO && L->dev_fdt == 1 && L->layout == 1 && L->n_act * L->kh <= 16 &&
-                   batch >= kPrefillMinBatch);
+                  (L->kernel == BITSTACK_KERNEL_AUTO && L->dev_fdt != 0 && L->layout == 1 && L->n_act * L->kh <= 16 &&
+                   prefill_auto(L, batch));
   const bool plain_io = !pf && (L->layout == 1 || L->kernel == BITSTACK_KERNEL_SIMT) && L->n_act > 0;
   const bool small = xbytes <= (1 << 20) && ybytes <= (1 << 20);
   const void* xd = x;
@@ -1170,6 +1216,10 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   }
   DeviceGuard guard(layers[0]->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  for (int i = 0; i < fc; ++i) {
+    bitstack_status ors = order_after_last(fl[i], st);
+    if (ors) return ors;
+  }
   const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype), ysz = y_dtype == BITSTACK_F32 ? 4 : 2;
@@ -1196,6 +1246,8 @@ bitstack_status bitstack_reconstruct(bitstack_layer L, void* w, bitstack_dtype w
   if (L->n_res == 0) return fail(BITSTACK_E_LEVEL_OUT_OF_RANGE, "no resident blocks");
   DeviceGuard guard(L->device);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bitstack_status ors = order_after_last(L, st);
+  if (ors) return ors;
   const int wdt = w_dtype == BITSTACK_F32 ? 0 : (w_dtype == BITSTACK_BF16 ? 1 : 2);
   dim3 grid((unsigned)((L->d_in + 31) / 32), (unsigned)((L->rows_local + 7) / 8));
   bs::reconstruct_kernel<<<grid, 256, 0, st>>>(L->signs, L->u, L->v, L->inv_s, w, L->n_act * L->kh, L->nq,

@@ -99,8 +99,10 @@ __global__ void __launch_bounds__(256) xprep_kernel(const void* __restrict__ x, 
 // ------------------------------------------------------------------ W' image
 struct WtileParams {
   const uint4* signs;     // [n_cap][nq][rows_pad] F8 device layout
-  const __nv_bfloat16* u; // [n_cap][rows_pad][16] U'
-  const __nv_bfloat16* v; // [n_cap][d_in_pad][16] V'
+  const uint16_t* u;      // [n_cap][rows_pad][16] U' (bf16 or f16 storage)
+  const uint16_t* v;      // [n_cap][d_in_pad][16] V'
+  const float* vmaxr;     // [n_cap][16] max_c |V'[c, r]|
+  int f16;                // 1: fp16 factor storage (MMA format 0), 0: bf16 (format 1)
   uint8_t* img;           // [row_tiles_img][kc] tiles of kImgTileA bytes
   int* rowexp;            // [rows_pad] W' row j is stored as W'[j,:] 2^-rowexp[j] (fp16 range)
   int n, nq, rows_pad, row_tiles, row_tiles_img, kc;
@@ -151,7 +153,7 @@ __global__ void __launch_bounds__(256, (2 * G * kPK <= 256) ? 2 : 1) wtile_kerne
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-  constexpr uint32_t idesc = idesc_f16_f32(128, kPK, 1);   // bf16 x bf16 -> f32
+  const uint32_t idesc = idesc_f16_f32(128, kPK, p.f16 ? 0u : 1u);   // bf16 / fp16 factors -> f32
 
   int gstep = 0;   // steps issued by this CTA so far (TMEM buffer = gstep & 1, barrier phase)
   for (long long e = e0; e < e1;) {
@@ -239,8 +241,8 @@ __global__ void __launch_bounds__(256, (2 * G * kPK <= 256) ? 2 : 1) wtile_kerne
     fence_proxy_async_smem();
     __syncthreads();                 // U' and V'(0) in SMEM (the previous segment's MMAs all waited)
     if (tid == 0) issue(vb0, sbase & 1, g_0);
-    // |W'[row, c]| <= 2^8 sum_i sum_r |U'_i[row, r]| (|V'| <= 2^8 after the load-time rebalancing):
-    // the row's fp16 image is W' 2^-re with that bound below 2^15
+    // |W'[row, c]| <= sum_i sum_r |U'_i[row, r]| max_c |V'_i[c, r]|: the row's fp16 image is
+    // W' 2^-re with that bound below 2^15
     int re = 0;
     {
       float bound = 0.f;
@@ -248,14 +250,15 @@ __global__ void __launch_bounds__(256, (2 * G * kPK <= 256) ? 2 : 1) wtile_kerne
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const uint4 raw = *reinterpret_cast<const uint4*>(su + i * C::kUBytes + ((j >> 3) * 2 + kk) * 128 + (j & 7) * 16);
-          const __nv_bfloat162* bp = reinterpret_cast<const __nv_bfloat162*>(&raw);
+          const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
           for (int e2 = 0; e2 < 4; ++e2) {
-            const float2 f = __bfloat1622float2(bp[e2]);
-            bound += fabsf(f.x) + fabsf(f.y);
+            const float2 f = p.f16 ? __half22float2(*reinterpret_cast<const __half2*>(&wv[e2]))
+                                   : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e2]));
+            const int r = kk * 8 + 2 * e2;
+            bound += fabsf(f.x) * __ldg(p.vmaxr + i * 16 + r) + fabsf(f.y) * __ldg(p.vmaxr + i * 16 + r + 1);
           }
         }
-      bound *= 256.f;
       if (bound > 0.f && bound < __int_as_float(0x7f800000)) re = xs_exp(__float_as_uint(bound), 15);
       if (h == 0 && c0 == 0) p.rowexp[row] = re;
     }

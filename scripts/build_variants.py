@@ -9,13 +9,13 @@ from paper_2410_23918_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": [],
+    "r3": ["-DBS_MX_R1=3"],
     "r2": ["-DBS_MX_R1=2"],
-    "tpi2": ["-DBS_MX_TPI=2"],
-    "nomma": ["-DBS_MX_EXP_NOMMA"],
-    "noexp": ["-DBS_MX_EXP_NOEXP"],
     "skel": ["-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
-    "skelnodata": ["-DBS_MX_EXP_NODATA", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
-    "nodata": ["-DBS_MX_EXP_NODATA"],
+    "r3skel": ["-DBS_MX_R1=3", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
+    "r2skel": ["-DBS_MX_R1=2", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
+    "nomma": ["-DBS_MX_EXP_NOMMA"],
+    "r3nomma": ["-DBS_MX_R1=3", "-DBS_MX_EXP_NOMMA"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)

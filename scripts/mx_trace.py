@@ -18,6 +18,9 @@ for i in range(ncp):
     lay = pkg.Layer(do, di, 16, n, "bf16")
     lay.load_blocks(0, signs, torch.from_numpy(u).to(torch.bfloat16), torch.from_numpy(v).to(torch.bfloat16), s)
     lays.append(lay)
+for a in sys.argv:
+    if a.startswith("n="):
+        for l in lays: l.set_num_blocks(int(a[2:]))
 x = torch.from_numpy(make_x(1, channel_gains(di, 5), 6).astype(np.float32)).to(torch.bfloat16).cuda()
 y = torch.empty(1, do, device="cuda")
 for _ in range(5):
@@ -36,6 +39,8 @@ for rep in range(2):
     cta = cta[cta[:, 0] != 0]
     t0 = cta[:, 0].min()
     ex = np.sort((cta[:, 1] - t0) / 1e3)
+    ent = np.sort((cta[:, 0] - t0) / 1e3)
+    print("entry quantiles us", np.round(ent[[0, len(ent)//4, len(ent)//2, 3*len(ent)//4, -1]], 2))
     print(f"call {e0.elapsed_time(e1)*1e3:.1f} us; CTAs {len(cta)} entry spread {(cta[:,0].max()-t0)/1e3:.2f} us; exit min {ex[0]:.2f} med {np.median(ex):.2f} max {ex[-1]:.2f} us; units {cta[:,2].min()}-{cta[:,2].max()}")
 t = full[:65536].reshape(-1, 16)
 print("unit | prod_issue | exp0: landed expanded afull_arrive st_done | iss: afull_done - commit | iss: loop_top - -  (cycles, CTA clock)")

@@ -77,7 +77,7 @@ TOL = {"bf16": 1e-3, "f16": 1e-3, "f32": 1e-5}
 # (path name, factor dtype, kernel): the MX e4m3 decode, the fp16 decode (fp32 factors), the
 # prefill GEMM (forced at small batches), the SIMT kernel
 PATHS = [("mx", "bf16", "tc"), ("mx16", "f16", "tc"), ("fp16dec", "f32", "tc"), ("prefill", "bf16", "prefill"),
-         ("simt", "bf16", "simt")]
+         ("prefill16", "f16", "prefill"), ("simt", "bf16", "simt")]
 
 
 @pytest.mark.parametrize("path,dtype,kernel", PATHS)
@@ -195,3 +195,27 @@ def test_decode_sign_expansion_bit_exact(bs, k, factor_dtype):
         code = (w + (2 ** n - 1)) // 2
         for i in range(n):
             np.testing.assert_array_equal((code >> i) & 1, want[i][:, c])
+
+
+# ------------------------------------------------------------------ one handle, several streams
+def test_calls_on_one_handle_from_two_streams(bs):
+    """A handle's workspaces are reused by every call; calls issued on alternating streams must be
+    ordered by the library (include/bitstack.h conventions) and give the single-stream results."""
+    g, s32, blocks = case(512, 1024, 4, "bf16", 9100)
+    lay = layer(bs, 512, 1024, blocks, s32, "bf16")
+    xs = [torch.from_numpy(make_x(b, g, 200 + i).astype(np.float32)).cuda() for i, b in enumerate([1, 3, 1, 8, 2, 20] * 3)]
+    ref = []
+    for x in xs:
+        ref.append(lay.matmul(x).clone())
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for i, x in enumerate(xs):
+        st = s1 if i % 2 == 0 else s2
+        y = torch.empty((x.shape[0], 512), dtype=torch.float32, device="cuda")
+        y.record_stream(st)
+        lay.matmul_raw(x.data_ptr(), bs.F32, y.data_ptr(), bs.F32, x.shape[0], st.cuda_stream)
+        outs.append(y)
+    torch.cuda.synchronize()
+    for y, r in zip(outs, ref):
+        assert torch.equal(y, r)
