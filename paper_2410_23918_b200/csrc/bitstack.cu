@@ -294,6 +294,7 @@ bitstack_status launch_decode_mx(bitstack_layer L, const bs::DecodeParams& prm_i
   return BITSTACK_OK;
 }
 
+int mx_occ(int nb) { return nb == 1 ? bs::MxGeom<1>::OCC : 1; }
 int mx_rows(int nb) {
   switch (nb) {
     case 1: return bs::MxGeom<1>::R;
@@ -556,7 +557,7 @@ bitstack_status launch_grouped_mx(const bitstack_layer* layers, int count, const
     cpg[i] = 1;
     total += n_groups[i];
   }
-  const int budget = layers[0]->sm_count;
+  const int budget = layers[0]->sm_count * C::OCC;
   for (;;) {
     int best = -1;
     double best_w = 0.0;
@@ -1080,7 +1081,7 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
       const int R = mx_rows(nb);
       const int n_groups = (L->row_tiles + R - 1) / R;
       const int64_t units = (int64_t)L->n_act * (kfuse ? 1 : L->kh) * L->nq;
-      int cpg = std::max(1, L->sm_count / n_groups);
+      int cpg = std::max(1, mx_occ(nb) * L->sm_count / n_groups);
       cpg = (int)std::min<int64_t>(cpg, units);
       bs::DecodeParams prm = decode_params(L, x, xdt, xsz, y, ydt, ysz, b0, bc, n_groups, cpg);
       if (kfuse) {

@@ -230,14 +230,17 @@ template <int NB> struct MxGeom;                        // row tiles per CTA by 
 #ifndef BS_MX_R1
 #define BS_MX_R1 4
 #endif
-template <> struct MxGeom<1> { static constexpr int R = BS_MX_R1; };
-template <> struct MxGeom<2> { static constexpr int R = 2; };
-template <> struct MxGeom<3> { static constexpr int R = 2; };
-template <> struct MxGeom<4> { static constexpr int R = 1; };
-template <> struct MxGeom<5> { static constexpr int R = 1; };
-template <> struct MxGeom<6> { static constexpr int R = 1; };
-template <> struct MxGeom<7> { static constexpr int R = 1; };
-template <> struct MxGeom<8> { static constexpr int R = 1; };
+#ifndef BS_MX_OCC1
+#define BS_MX_OCC1 1
+#endif
+template <> struct MxGeom<1> { static constexpr int R = BS_MX_R1, OCC = BS_MX_OCC1; };
+template <> struct MxGeom<2> { static constexpr int OCC = 1, R = 2; };
+template <> struct MxGeom<3> { static constexpr int OCC = 1, R = 2; };
+template <> struct MxGeom<4> { static constexpr int OCC = 1, R = 1; };
+template <> struct MxGeom<5> { static constexpr int OCC = 1, R = 1; };
+template <> struct MxGeom<6> { static constexpr int OCC = 1, R = 1; };
+template <> struct MxGeom<7> { static constexpr int OCC = 1, R = 1; };
+template <> struct MxGeom<8> { static constexpr int OCC = 1, R = 1; };
 
 #ifndef BS_MX_SMEM_KB
 #define BS_MX_SMEM_KB 200
@@ -273,19 +276,21 @@ struct DecodeMxCfg {
   static constexpr int kThreads = 32 * (5 * NI + 5);
   static constexpr int kSignBytes = R * kTileRows * 16;
   static constexpr int kStageBytes = (kSignBytes + Z::kUnit + 1023) / 1024 * 1024;
-  static constexpr int S0 = BS_MX_SMEM_KB * 1024 / kStageBytes;
+  static constexpr int OCC = MxGeom<NB>::OCC;         // resident CTAs per SM (TMEM / smem split)
+  static constexpr int kTmemCols = 512 / OCC;
+  static constexpr int S0 = BS_MX_SMEM_KB * 1024 / OCC / kStageBytes;
   static constexpr int STAGES = S0 > BS_MX_STAGES ? BS_MX_STAGES : (S0 < 2 ? 2 : S0);
   static constexpr int kBarBytes = 1024;
   static constexpr int kSmemBytes = STAGES * kStageBytes + kBarBytes + 1024;   // + alignment slack
   // TMEM columns: A slots [slot][tile] (32 each) | accumulators [t] (N each) | SFA (4) | SFB [i][slot]
   static constexpr int kSfCols = 4 * Z::NCH;
-  static constexpr int NS0 = (512 - R * N - 4) / (R * 32 + NI * kSfCols);
+  static constexpr int NS0 = (kTmemCols - R * N - 4) / (R * 32 + NI * kSfCols);
   static constexpr int NSLOT = NS0 > 4 ? 4 : NS0;
   static constexpr uint32_t kColAcc = NSLOT * R * 32;
   static constexpr uint32_t kColSfa = kColAcc + R * N;
   static constexpr uint32_t kColSfb = kColSfa + 4;
   static_assert(NSLOT >= 2, "need a double-buffered A slot");
-  static_assert(kColSfb + NI * NSLOT * kSfCols <= 512, "TMEM overflow");
+  static_assert(kColSfb + NI * NSLOT * kSfCols <= kTmemCols, "TMEM overflow");
   static_assert(kSmemBytes <= 227 * 1024, "smem overflow");
   static_assert(R * kTileRows * NB <= kPartStride, "split-K slot");
 };
@@ -350,7 +355,7 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
     }
     fence_mbar_init();
   }
-  if (warp == C::kWarpProd) tmem_alloc<512>(tmem_slot);
+  if (warp == C::kWarpProd) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -594,7 +599,7 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == C::kWarpProd) tmem_dealloc<512>(tbase);
+  if (warp == C::kWarpProd) tmem_dealloc<C::kTmemCols>(tbase);
   if (threadIdx.x == 0) {
     __threadfence();
     const int prev = atomicAdd(p.counters + g, 1);
@@ -609,7 +614,7 @@ __device__ __forceinline__ void decode_mx_body(const DecodeParams& p, const int 
 }
 
 template <int NB>
-__global__ void __launch_bounds__(DecodeMxCfg<NB>::kThreads, 1) decode_mx_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(DecodeMxCfg<NB>::kThreads, DecodeMxCfg<NB>::OCC) decode_mx_kernel(const DecodeParams p) {
   decode_mx_body<NB>(p, (int)blockIdx.x);
 }
 
@@ -619,7 +624,7 @@ struct DecodeMxGroup {
   DecodeParams prm[kMaxMxGroup];
 };
 template <int NB>
-__global__ void __launch_bounds__(DecodeMxCfg<NB>::kThreads, 1) decode_mx_grouped_kernel(
+__global__ void __launch_bounds__(DecodeMxCfg<NB>::kThreads, DecodeMxCfg<NB>::OCC) decode_mx_grouped_kernel(
     const __grid_constant__ DecodeMxGroup grp) {
   int i = 0;
   while (i + 1 < grp.count && (int)blockIdx.x >= grp.cta_start[i + 1]) ++i;

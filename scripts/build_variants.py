@@ -9,13 +9,10 @@ from paper_2410_23918_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "base": [],
-    "r3": ["-DBS_MX_R1=3"],
-    "r2": ["-DBS_MX_R1=2"],
+    "occ2": ["-DBS_MX_R1=2", "-DBS_MX_OCC1=2"],
+    "occ2r1": ["-DBS_MX_R1=1", "-DBS_MX_OCC1=2"],
+    "occ2skel": ["-DBS_MX_R1=2", "-DBS_MX_OCC1=2", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
     "skel": ["-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
-    "r3skel": ["-DBS_MX_R1=3", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
-    "r2skel": ["-DBS_MX_R1=2", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
-    "nomma": ["-DBS_MX_EXP_NOMMA"],
-    "r3nomma": ["-DBS_MX_R1=3", "-DBS_MX_EXP_NOMMA"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)

@@ -9,7 +9,7 @@ using namespace bs;
 
 template <int STAGES>
 __global__ void __launch_bounds__(64, 1) stream(const uint8_t* src, int units, int chunk, long long stride, int G,
-                                                int J, long long* out) {
+                                                int J, long long* out, const uint8_t* zsrc, int zbytes) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[STAGES], empty[STAGES];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -26,7 +26,9 @@ __global__ void __launch_bounds__(64, 1) stream(const uint8_t* src, int units, i
       int s = 0; uint32_t ph = 0;
       for (int u = u0; u < u1; ++u) {
         if (u - u0 >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], chunk);
+        mbar_arrive_expect_tx(&full[s], chunk + zbytes);
+        if (zbytes)   // a second copy per unit from an L2-resident buffer (the decode's Zq unit)
+          bulk_g2s(smem + STAGES * chunk + s * zbytes, zsrc + (long long)u * zbytes, zbytes, &full[s], pol);
         bulk_g2s(smem + s * chunk, src + (long long)u * stride + (long long)g * chunk, chunk, &full[s], pol);
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
@@ -43,17 +45,18 @@ __global__ void __launch_bounds__(64, 1) stream(const uint8_t* src, int units, i
 }
 
 template <int STAGES>
-void go(const char* name, const uint8_t* buf, int units, int chunk, long long stride, int G, int J) {
+void go(const char* name, const uint8_t* buf, int units, int chunk, long long stride, int G, int J,
+        const uint8_t* zbuf = nullptr, int zbytes = 0) {
   long long* d;
   cudaMalloc(&d, 8 * G * J);
-  const int smem = STAGES * chunk;
+  const int smem = STAGES * (chunk + zbytes);
   cudaFuncSetAttribute(stream<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
-  stream<STAGES><<<G * J, 64, smem>>>(buf, units, chunk, stride, G, J, d);   // warm
+  stream<STAGES><<<G * J, 64, smem>>>(buf, units, chunk, stride, G, J, d, zbuf, zbytes);   // warm
   cudaEventRecord(e0);
   const int reps = 5;
-  for (int r = 0; r < reps; ++r) stream<STAGES><<<G * J, 64, smem>>>(buf, units, chunk, stride, G, J, d);
+  for (int r = 0; r < reps; ++r) stream<STAGES><<<G * J, 64, smem>>>(buf, units, chunk, stride, G, J, d, zbuf, zbytes);
   cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   float ms = 0;
@@ -77,6 +80,11 @@ int main() {
   go<8>("C5 pattern, 16 KB chunks", buf, 1344, 16384, 262144, 16, 9);
   go<8>("C5 pattern, 4 KB chunks", buf, 5376, 4096, 65536, 16, 9);
   go<8>("C5 pattern 148 CTAs (37 x 4)", buf, 2688, 8192, 131072, 16, 9);
+  uint8_t* zq;
+  cudaMalloc(&zq, 2688ll * 6656);
+  cudaMemset(zq, 2, 2688ll * 6656);
+  go<8>("C5 pattern + 6.5 KB Zq copy per unit", buf, 2688, 8192, 131072, 16, 9, zq, 6656);
+  go<13>("C5 pattern + 6.5 KB Zq copy per unit", buf, 2688, 8192, 131072, 16, 9, zq, 6656);
   cudaFree(buf);
   return 0;
 }
