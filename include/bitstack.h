@@ -63,7 +63,9 @@ typedef enum {
   BITSTACK_E_CAPACITY = -5,           /* first_block + count > n_capacity */
   BITSTACK_E_OOM = -6,                /* device allocation failed */
   BITSTACK_E_CUDA = -7,               /* CUDA runtime error (message has the CUDA string) */
-  BITSTACK_E_UNSUPPORTED = -8         /* not an sm_100 device, a forced path that cannot run, ... */
+  BITSTACK_E_UNSUPPORTED = -8,        /* not an sm_100 device, a forced path that cannot run, ... */
+  BITSTACK_E_IO = -9                  /* block store: file error, bad magic / version, corrupt or
+                                         truncated record (SPEC S:465 BadMagic / CorruptRecord / ...) */
 } bitstack_status;
 
 /* Kernel selection for bitstack_matmul (bitstack_set_kernel). */
@@ -208,6 +210,63 @@ BITSTACK_API bitstack_status bitstack_set_kernel(bitstack_layer layer, bitstack_
 /* Eq.9: delta_W = m*n + factor_bits*k*(m+n) bits (factor_bits = 16 in
  * the paper).  Pure host arithmetic, never fails. */
 BITSTACK_API int64_t bitstack_block_size_bits(int64_t m, int64_t n, int32_t k, int32_t factor_bits);
+
+/* ---------------------------------------------------------------- block store (on disk)
+ * Residual blocks as "basic transmission units" between storage and the device (PAPER.md
+ * abstract P:8; Fig.2 P:64 "load more weight residuals from storage when available memory
+ * increases"; SPEC S:446-497 store).  A store is a file of block records in the order they were
+ * appended -- the caller's universal stack order (budget.py), so a memory-budget prefix is a
+ * contiguous byte range -- with an offset index, so any record range is read without touching
+ * the rest of the file.  Format v1 (little-endian, written once, no in-place mutation) in
+ * csrc/store.cuh.  Host code only: usable without a GPU except bitstack_store_load_range.
+ * A store handle is used by one host thread at a time. */
+typedef struct bitstack_store_s* bitstack_store;
+
+typedef struct {
+  int32_t stack;                 /* caller's stack id (e.g. the weight matrix index) */
+  int32_t block;                 /* block index i of that stack (Eq.8 order) */
+  int64_t d_out, d_in;
+  int32_t k;
+  bitstack_dtype factor_dtype;
+  int64_t size_bits;             /* declared Eq.9 size at the dtype's factor bits */
+  int64_t sign_bytes, u_bytes, v_bytes, s_bytes;   /* payload parts; s only with block 0 */
+  int64_t offset;                /* record byte offset in the file */
+  uint32_t crc32;                /* CRC-32 (IEEE) of the payload */
+} bitstack_store_record;
+
+/* Create (truncate) a store file for writing.  Errors: E_INVALID_ARG, E_IO. */
+BITSTACK_API bitstack_status bitstack_store_create(const char* path, bitstack_store* out);
+/* Append one block record: the canonical layouts of bitstack_load_blocks for ONE block (host
+ * buffers), s (d_in float32) given with block 0 and only there.
+ * Errors: E_INVALID_ARG, E_MALFORMED_BUFFER (pad bits), E_IO. */
+BITSTACK_API bitstack_status bitstack_store_append(bitstack_store store, int32_t stack, int32_t block,
+                                                   int64_t d_out, int64_t d_in, int32_t k,
+                                                   bitstack_dtype factor_dtype, const uint8_t* signs,
+                                                   const void* u, const void* v, const float* s);
+/* Open a store for reading (header + index only; record headers and payloads are read on demand).
+ * Errors: E_INVALID_ARG, E_IO (cannot open, bad magic, version / endianness mismatch, truncated
+ * or corrupt index). */
+BITSTACK_API bitstack_status bitstack_store_open(const char* path, bitstack_store* out);
+BITSTACK_API bitstack_status bitstack_store_count(bitstack_store store, int64_t* n_records);
+/* Record metadata (reads its 64-byte header).  Errors: E_LEVEL_OUT_OF_RANGE, E_IO. */
+BITSTACK_API bitstack_status bitstack_store_record_info(bitstack_store store, int64_t record,
+                                                        bitstack_store_record* out);
+/* Payload of one record into host buffers sized by record_info (NULL skips a part; the CRC is
+ * checked when every part is read).  Errors: E_LEVEL_OUT_OF_RANGE, E_IO (truncated, CRC). */
+BITSTACK_API bitstack_status bitstack_store_read(bitstack_store store, int64_t record, uint8_t* signs, void* u,
+                                                 void* v, float* s);
+/* Stream records [first_record, first_record + count) -- consecutive blocks of the stack the
+ * layer holds -- from the file into the layer: each record is read into one of two pinned
+ * buffers of the store (the read of record j+1 overlaps the DMA and repack of record j) and
+ * pushed with bitstack_load_blocks_async at its block index (so the range must continue the
+ * layer's resident prefix).  Returns once enqueued on `stream`.
+ * Errors: E_LEVEL_OUT_OF_RANGE, E_DIM_MISMATCH (shape / rank / dtype), E_IO, and the errors of
+ * bitstack_load_blocks. */
+BITSTACK_API bitstack_status bitstack_store_load_range(bitstack_store store, bitstack_layer layer,
+                                                       int64_t first_record, int64_t count, void* stream);
+/* Writer: write the index and header, fsync.  Reader: release (waits for pending loads).
+ * NULL is a no-op.  Errors: E_IO. */
+BITSTACK_API bitstack_status bitstack_store_close(bitstack_store store);
 
 /* Thread-local message of the last error on this thread ("" if none). */
 BITSTACK_API const char* bitstack_last_error(void);

@@ -3,6 +3,6 @@
 (include/bitstack.h).  Python here is argument marshalling only."""
 from .bitstack import (  # noqa: F401
     BF16, F16, F32, BitStackError, Group, Layer, block_size_bits, compress, launch_count, load_library, matmul_grouped,
-    profile_begin, profile_end,
+    profile_begin, profile_end, Store,
 )
 from . import budget  # noqa: F401,E402  (memory-budget level selection, host logic)

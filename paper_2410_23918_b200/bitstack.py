@@ -22,7 +22,7 @@ _DTYPE_NAMES = {"f32": F32, "float32": F32, "bf16": BF16, "bfloat16": BF16, "f16
 
 STATUS = {
     0: "OK", -1: "E_INVALID_ARG", -2: "E_DIM_MISMATCH", -3: "E_LEVEL_OUT_OF_RANGE",
-    -4: "E_MALFORMED_BUFFER", -5: "E_CAPACITY", -6: "E_OOM", -7: "E_CUDA", -8: "E_UNSUPPORTED",
+    -4: "E_MALFORMED_BUFFER", -5: "E_CAPACITY", -6: "E_OOM", -7: "E_CUDA", -8: "E_UNSUPPORTED", -9: "E_IO",
 }
 
 EXPORTED_SYMBOLS = (
@@ -31,6 +31,8 @@ EXPORTED_SYMBOLS = (
     "bitstack_matmul", "bitstack_matmul_grouped", "bitstack_reconstruct", "bitstack_get_info", "bitstack_set_kernel",
     "bitstack_block_size_bits", "bitstack_last_error", "bitstack_compress", "bitstack_profile_begin",
     "bitstack_profile_end", "bitstack_launch_count",
+    "bitstack_store_create", "bitstack_store_append", "bitstack_store_open", "bitstack_store_count",
+    "bitstack_store_record_info", "bitstack_store_read", "bitstack_store_load_range", "bitstack_store_close",
 )
 
 
@@ -49,6 +51,17 @@ class Info(ctypes.Structure):
         ("n_resident", ctypes.c_int32), ("n_active", ctypes.c_int32),
         ("factor_dtype", ctypes.c_int32), ("device", ctypes.c_int32),
         ("device_bytes", ctypes.c_int64), ("block_bytes_device", ctypes.c_int64),
+    ]
+
+
+class StoreRecord(ctypes.Structure):
+    _fields_ = [
+        ("stack", ctypes.c_int32), ("block", ctypes.c_int32),
+        ("d_out", ctypes.c_int64), ("d_in", ctypes.c_int64),
+        ("k", ctypes.c_int32), ("factor_dtype", ctypes.c_int32),
+        ("size_bits", ctypes.c_int64),
+        ("sign_bytes", ctypes.c_int64), ("u_bytes", ctypes.c_int64), ("v_bytes", ctypes.c_int64),
+        ("s_bytes", ctypes.c_int64), ("offset", ctypes.c_int64), ("crc32", ctypes.c_uint32),
     ]
 
 
@@ -86,6 +99,14 @@ def load_library(path: Optional[str] = None) -> ctypes.CDLL:
         "bitstack_profile_begin": (I32, [I32]),
         "bitstack_profile_end": (I32, [P(I32), P(ctypes.c_double)]),
         "bitstack_launch_count": (I64, []),
+        "bitstack_store_create": (I32, [ctypes.c_char_p, P(VP)]),
+        "bitstack_store_append": (I32, [VP, I32, I32, I64, I64, I32, I32, VP, VP, VP, VP]),
+        "bitstack_store_open": (I32, [ctypes.c_char_p, P(VP)]),
+        "bitstack_store_count": (I32, [VP, P(I64)]),
+        "bitstack_store_record_info": (I32, [VP, I64, P(StoreRecord)]),
+        "bitstack_store_read": (I32, [VP, I64, VP, VP, VP, VP]),
+        "bitstack_store_load_range": (I32, [VP, VP, I64, I64, VP]),
+        "bitstack_store_close": (I32, [VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -303,3 +324,90 @@ def compress(w, x_cal, n: int, k: int = 16, factor_dtype="bf16", oversample: int
                                  int(power_iters), int(seed), _ptr(signs), _ptr(u), _ptr(v), _ptr(s), _ptr(sigma),
                                  _ptr(resid), _stream_handle(stream)))
     return signs, u, v, s, sigma, resid
+
+
+# ---------------------------------------------------------------- block store (on disk)
+_NP_FACTOR = {F32: np.float32, BF16: np.uint16, F16: np.float16}
+
+
+class Store:
+    """bitstack_store_* (include/bitstack.h): residual blocks on disk in universal-stack order,
+    readable by record range.  Store.create(path) writes, Store.open(path) reads."""
+
+    def __init__(self, handle, writer: bool):
+        self._h = handle
+        self.writer = writer
+
+    @classmethod
+    def create(cls, path: str) -> "Store":
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.bitstack_store_create(os.fsencode(path), ctypes.byref(h)))
+        return cls(h, True)
+
+    @classmethod
+    def open(cls, path: str) -> "Store":
+        lib = load_library()
+        h = ctypes.c_void_p()
+        _check(lib.bitstack_store_open(os.fsencode(path), ctypes.byref(h)))
+        return cls(h, False)
+
+    def append(self, stack: int, block: int, signs, u, v, s=None, factor_dtype="bf16") -> None:
+        """One block in the canonical host layouts of Layer.load_blocks (u / v: [d_out, k] /
+        [d_in, k] in the factor dtype; bf16 as uint16 bit patterns); s with block 0 only."""
+        fdt = dtype_code(factor_dtype)
+        signs = np.ascontiguousarray(signs, dtype=np.uint8)
+        u = np.ascontiguousarray(u)
+        v = np.ascontiguousarray(v)
+        s_arr = None if s is None else np.ascontiguousarray(s, dtype=np.float32)
+        d_out, k = u.shape
+        d_in = v.shape[0]
+        _check(_lib.bitstack_store_append(self._h, stack, block, d_out, d_in, k, fdt, _ptr(signs), _ptr(u), _ptr(v),
+                                          _ptr(s_arr)))
+
+    def __len__(self) -> int:
+        n = ctypes.c_int64()
+        _check(_lib.bitstack_store_count(self._h, ctypes.byref(n)))
+        return int(n.value)
+
+    def info(self, record: int) -> dict:
+        r = StoreRecord()
+        _check(_lib.bitstack_store_record_info(self._h, record, ctypes.byref(r)))
+        return {name: getattr(r, name) for name, _ in StoreRecord._fields_}
+
+    def read(self, record: int):
+        """(stack, block, signs, u, v, s or None) of one record, host numpy arrays."""
+        r = self.info(record)
+        signs = np.empty(r["sign_bytes"], np.uint8)
+        ft = _NP_FACTOR[r["factor_dtype"]]
+        u = np.empty((r["d_out"], r["k"]), ft)
+        v = np.empty((r["d_in"], r["k"]), ft)
+        s = np.empty(r["d_in"], np.float32) if r["s_bytes"] else None
+        _check(_lib.bitstack_store_read(self._h, record, _ptr(signs), _ptr(u), _ptr(v), _ptr(s)))
+        return r["stack"], r["block"], signs, u, v, s
+
+    def read_range(self, first: int, count: int):
+        return [self.read(first + j) for j in range(count)]
+
+    def load_range(self, layer, first: int, count: int, stream=None) -> None:
+        """Stream records [first, first + count) of one stack into `layer` (async on `stream`)."""
+        _check(_lib.bitstack_store_load_range(self._h, layer._h, first, count, _stream_handle(stream)))
+
+    def close(self) -> None:
+        if self._h is not None:
+            _check(_lib.bitstack_store_close(self._h))
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and _lib is not None:
+                _lib.bitstack_store_close(self._h)
+                self._h = None
+        except Exception:  # noqa: BLE001
+            pass

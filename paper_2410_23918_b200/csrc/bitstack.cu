@@ -1501,3 +1501,5 @@ bitstack_status bitstack_profile_end(int32_t* launches, double* total_ms) {
 }
 
 }  // extern "C"
+
+#include "store.cuh"

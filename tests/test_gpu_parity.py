@@ -700,3 +700,55 @@ def test_full_size_sampled_rows(bs, name, d_out, d_in, n, batch):
     ref = _sampled_reference(signs, u_val, v_val, s, n, xr, rows, d_out, d_in)
     assert O.relative_l2(y[:, rows], ref) <= 1e-3
     del lay
+
+
+# ------------------------------------------------------------------ on-disk block store
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_store_load_range_matches_memory_load(bs, tmp_path, dtype):
+    """Blocks written to a BSTK file (two stacks interleaved, as the universal order does) and
+    streamed back with bitstack_store_load_range give the same y as bitstack_load_blocks from
+    memory, bit for bit, and a partial record range is a usable prefix (P:8 "basic transmission
+    units"; SPEC S:475)."""
+    cases = [compress_case(384, 512, 4, dtype, 7100), compress_case(256, 640, 4, dtype, 7101)]
+    path = str(tmp_path / "m.bstk")
+    with bs.Store.create(path) as st:
+        for i in range(4):
+            for sid, (g, s32, blocks) in enumerate(cases):
+                signs, u, v = stack_blocks(blocks[i:i + 1], dtype)
+                st.append(sid, i, signs[0], u[0], v[0], s32 if i == 0 else None, factor_dtype=dtype)
+    with bs.Store.open(path) as st:
+        for sid, (g, s32, blocks) in enumerate(cases):
+            d_out, d_in = (384, 512) if sid == 0 else (256, 640)
+            ref_lay = make_layer(bs, d_out, d_in, blocks, s32, dtype)
+            lay = bs.Layer(d_out, d_in, k=16, n_capacity=4, factor_dtype=dtype)
+            x = make_x(3, g, 11)
+            for i in range(4):                     # record of (stack sid, block i) = 2 i + sid
+                st.load_range(lay, 2 * i + sid, 1)
+                lay.set_num_blocks(i + 1)
+                ref_lay.set_num_blocks(i + 1)
+                y, xr = gpu_y(lay, x)
+                y_ref, _ = gpu_y(ref_lay, x)
+                assert np.array_equal(y, y_ref)
+                assert O.relative_l2(y, oracle_y(blocks, s32, i + 1, xr)) <= 1e-3
+            with pytest.raises(bs.BitStackError):   # a record of the other stack: shape mismatch
+                st.load_range(lay, 1 - sid, 1)
+    # one stack, contiguous: a 2-record prefix then the rest
+    g, s32, blocks = cases[0]
+    path2 = str(tmp_path / "one.bstk")
+    with bs.Store.create(path2) as st:
+        signs, u, v = stack_blocks(blocks, dtype)
+        for i in range(4):
+            st.append(0, i, signs[i], u[i], v[i], s32 if i == 0 else None, factor_dtype=dtype)
+    with bs.Store.open(path2) as st:
+        lay = bs.Layer(384, 512, k=16, n_capacity=4, factor_dtype=dtype)
+        st.load_range(lay, 0, 2)
+        torch.cuda.synchronize()
+        assert lay.info()["n_resident"] == 2
+        lay.set_num_blocks(2)                      # loads never raise the active level
+        x = make_x(2, g, 12)
+        y, xr = gpu_y(lay, x)
+        assert O.relative_l2(y, oracle_y(blocks, s32, 2, xr)) <= 1e-3
+        st.load_range(lay, 2, 2)
+        lay.set_num_blocks(4)
+        y, xr = gpu_y(lay, x)
+        assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 1e-3
