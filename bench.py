@@ -724,6 +724,11 @@ def main():
     ap.add_argument("--order", choices=["average", "random"], default="average",
                     help="c4: the universal stack's sorting (P:351); Greedy needs measured perplexities")
     ap.add_argument("--sweep", action="store_true", help="also report us/layer for n = 1, 2, 4, 8, 16")
+    ap.add_argument("--kernel", choices=["auto", "tc", "prefill", "simt"], default="auto",
+                    help="decode workloads: force one path (bitstack_set_kernel) for crossover sweeps")
+    ap.add_argument("--shard", type=int, default=1,
+                    help="decode, one GPU: time rank 0's row shard of a G-way row split (the per-rank "
+                         "kernel of SURVEY §8(e) at r_G = d_out / G rows, V and s replicated)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -787,8 +792,12 @@ def main():
     pkg.load_library()
 
     d_out, d_in, k = w["d_out"], w["d_in"], w["k"]
-    r0 = d_out * rank // world
-    r1 = d_out * (rank + 1) // world
+    if args.shard > 1:
+        assert world == 1, "--shard G times one rank's shard on one GPU"
+        r0, r1 = 0, d_out // args.shard
+    else:
+        r0 = d_out * rank // world
+        r1 = d_out * (rank + 1) // world
     rows = r1 - r0
     # ---- layer copies: working set per rank >= 4 x L2 (inputs larger than L2)
     per_layer = alg_bytes_per_rank(w, rows, batch, n)
@@ -802,6 +811,8 @@ def main():
                         device=local_rank)
         lay.load_blocks(0, signs, u_bf, v_bf, s)
         lay.set_num_blocks(n)
+        if args.kernel != "auto":
+            lay.set_kernel(args.kernel)
         layers.append(lay)
     x = torch.from_numpy(make_x(batch, channel_gains(d_in, 5), 6).astype(np.float32)).to(torch.bfloat16).cuda()
     y = torch.empty((batch, rows), dtype=torch.float32, device="cuda")
@@ -865,7 +876,8 @@ def main():
     step(0)
     per_step_launches = pkg.launch_count() - l0   # our kernels per bitstack_matmul call
     torch.cuda.synchronize()
-    decode_path = batch < 16   # bitstack_matmul AUTO: prefill path from 16 tokens (bf16 factors)
+    # bitstack_matmul AUTO: prefill path from 9 tokens (bf16 factors, shards of >= 128 rows)
+    decode_path = args.kernel in ("tc", "simt") or (args.kernel == "auto" and (batch <= 8 or rows < 128))
 
     sampler = ClockSampler(local_rank)
     with sampler:
@@ -893,7 +905,7 @@ def main():
         total_units = float(tb.item())
     value = total_units / (ms_step * 1e-3)
     kernel_ms = kms / max(nk, 1)
-    assert kernel_ms <= ms_step * 1.02 or world > 1, (kernel_ms, ms_step)   # a kernel cannot outlast its step
+    assert kernel_ms <= ms_step * (1.02 if use_graph else 1.1) or world > 1, (kernel_ms, ms_step)   # a kernel cannot outlast its step
     if decode_path:   # dominant kernel: the zq + decode PDL pair(s), algorithmic bytes
         dom_units = alg_bytes_per_rank(w, rows, batch, n) / 1e9
         nbk = min(batch, 8)
@@ -979,7 +991,7 @@ def main():
             lay.set_num_blocks(n)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.shard == 1:
         rows_s = 256
         dt, _ = oracle_sample_time(w, n, batch, rows_s, 1, 0, seed_for(2, 0, "blocks"))
         cpu = {"value": step_units(w, d_out, batch, n) / (dt * d_out / rows_s), "unit": unit_name(w),
@@ -1035,6 +1047,11 @@ def main():
             "gpu_launches": int(launches),
             "cpu_baseline": cpu,
         }
+        if args.shard > 1:
+            line["config"]["parallelism"] = f"rank 0 of a tp{args.shard} row split, timed alone on one GPU"
+            line["config"]["shard"] = {"of": args.shard, "rows": rows,
+                                       "hbm_floor_us": dom_units * 1e9 / (peak * 1e9) * 1e6,
+                                       "note": "value = this rank's units / its step time (no collective)"}
         if sweep:
             line["n_sweep"] = sweep
         if coll is not None:

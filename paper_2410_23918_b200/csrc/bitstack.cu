@@ -163,11 +163,11 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
   return BITSTACK_OK;
 }
 
-// e4m3 decode geometry per batch class: (R row tiles per CTA, TPW tiles per handshake)
-constexpr int64_t kPrefillMinBatch = 16;   // AUTO: restored-tile GEMM path from this batch on
+constexpr int64_t kPrefillMinBatch = 9;    // AUTO: restored-tile GEMM path from this batch on
 
 // AUTO takes the restored-tile GEMM (fp16 operands, ~3e-4 relative error) from kPrefillMinBatch
-// tokens on, for shards of at least one full 128-row tile; tiny shards stay on the decode path
+// tokens on -- past one MX decode pass (<= 8 tokens), where the decode's tensor work (48 Zq
+// columns per token) costs more than restoring W' (measured crossover) -- for shards of at least one full 128-row tile; tiny shards stay on the decode path
 // (one tile of GEMM work is not worth the restore, and y over a handful of rows is where the fp16
 // operand rounding shows most).
 bool prefill_auto(bitstack_layer L, int64_t batch) { return batch >= kPrefillMinBatch && L->rows_local >= 128; }
@@ -245,14 +245,27 @@ bs::ZqMxParams zq_mx_params(bitstack_layer L, const bs::DecodeParams& p) {
   return zp;
 }
 
+// Zq CTAs resident per SM (persistent grid = SMs x this), per batch class; the same on every
+// device of one architecture (the library is built for sm_100a only).
+template <int NB>
+std::atomic<int>& zq_occ() {
+  static std::atomic<int> occ{1};
+  return occ;
+}
+template <int NB>
+constexpr int zq_smem() { return 2 * bs::MxCfg<NB>::kUnit; }
+
 template <int NB>
 bitstack_status mx_attrs() {
   static std::atomic<unsigned long long> done{0};
   return once_per_device(done, [&]() -> bitstack_status {
     using C = bs::DecodeMxCfg<NB>;
-    constexpr int zs = bs::MxCfg<NB>::kUnit;
+    constexpr int zs = zq_smem<NB>();
     CK(cudaFuncSetAttribute(bs::zq_mx_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zs));
     CK(cudaFuncSetAttribute(bs::zq_mx_grouped_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, zs));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bs::zq_mx_grouped_kernel<NB>, bs::zq_threads<NB>(), zs));
+    zq_occ<NB>().store(occ > 0 ? occ : 1);
     CK(cudaFuncSetAttribute(bs::decode_mx_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes));
     CK(cudaFuncSetAttribute(bs::decode_mx_grouped_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             C::kSmemBytes));
@@ -282,7 +295,8 @@ bitstack_status launch_decode_mx(bitstack_layer L, const bs::DecodeParams& prm_i
   rs = ensure_zq_mx<NB>(L, st);
   if (rs) return rs;
   const int64_t units = (int64_t)prm_in.n * prm_in.nq;
-  bs::zq_mx_kernel<NB><<<(unsigned)units, bs::kZqThreads, bs::MxCfg<NB>::kUnit, st>>>(zq_mx_params(L, prm_in));
+  const int zgrid = (int)std::min<int64_t>(units, (int64_t)L->sm_count * zq_occ<NB>().load());
+  bs::zq_mx_kernel<NB><<<(unsigned)zgrid, bs::zq_threads<NB>(), zq_smem<NB>(), st>>>(zq_mx_params(L, prm_in), (int)units);
   count_launch();
   CK(cudaGetLastError());
   bs::DecodeParams prm = prm_in;
@@ -589,7 +603,8 @@ bitstack_status launch_grouped_mx(const bitstack_layer* layers, int count, const
   int slot = -1;
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
-  bs::zq_mx_grouped_kernel<NB><<<(unsigned)zg.unit_start[count], bs::kZqThreads, bs::MxCfg<NB>::kUnit, st>>>(zg);
+  const int zgrid = std::min(zg.unit_start[count], layers[0]->sm_count * zq_occ<NB>().load());
+  bs::zq_mx_grouped_kernel<NB><<<(unsigned)zgrid, bs::zq_threads<NB>(), zq_smem<NB>(), st>>>(zg);
   count_launch();
   CK(cudaGetLastError());
   cudaLaunchAttribute attr[1];

@@ -130,86 +130,163 @@ struct ZqMxParams {
   int kfuse;            // k > 16 at batch 1: token slot b = rank half b of block i (x row 0)
 };
 
-// 512 threads per unit: thread (rank group g = tid / 128, channel c = tid % 128) computes the 4
-// ranks 4g .. 4g+3 of channel c, so each warp is one 32-channel K-block of 4 ranks and the
-// per-thread dependency chain (3 digits x 4 ranks) is short: this kernel's latency sits on the
-// critical path of every call (the decode's MMAs wait for it).
-constexpr int kZqThreads = 512;
+// Persistent CTAs, one unit (block half i, 128-channel chunk q) at a time, 128 threads per token
+// group (ZqTG<NB> groups; group g computes tokens g, g + TG, ...).  Thread t of a group holds 4
+// consecutive channels 4 (t >> 2) .. +3 and the 4 ranks 4 (t & 3) .. +3, so warp w of a group is
+// one 32-channel K-block: the block maximum of a rank is a 4-way local max plus 3 xor-shuffles
+// over the 8 lanes of the same rank group, and each (rank, digit) is one 32-bit shared store (4
+// channels are contiguous in the UMMA B image).  Units alternate between two shared tiles, one
+// __syncthreads per unit; V' of the next unit is loaded before the current one is computed, and
+// the copy of the finished tile to global overlaps the next unit.
+template <int NB> struct ZqTG { static constexpr int value = NB >= 4 ? 4 : NB; };
+template <int NB> __host__ __device__ constexpr int zq_threads() { return 128 * ZqTG<NB>::value; }
+template <int NB> __host__ __device__ constexpr int zq_min_ctas() { return 1024 / zq_threads<NB>(); }   // <= 64 regs
 
-template <int NB>
-__device__ __forceinline__ void zq_mx_body(const ZqMxParams& p, const int unit) {
-  using C = MxCfg<NB>;
-  constexpr int N = C::N;
-  extern __shared__ __align__(128) uint8_t tile[];   // C::kUnit bytes (dynamic: > 48 KB at NB = 8)
-  asm volatile("griddepcontrol.launch_dependents;");
-  const int i = unit / p.nq, q = unit % p.nq;
-  const int tid = threadIdx.x, lane = tid & 31, c = tid & 127, kb = c >> 5, rg = tid >> 7;
-  const int col = q * kSubK + c;
+// V' of one unit for thread (rank group rg, channel quad): 4 channels x 4 ranks, raw 16-bit pairs.
+__device__ __forceinline__ void zq_load_v(const ZqMxParams& p, long long blk, int q, uint2 (&raw)[4]) {
+  const int t = threadIdx.x & 127;
   const long long dpad = (long long)p.nq * kSubK;
-  auto load_v4 = [&](long long blk, float (&vv)[4]) {   // ranks 4 rg .. 4 rg + 3 of V'[blk][col]
-    const uint2 raw = __ldg(reinterpret_cast<const uint2*>(
-        reinterpret_cast<const uint16_t*>(p.v) + ((blk * dpad + col) * 16 + 4 * rg)));
-    float2 f0, f1;
-    if (p.f_dtype == 1) {
-      f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-      f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-    } else {
-      f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-      f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-    }
-    vv[0] = f0.x; vv[1] = f0.y; vv[2] = f1.x; vv[3] = f1.y;
-  };
-  float vv[4];
-  if (!p.kfuse) load_v4(i, vv);
-  const float is = col < p.d_in ? __ldg(p.inv_s + col) : 0.f;
-  const int kc = (c >> 4) * (N / 8) * 128 + (c & 15);   // this channel's byte offset in the B image
-#pragma unroll 1
-  for (int b = 0; b < NB; ++b) {
-    if (p.kfuse) load_v4(2 * i + b, vv);
-    const bool on = p.kfuse || b < p.batch;
-    const long long xi = (long long)(p.kfuse ? 0 : b) * p.x_stride + col;
-    const float xs = (on && col < p.d_in) ? __fmul_rn(load_act(p.x, xi, p.x_dtype), is) : 0.f;
-    float val[4];
+  const int col0 = q * kSubK + 4 * (t >> 2);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) val[r] = __fmul_rn(vv[r], xs);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      uint32_t amax[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) amax[r] = __reduce_max_sync(0xffffffffu, __float_as_uint(val[r]) & 0x7fffffffu);
-      int my_sf = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int n = b * 48 + d * 16 + 4 * rg + r;
-        // branch-free: sigma puts the K-block maximum into [128, 256) (clamped: a K-block below
-        // 2^-106 keeps sigma = -113 and its tiny digits round to 0); a non-finite value stays
-        // non-finite (e4m3 NaN), so y is NaN as in the oracle
-        const int sig = min(max((int)(amax[r] >> 23) - 134, -113), 120);
-        const float scaled = __fmul_rn(val[r], pow2f(-sig));
-        const bool fin = fabsf(val[r]) <= 3.4028235e38f;
-        const uint8_t q8 = fin ? (uint8_t)__nv_cvt_float_to_fp8(scaled, __NV_SATFINITE, __NV_E4M3) : (uint8_t)0x7f;
-        const float back = __half2float(__half(__nv_cvt_fp8_to_halfraw(q8, __NV_E4M3)));
-        val[r] = fin ? __fmul_rn(__fsub_rn(scaled, back), pow2f(sig)) : val[r];   // exact residual
-        tile[kc + (n / 8) * 128 + (n % 8) * 16] = q8;
-        if (lane == r) my_sf = sig + 127;
-      }
-      if (lane < 4) {   // lane r writes the scale byte of column (b, d, 4 rg + r) for this K-block
-        const int n = b * 48 + d * 16 + 4 * rg + lane;
-        tile[C::kB + 512 * (n / 128) + 16 * (n & 31) + 4 * ((n & 127) >> 5) + kb] = (uint8_t)my_sf;
-      }
-    }
-  }
-  // SFB bytes of columns >= N in the last chunk: defined (never used by an MMA)
-  for (int e = N + tid; e < 128 * C::NCH; e += kZqThreads)
-    for (int k4 = 0; k4 < 4; ++k4) tile[C::kB + 512 * (e / 128) + 16 * (e & 31) + 4 * ((e & 127) >> 5) + k4] = 0;
-  __syncthreads();
-  uint4* dst = reinterpret_cast<uint4*>(p.zq + (long long)unit * C::kUnit);
-  for (int e = tid; e < C::kUnit / 16; e += kZqThreads) dst[e] = reinterpret_cast<const uint4*>(tile)[e];
+  for (int j = 0; j < 4; ++j)
+    raw[j] = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(p.v) +
+                                                  ((blk * dpad + col0 + j) * 16 + 4 * (t & 3))));
 }
 
 template <int NB>
-__global__ void __launch_bounds__(kZqThreads) zq_mx_kernel(const ZqMxParams p) {
-  zq_mx_body<NB>(p, (int)blockIdx.x);
+__device__ __forceinline__ void zq_mx_unit(const ZqMxParams& p, const int unit, uint8_t* tile, const uint2 (&raw0)[4]) {
+  using C = MxCfg<NB>;
+  constexpr int N = C::N, TG = ZqTG<NB>::value;
+  const int i = unit / p.nq, q = unit % p.nq;
+  const int t = threadIdx.x & 127, tg = threadIdx.x >> 7;
+  const int lane = t & 31, rg = t & 3, cq = t >> 2, kb = cq >> 3;
+  const int c0 = 4 * cq, col0 = q * kSubK + c0;
+  float vv[4][4];   // [channel j][rank 4 rg + r]
+  auto unpack = [&](const uint2 (&raw)[4]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f0, f1;
+      if (p.f_dtype == 1) {
+        f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[j].x));
+        f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw[j].y));
+      } else {
+        f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw[j].x));
+        f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw[j].y));
+      }
+      vv[j][0] = f0.x; vv[j][1] = f0.y; vv[j][2] = f1.x; vv[j][3] = f1.y;
+    }
+  };
+  if (!p.kfuse) unpack(raw0);
+  float is[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) is[j] = col0 + j < p.d_in ? __ldg(p.inv_s + col0 + j) : 0.f;
+  const int kc = (c0 >> 4) * (N / 8) * 128 + (c0 & 15);   // byte offset of channel c0 in the B image
+#pragma unroll 1
+  for (int b = tg; b < NB; b += TG) {
+    if (p.kfuse) {
+      uint2 raw[4];
+      zq_load_v(p, 2 * i + b, q, raw);
+      unpack(raw);
+    }
+    const bool on = p.kfuse || b < p.batch;
+    const long long xrow = (long long)(p.kfuse ? 0 : b) * p.x_stride;
+    float xs[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      xs[j] = (on && col0 + j < p.d_in) ? __fmul_rn(load_act(p.x, xrow + col0 + j, p.x_dtype), is[j]) : 0.f;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      // digit 0 scale: sigma puts the K-block maximum of V'[:, r] x' into [128, 256) (clamped: a
+      // K-block below 2^-106 keeps sigma = -113 and its tiny digits round to 0); digit d scales
+      // by 2^(sigma - 4d): the previous digit's residual is at most half an e4m3 ulp (<= 8, then
+      // <= 4, in its own units), so x16 keeps it inside e4m3 range.  A non-finite value becomes
+      // NaN (e4m3 0x7f in every digit), so y is NaN as in the oracle.
+      float val[4];
+      uint32_t m = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        val[j] = __fmul_rn(vv[j][r], xs[j]);
+        m = max(m, __float_as_uint(val[j]) & 0x7fffffffu);
+      }
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 8));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 16));
+      const int sig = min(max((int)(m >> 23) - 134, -113), 120);
+      const float sc = pow2f(-sig);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        val[j] = fabsf(val[j]) <= 3.4028235e38f ? __fmul_rn(val[j], sc) : __uint_as_float(0x7fffffffu);
+      const int n0 = b * 48 + 4 * rg + r;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const __nv_fp8x2_storage_t q01 =
+            __nv_cvt_float2_to_fp8x2(make_float2(val[0], val[1]), __NV_SATFINITE, __NV_E4M3);
+        const __nv_fp8x2_storage_t q23 =
+            __nv_cvt_float2_to_fp8x2(make_float2(val[2], val[3]), __NV_SATFINITE, __NV_E4M3);
+        const int n = n0 + 16 * d;
+        *reinterpret_cast<uint32_t*>(tile + kc + (n / 8) * 128 + (n % 8) * 16) =
+            (uint32_t)q01 | ((uint32_t)q23 << 16);
+        if (d < 2) {   // exact: the residual of a 4-significant-bit rounding, times 16
+          const float2 b01 = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2(q01, __NV_E4M3)));
+          const float2 b23 = __half22float2(__half2(__nv_cvt_fp8x2_to_halfraw2(q23, __NV_E4M3)));
+          val[0] = __fmul_rn(__fsub_rn(val[0], b01.x), 16.f);
+          val[1] = __fmul_rn(__fsub_rn(val[1], b01.y), 16.f);
+          val[2] = __fmul_rn(__fsub_rn(val[2], b23.x), 16.f);
+          val[3] = __fmul_rn(__fsub_rn(val[3], b23.y), 16.f);
+        }
+        if (lane < 4)   // lanes 0..3 (rank groups 0..3 of channel quad 0): this K-block's scale bytes
+          tile[C::kB + 512 * (n / 128) + 16 * (n & 31) + 4 * ((n & 127) >> 5) + kb] = (uint8_t)(sig + 127 - 4 * d);
+      }
+    }
+  }
+}
+
+// Units [0, units) of one layer (or of a group: `locate` maps a global unit to its parameters).
+template <int NB, typename Locate>
+__device__ __forceinline__ void zq_mx_loop(const int units, Locate locate) {
+  using C = MxCfg<NB>;
+  constexpr int N = C::N, NT = zq_threads<NB>();
+  extern __shared__ __align__(128) uint8_t zq_tiles[];   // 2 x C::kUnit bytes
+  asm volatile("griddepcontrol.launch_dependents;");
+  // SFB bytes of columns >= N in the last chunk: defined (never used by an MMA), written once
+  for (int t = 0; t < 2; ++t)
+    for (int e = N + (int)threadIdx.x; e < 128 * C::NCH; e += NT)
+      for (int k4 = 0; k4 < 4; ++k4)
+        zq_tiles[t * C::kUnit + C::kB + 512 * (e / 128) + 16 * (e & 31) + 4 * ((e & 127) >> 5) + k4] = 0;
+  int u = blockIdx.x;
+  if (u >= units) return;
+  const ZqMxParams* p;
+  int lu;
+  locate(u, p, lu);
+  uint2 raw[4];
+  if (!p->kfuse) zq_load_v(*p, lu / p->nq, lu % p->nq, raw);
+#pragma unroll 1
+  for (int it = 0;; ++it) {
+    const int un = u + gridDim.x;
+    const ZqMxParams* pn = p;
+    int lun = 0;
+    uint2 rawn[4];
+    if (un < units) {   // next unit's V' in flight while this one is computed
+      locate(un, pn, lun);
+      if (!pn->kfuse) zq_load_v(*pn, lun / pn->nq, lun % pn->nq, rawn);
+    }
+    uint8_t* tile = zq_tiles + (it & 1) * C::kUnit;
+    zq_mx_unit<NB>(*p, lu, tile, raw);
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(p->zq + (long long)lu * C::kUnit);
+    for (int e = threadIdx.x; e < C::kUnit / 16; e += NT) dst[e] = reinterpret_cast<const uint4*>(tile)[e];
+    if (un >= units) break;
+    u = un;
+    p = pn;
+    lu = lun;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) raw[j] = rawn[j];
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(zq_threads<NB>(), zq_min_ctas<NB>()) zq_mx_kernel(const __grid_constant__ ZqMxParams p, const int units) {
+  zq_mx_loop<NB>(units, [&](int u, const ZqMxParams*& pp, int& lu) { pp = &p; lu = u; });
 }
 
 constexpr int kMaxMxGroup = 8;
@@ -219,10 +296,13 @@ struct ZqMxGroup {
   ZqMxParams prm[kMaxMxGroup];
 };
 template <int NB>
-__global__ void __launch_bounds__(kZqThreads) zq_mx_grouped_kernel(const __grid_constant__ ZqMxGroup grp) {
-  int i = 0;
-  while (i + 1 < grp.count && (int)blockIdx.x >= grp.unit_start[i + 1]) ++i;
-  zq_mx_body<NB>(grp.prm[i], (int)blockIdx.x - grp.unit_start[i]);
+__global__ void __launch_bounds__(zq_threads<NB>(), zq_min_ctas<NB>()) zq_mx_grouped_kernel(const __grid_constant__ ZqMxGroup grp) {
+  zq_mx_loop<NB>(grp.unit_start[grp.count], [&](int u, const ZqMxParams*& pp, int& lu) {
+    int i = 0;
+    while (i + 1 < grp.count && u >= grp.unit_start[i + 1]) ++i;
+    pp = &grp.prm[i];
+    lu = u - grp.unit_start[i];
+  });
 }
 
 // ------------------------------------------------------------------ decode kernel (H4-H7)
@@ -285,7 +365,10 @@ struct DecodeMxCfg {
   // TMEM columns: A slots [slot][tile] (32 each) | accumulators [t] (N each) | SFA (4) | SFB [i][slot]
   static constexpr int kSfCols = 4 * Z::NCH;
   static constexpr int NS0 = (kTmemCols - R * N - 4) / (R * 32 + NI * kSfCols);
-  static constexpr int NSLOT = NS0 > 4 ? 4 : NS0;
+#ifndef BS_MX_NSLOT
+#define BS_MX_NSLOT 4
+#endif
+  static constexpr int NSLOT = NS0 > BS_MX_NSLOT ? BS_MX_NSLOT : NS0;
   static constexpr uint32_t kColAcc = NSLOT * R * 32;
   static constexpr uint32_t kColSfa = kColAcc + R * N;
   static constexpr uint32_t kColSfb = kColSfa + 4;

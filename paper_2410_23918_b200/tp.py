@@ -26,6 +26,10 @@ def gather_rows(y_local: torch.Tensor, d_out: int, group=None) -> torch.Tensor:
     Shards may differ by one row: each rank pads to the largest shard, the padded
     [G, B, r_max] gather is reordered into [B, d_out] by copying each rank's rows."""
     world = dist.get_world_size(group)
+    if y_local.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo has no device all-gather: stage through host memory (used by the CPU-plumbed
+        # multi-process tests of the real library; NCCL moves device buffers directly)
+        return gather_rows(y_local.cpu(), d_out, group).to(y_local.device)
     batch = y_local.shape[0]
     r_max = -(-d_out // world)
     if y_local.shape[1] < r_max:

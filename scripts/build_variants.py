@@ -12,6 +12,10 @@ VARIANTS = {
     "occ2": ["-DBS_MX_R1=2", "-DBS_MX_OCC1=2"],
     "occ2r1": ["-DBS_MX_R1=1", "-DBS_MX_OCC1=2"],
     "occ2skel": ["-DBS_MX_R1=2", "-DBS_MX_OCC1=2", "-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
+    "r2s6": ["-DBS_MX_R1=2", "-DBS_MX_NSLOT=6"],
+    "r1s8": ["-DBS_MX_R1=1", "-DBS_MX_NSLOT=8"],
+    "r1s12": ["-DBS_MX_R1=1", "-DBS_MX_NSLOT=12"],
+    "r2s4": ["-DBS_MX_R1=2"],
     "skel": ["-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
 }
 if __name__ == "__main__":

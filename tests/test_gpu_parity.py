@@ -531,7 +531,8 @@ def test_grouped_matches_individual_and_oracle(bs, batch):
     c0 = bs.launch_count()
     ys = bs.matmul_grouped(lays, xs)
     torch.cuda.synchronize()
-    assert bs.launch_count() - c0 == 2 * ((batch + 7) // 8)   # zq_mx_grouped + decode_mx_grouped per 8 tokens
+    if batch <= 8:   # one zq_mx_grouped + decode_mx_grouped pair; from 9 tokens each member's own path
+        assert bs.launch_count() - c0 == 2
     for (g, s32, blocks, lay), n, x, y in zip(case, levels, xs, ys):
         y1 = lay.matmul(x)
         torch.cuda.synchronize()
@@ -635,7 +636,7 @@ def test_prefill_parity_ragged(bs, shape):
 
 
 def test_prefill_dtypes_auto_and_unsupported(bs):
-    """AUTO picks the prefill path from batch 16 on (same y as forcing it); f32/bf16/f16
+    """AUTO picks the prefill path from batch 9 on (same y as forcing it); f32/bf16/f16
     activations; bf16 y (4e-3); fp32 factors refuse a forced prefill (E_UNSUPPORTED)."""
     g, s32, blocks = compress_case(256, 384, 4, "bf16", 71)
     lay = make_layer(bs, 256, 384, blocks, s32, "bf16")
