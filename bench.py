@@ -724,7 +724,7 @@ def main():
     ap.add_argument("--order", choices=["average", "random"], default="average",
                     help="c4: the universal stack's sorting (P:351); Greedy needs measured perplexities")
     ap.add_argument("--sweep", action="store_true", help="also report us/layer for n = 1, 2, 4, 8, 16")
-    ap.add_argument("--kernel", choices=["auto", "tc", "prefill", "simt"], default="auto",
+    ap.add_argument("--kernel", choices=["auto", "tc", "prefill", "rgemv", "simt"], default="auto",
                     help="decode workloads: force one path (bitstack_set_kernel) for crossover sweeps")
     ap.add_argument("--shard", type=int, default=1,
                     help="decode, one GPU: time rank 0's row shard of a G-way row split (the per-rank "
@@ -876,8 +876,13 @@ def main():
     step(0)
     per_step_launches = pkg.launch_count() - l0   # our kernels per bitstack_matmul call
     torch.cuda.synchronize()
-    # bitstack_matmul AUTO: prefill path from 9 tokens (bf16 factors, shards of >= 128 rows)
-    decode_path = args.kernel in ("tc", "simt") or (args.kernel == "auto" and (batch <= 8 or rows < 128))
+    # bitstack_matmul AUTO with bf16 factors (csrc/bitstack.cu choose_path): the e4m3 decode up to
+    # 8 tokens, the prefill GEMM above (shards of >= 128 rows); --kernel rgemv forces restore-and-multiply
+    if args.kernel == "auto":
+        path = "decode" if (batch <= 8 or rows < 128) else "prefill"
+    else:
+        path = {"tc": "decode", "simt": "decode"}.get(args.kernel, args.kernel)
+    decode_path = path == "decode"
 
     sampler = ClockSampler(local_rank)
     with sampler:
@@ -905,17 +910,26 @@ def main():
         total_units = float(tb.item())
     value = total_units / (ms_step * 1e-3)
     kernel_ms = kms / max(nk, 1)
-    assert kernel_ms <= ms_step * (1.02 if use_graph else 1.1) or world > 1, (kernel_ms, ms_step)   # a kernel cannot outlast its step
+    assert kernel_ms <= ms_step * (1.02 if use_graph and decode_path else 1.1) or world > 1, (kernel_ms, ms_step)   # a kernel cannot outlast its step
     if decode_path:   # dominant kernel: the zq + decode PDL pair(s), algorithmic bytes
         dom_units = alg_bytes_per_rank(w, rows, batch, n) / 1e9
         nbk = min(batch, 8)
         dom_name = "bs::zq_mx_kernel<%d> + bs::decode_mx_kernel<%d> (PDL pair%s)" % (
             nbk, nbk, "" if batch <= 8 else ", %d pairs per call" % ((batch + 7) // 8))
+    elif path == "rgemv":   # dominant kernel: the restore, 2.5 issued lane-instructions per element and block
+        dom_units = 2.5 * n * rows * d_in / 1e12
+        dom_name = "bs::rgemv_kernel<%d> (restore-and-multiply)" % (16 if batch <= 16 else 32)
     else:             # dominant kernel: the GEMM, 2 B r d_in flops
         dom_units = 2.0 * batch * rows * d_in / 1e12
         dom_name = "bs::prefill_gemm_kernel<BN> (BN = 128 or 256 by wave fill)"
     achieved = dom_units / (kernel_ms * 1e-3)
-    peak, peak_src = peaks("decode" if decode_path else "prefill")
+    if path == "rgemv":
+        # issue roofline: 4 SMSPs x 32 lanes x one instruction per clock per SM at the max SM clock
+        mhz = float((clocks or {}).get("sm_max_mhz") or 1965.0)
+        sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+        peak, peak_src = sms * 128 * mhz * 1e6 / 1e12, "derived: SMs x 128 lane-instr/clk x max SM clock (B300_MICROARCH.md pipe rates)"
+    else:
+        peak, peak_src = peaks("decode" if decode_path else "prefill")
     traffic = traffic_key(f"{args.workload}_n{n}_b{batch}_g{world}")
 
     # ---- e2e: public API with host buffers (pinned), copies inside the timed region
@@ -1033,14 +1047,12 @@ def main():
                        "l2": f"inputs larger than L2: rotation over {copies} layer copies "
                              f"({copies * per_layer / 2 ** 20:.0f} MiB/rank > 4x126 MiB)",
                        "timing": "CUDA-graph replay" if use_graph else "eager launches"},
-            "roofline": {"bound": "hbm" if decode_path else "tensor", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s" if decode_path else "TFLOP/s",
+            "roofline": {"bound": {"decode": "hbm", "rgemv": "alu", "prefill": "tensor"}[path], "achieved": achieved,
+                         "peak": peak, "unit": {"decode": "GB/s", "rgemv": "Tlane-instr/s", "prefill": "TFLOP/s"}[path],
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         ("frac_of_spec_8000_gbs" if decode_path else "frac_of_nominal_2250_tflops"):
-                             achieved / (8000.0 if decode_path else 2250.0),
                          "kernel": dom_name, "kernel_us": kernel_ms * 1e3,
                          "kernel_launches_timed": nk,
-                         ("bytes_per_launch" if decode_path else "flops_per_launch"):
+                         {"decode": "bytes_per_launch", "rgemv": "lane_instr_per_launch", "prefill": "flops_per_launch"}[path]:
                              dom_units * (1e9 if decode_path else 1e12)},
             "clocks": clocks,
             "e2e": e2e,

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BITSTACK_LIB", os.path.join(HERE, "libbitstack.so"))
 
 F32, BF16, F16 = 0, 1, 2
-KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT, KERNEL_PREFILL = 0, 1, 2, 3
+KERNEL_AUTO, KERNEL_TC, KERNEL_SIMT, KERNEL_PREFILL, KERNEL_RGEMV = 0, 1, 2, 3, 4
 _DTYPE_NAMES = {"f32": F32, "float32": F32, "bf16": BF16, "bfloat16": BF16, "f16": F16, "float16": F16}
 
 STATUS = {
@@ -230,7 +230,7 @@ class Layer:
 
     def set_kernel(self, kernel) -> None:
         code = {"auto": KERNEL_AUTO, "tc": KERNEL_TC, "simt": KERNEL_SIMT,
-                "prefill": KERNEL_PREFILL}.get(kernel, kernel)
+                "prefill": KERNEL_PREFILL, "rgemv": KERNEL_RGEMV}.get(kernel, kernel)
         _check(_lib.bitstack_set_kernel(self._h, int(code)))
 
     def info(self) -> dict:

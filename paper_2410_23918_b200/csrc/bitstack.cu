@@ -22,6 +22,7 @@
 #include "decode_mx.cuh"
 #include "decode_tc.cuh"
 #include "prefill.cuh"
+#include "rgemv.cuh"
 
 struct bitstack_layer_s {
   int64_t d_out = 0, d_in = 0, row_begin = 0, row_end = 0, rows_local = 0;
@@ -53,6 +54,9 @@ struct bitstack_layer_s {
   uint8_t* pf_w = nullptr; // prefill path: W' operand image (transient workspace, grown on demand)
   uint8_t* pf_x = nullptr; // prefill path: X' operand image
   int64_t pf_w_bytes = 0, pf_x_bytes = 0;
+  uint8_t* rg_x = nullptr;     // restore-and-multiply path: X' unit images (grown on demand)
+  uint8_t* rg_part = nullptr;  // restore-and-multiply path: per-CTA partial y slots
+  int64_t rg_x_bytes = 0, rg_part_bytes = 0;
   uint8_t* stage_x = nullptr;  // host-buffer calls: device staging of x / y (grown on demand)
   uint8_t* stage_y = nullptr;
   int64_t stage_x_bytes = 0, stage_y_bytes = 0;
@@ -171,6 +175,19 @@ constexpr int64_t kPrefillMinBatch = 9;    // AUTO: restored-tile GEMM path from
 // (one tile of GEMM work is not worth the restore, and y over a handful of rows is where the fp16
 // operand rounding shows most).
 bool prefill_auto(bitstack_layer L, int64_t batch) { return batch >= kPrefillMinBatch && L->rows_local >= 128; }
+
+// The restore-and-multiply path (rgemv.cuh) is selected explicitly (BITSTACK_KERNEL_RGEMV): it
+// measured between the decode and the prefill paths, so AUTO keeps the e4m3
+// decode up to 8 tokens and the restored-tile GEMM above.
+enum MatmulPath { kPathDecode, kPathRgemv, kPathPrefill };
+MatmulPath choose_path(bitstack_layer L, int64_t batch) {
+  const bool fp16ok = L->dev_fdt != 0 && L->layout == 1;
+  if (L->kernel == BITSTACK_KERNEL_PREFILL) return kPathPrefill;
+  if (L->kernel == BITSTACK_KERNEL_RGEMV) return kPathRgemv;
+  if (L->kernel != BITSTACK_KERNEL_AUTO || !fp16ok) return kPathDecode;
+  if (L->n_act * L->kh <= 16 && prefill_auto(L, batch)) return kPathPrefill;
+  return kPathDecode;
+}
 
 // A handle's workspaces (Zq units, split-K slots and counters, staging, prefill images) are
 // reused by every call.  Calls on one stream are ordered by the stream; when a call arrives on a
@@ -471,6 +488,64 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   return record_prof(st, false, &slot);
 }
 
+// Restore-and-multiply path (rgemv.cuh): X' images, then one kernel; 2 launches on `st`.
+template <int BP>
+bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
+                                cudaStream_t st) {
+  using C = bs::RgCfg<BP>;
+  static std::atomic<unsigned long long> attr_done{0};
+  bitstack_status rs = once_per_device(attr_done, [&]() -> bitstack_status {
+    CK(cudaFuncSetAttribute(bs::rgemv_kernel<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    return BITSTACK_OK;
+  });
+  if (rs) return rs;
+  // CTAs: each row tile split into `splits` contiguous unit ranges so that the grid fills the SMs
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(L->sm_count / std::max(1, L->row_tiles), L->nq));
+  const int grid = L->row_tiles * splits;
+  rs = grow(L, &L->rg_x, &L->rg_x_bytes, (int64_t)L->nq * C::kXImg, st);
+  if (rs) return rs;
+  rs = grow(L, &L->rg_part, &L->rg_part_bytes, (int64_t)grid * BP * 128 * 4, st);
+  if (rs) return rs;
+  const long long pieces = (long long)L->nq * BP * 32;
+  const int xgrid = (int)std::min<long long>((pieces + 255) / 256, (long long)L->sm_count * 8);
+  bs::rg_xprep_kernel<<<xgrid, 256, 0, st>>>(x, xdt, L->d_in, L->inv_s, (int)batch, (int)L->d_in, L->nq, BP,
+                                            reinterpret_cast<uint4*>(L->rg_x));
+  count_launch();
+  CK(cudaGetLastError());
+  bs::RgParams rp;
+  rp.signs = L->signs;
+  rp.u = reinterpret_cast<const uint16_t*>(L->u);
+  rp.v = reinterpret_cast<const uint16_t*>(L->v);
+  rp.ximg = L->rg_x;
+  rp.part = reinterpret_cast<float*>(L->rg_part);
+  rp.counters = L->counters;
+  rp.y = y;
+  rp.y_stride = L->rows_local;
+  rp.y_dtype = ydt;
+  rp.n = L->n_act * L->kh;
+  rp.ksh = L->kh == 2 ? 1 : 0;
+  rp.nq = L->nq;
+  rp.rows_pad = L->rows_pad;
+  rp.rows_local = (int)L->rows_local;
+  rp.row_tiles = L->row_tiles;
+  rp.splits = splits;
+  rp.batch = (int)batch;
+  rp.f16 = L->dev_fdt == 2 ? 1 : 0;
+  int slot = -1;   // measurement hooks bracket the dominant kernel
+  bitstack_status ps = record_prof(st, true, &slot);
+  if (ps) return ps;
+  bs::rgemv_kernel<BP><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  count_launch();
+  CK(cudaGetLastError());
+  return record_prof(st, false, &slot);
+}
+
+bitstack_status launch_rgemv(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
+                             cudaStream_t st) {
+  if (batch <= 16) return launch_rgemv_bp<16>(L, x, xdt, y, ydt, batch, st);
+  return launch_rgemv_bp<32>(L, x, xdt, y, ydt, batch, st);
+}
+
 bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
                                cudaStream_t st) {
   int bn = 256, mh = 2;
@@ -769,6 +844,8 @@ bitstack_status bitstack_destroy(bitstack_layer L) {
   cudaFree(L->pf_x);
   cudaFree(L->stage_x);
   cudaFree(L->stage_y);
+  cudaFree(L->rg_x);
+  cudaFree(L->rg_part);
   delete L;
   return BITSTACK_OK;
 }
@@ -793,7 +870,7 @@ bitstack_status bitstack_get_info(bitstack_layer L, bitstack_info* out) {
 bitstack_status bitstack_set_kernel(bitstack_layer L, bitstack_kernel kernel) {
   if (!L) return fail(BITSTACK_E_INVALID_ARG, "NULL layer");
   if (kernel != BITSTACK_KERNEL_AUTO && kernel != BITSTACK_KERNEL_TC && kernel != BITSTACK_KERNEL_SIMT &&
-      kernel != BITSTACK_KERNEL_PREFILL)
+      kernel != BITSTACK_KERNEL_PREFILL && kernel != BITSTACK_KERNEL_RGEMV)
     return fail(BITSTACK_E_INVALID_ARG, "bad kernel selector %d", (int)kernel);
   L->kernel = kernel;
   return BITSTACK_OK;
@@ -1044,12 +1121,20 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
   const int xdt = x_dtype == BITSTACK_F32 ? 0 : (x_dtype == BITSTACK_BF16 ? 1 : 2);
   const int ydt = y_dtype == BITSTACK_F32 ? 0 : 1;
   const int xsz = dsize(x_dtype);
-  // large batch: restored-tile GEMM path (bf16 factors); forced with BITSTACK_KERNEL_PREFILL
-  const bool pf_ok = L->dev_fdt != 0 && L->layout == 1 && L->n_act * L->kh <= 16;
-  if (L->kernel == BITSTACK_KERNEL_PREFILL && !pf_ok)
-    return fail(BITSTACK_E_UNSUPPORTED, "prefill path needs bf16 factors and n <= 16");
-  if (L->kernel == BITSTACK_KERNEL_PREFILL || (L->kernel == BITSTACK_KERNEL_AUTO && pf_ok && prefill_auto(L, batch)))
+  // small / large batches with 16-bit factors: restore-and-multiply or restored-tile GEMM
+  // (forced with BITSTACK_KERNEL_RGEMV / BITSTACK_KERNEL_PREFILL)
+  const MatmulPath path = choose_path(L, batch);
+  const bool fp16ok = L->dev_fdt != 0 && L->layout == 1;
+  if (path == kPathPrefill) {
+    if (!fp16ok || L->n_act * L->kh > 16)
+      return fail(BITSTACK_E_UNSUPPORTED, "prefill path needs bf16 / f16 factors and n <= 16");
     return launch_prefill(L, x, xdt, y, ydt, batch, st);
+  }
+  if (path == kPathRgemv) {
+    if (!fp16ok || batch > bs::kRgMaxBatch)
+      return fail(BITSTACK_E_UNSUPPORTED, "restore-and-multiply path needs bf16 / f16 factors and batch <= 32");
+    return launch_rgemv(L, x, xdt, y, ydt, batch, st);
+  }
 
   // tcgen05 path: k <= 16 (zero-padded columns of U', V'), x rows bulk-copied by the
   // TMA engine -> 16-byte aligned x and d_in % 8 == 0.
@@ -1152,9 +1237,7 @@ bitstack_status bitstack_matmul(bitstack_layer L, const void* x, bitstack_dtype 
   // and write y with plain loads / stores (e4m3 decode, SIMT) are used in place: the transfer
   // is the kernels' own PCIe traffic.  Everything else is staged through device memory with
   // cudaMemcpyAsync on `stream` (synchronous with respect to pageable host memory).
-  const bool pf = L->kernel == BITSTACK_KERNEL_PREFILL ||
-                  (L->kernel == BITSTACK_KERNEL_AUTO && L->dev_fdt != 0 && L->layout == 1 && L->n_act * L->kh <= 16 &&
-                   prefill_auto(L, batch));
+  const bool pf = choose_path(L, batch) == kPathPrefill;
   const bool plain_io = !pf && (L->layout == 1 || L->kernel == BITSTACK_KERNEL_SIMT) && L->n_act > 0;
   const bool small = xbytes <= (1 << 20) && ybytes <= (1 << 20);
   const void* xd = x;

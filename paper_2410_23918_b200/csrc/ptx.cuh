@@ -52,6 +52,27 @@ __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
 }
+// Wait with a suspend-time hint: a warp whose phase is not complete is parked by the hardware
+// until the phase completes (or the hint expires) instead of re-issuing try_wait, so long waits
+// do not take issue slots from the working warps of the SMSP.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ void mbar_wait_sleep_slow(uint64_t* bar, uint32_t parity) {
+  uint32_t spins = 0;
+  while (!mbar_try_wait_sleep(bar, parity)) {
+    if (++spins > BS_WATCHDOG_SPINS) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  if (!mbar_try_wait(bar, parity)) mbar_wait_sleep_slow(bar, parity);
+}
 // Warp-collective variants: ONE lane touches the barrier (an mbarrier operation issued by all 32
 // lanes costs the SM's shared synchronisation unit up to 32 requests), the result is broadcast.
 __device__ __forceinline__ bool mbar_try_wait_warp(uint64_t* bar, uint32_t parity) {

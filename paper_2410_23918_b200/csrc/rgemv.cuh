@@ -1,0 +1,376 @@
+// Restore-and-multiply path for small batches (2 < B <= 32): y = W_hat_n x with the restored
+// weight never leaving the SM (VERDICT r1 "prefill without the W' round trip").
+//
+//     W'[j, c] = sum_{i<n} S_i[j, c] (U'_i V'_i^T)[j, c]      (Eq.5, Eq.8)
+//     y[b, j]  = sum_c W'[j, c] X'[b, c],  X' = x diag(1/s)   (Eq.4)
+//
+// The e4m3 decode pays 48 Zq columns of tensor work per token and sign element, so from a few
+// tokens on its tensor time exceeds the cost of restoring W' (2.5 ALU ops per element and block
+// plus a K = 16 MMA); the prefill path restores W' once but writes and re-reads it through HBM
+// as an fp16 operand and pads the GEMM to 128 tokens.  Here each CTA owns one 128-row tile and a
+// contiguous range of 128-column units and, per (unit, block):
+//   producer warp   cp.async of the U'_i tile and the V'_i chunk (16-byte pieces into the UMMA
+//                   K-major core layout), one bulk copy of the 128 x 128 sign tile; stage ring
+//   MMA warp        P_i = U'_i V'_i^T (tcgen05 kind::f16, M128 N128 K16: exact products, fp32
+//                   TMEM, triple-buffered); per unit, after its restore: y_acc += W' X'^T
+//                   (kind::tf32, 16 x K8 MMAs, A = W' from SMEM, B = the unit's X' image)
+//   16 restore warps  (lane quadrant, 32-column quarter): tcgen05.ld P_i, apply the signs (SHF +
+//                   LOP3 per element) and sum the blocks in fp32 (FADD2); at the unit's last
+//                   block round W' to tf32 (RNA) into the SMEM A image
+// then y_acc (TMEM, fp32) -> per-CTA partial slots -> the row tile's last CTA sums the slots in
+// order (deterministic) and writes y.  Numerics: W' and X' rounded once to tf32 (10 explicit
+// mantissa bits, fp32 range: no operand scaling), fp32 accumulation.
+#pragma once
+#include "decode_tc.cuh"
+
+namespace bs {
+
+struct RgParams {
+  const uint4* signs;     // [n_cap][nq][rows_pad] F8 layout
+  const uint16_t* u;      // [n x kh][rows_pad][16] U' (bf16 / f16 storage)
+  const uint16_t* v;      // [n x kh][d_in_pad][16] V'
+  const uint8_t* ximg;    // [nq] X' images of BP x 128 tf32 (rg_xprep_kernel)
+  float* part;            // [grid][BP][128] fp32 partial y of each CTA
+  int* counters;          // [row_tiles], zero on entry and on exit
+  void* y;
+  long long y_stride;
+  int y_dtype;            // 0 f32, 1 bf16
+  int n;                  // active 16-rank blocks (halves)
+  int ksh;                // sign tile of block i is i >> ksh
+  int nq, rows_pad, rows_local, row_tiles, splits, batch, f16;
+};
+
+constexpr int kRgStages = 10;
+constexpr int kRgPBuf = 3;                      // TMEM P buffers (128 columns each)
+#ifndef BS_RG_COLS
+#define BS_RG_COLS 64
+#endif
+constexpr int kRgCols = BS_RG_COLS;             // columns of a unit per restore warp (32 or 64)
+constexpr int kRgNR = 4 * (128 / kRgCols);      // restore warps (4 lane quadrants x column groups)
+constexpr int kRgWarpMma = kRgNR, kRgWarpProd = kRgNR + 1;
+constexpr int kRgWarps = kRgNR + 2;             // restore warps + MMA + producer
+constexpr int kRgMaxBatch = 32;
+constexpr int kRgStage = 4096 + 4096 + 2048;    // U' tile, V' chunk, sign tile
+constexpr int kRgAImg = 128 * 128 * 4;          // W' unit, tf32
+template <int BP> struct RgCfg {
+  static constexpr int kXImg = BP * 128 * 4;    // X' unit, tf32
+  static constexpr int kBarOff = kRgStages * kRgStage + kRgAImg + 2 * kXImg;
+  static constexpr int kSmem = kBarOff + 512 + 1024;   // barriers + alignment slack
+};
+
+// X' = x / s per (unit q, token t < BP, channel k < 128), tf32 (RNA) in the UMMA K-major image:
+// (t, k) at ((t / 8) 32 + k / 4) 128 + (t % 8) 16 + (k % 4) 4.  Tokens >= batch and channels >=
+// d_in are zero.  One thread per 16-byte core row (4 channels of one token).
+__global__ void __launch_bounds__(256) rg_xprep_kernel(const void* __restrict__ x, int x_dtype, long long x_stride,
+                                                      const float* __restrict__ inv_s, int batch, int d_in, int nq,
+                                                      int bp, uint4* __restrict__ img) {
+  const long long pieces = (long long)nq * bp * 32;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < pieces;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int q = (int)(e / (bp * 32));
+    const int rem = (int)(e % (bp * 32));
+    const int t = rem / 32, k4 = rem % 32;
+    uint32_t o[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int c = q * 128 + k4 * 4 + m;
+      float v = 0.f;
+      if (t < batch && c < d_in) v = load_act(x, (long long)t * x_stride + c, x_dtype) * __ldg(inv_s + c);
+      uint32_t r;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+      o[m] = r;
+    }
+    const long long off = (long long)q * bp * 128 * 4 + ((t / 8) * 32 + k4) * 128 + (t % 8) * 16;
+    img[off / 16] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int BP>
+__global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams p) {
+  using C = RgCfg<BP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* stages = smem;                                   // [kRgStages][U' 4K | V' 4K | signs 2K]
+  uint8_t* aimg = smem + kRgStages * kRgStage;              // W' unit (tf32 A image)
+  uint8_t* ximg = aimg + kRgAImg;                           // [2] X' units
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* full = bars;                      // [S] 32 producer lanes (after their cp.async) + 1 sign tx
+  uint64_t* sempty = full + kRgStages;        // [S] MMA commit + the restore warps (signs read)
+  uint64_t* pfull = sempty + kRgStages;       // [3] commit of P_i
+  uint64_t* pempty = pfull + kRgPBuf;         // [3] the restore warps (after a named barrier)
+  uint64_t* afull = pempty + kRgPBuf;         // 16 restore warps wrote the W' unit
+  uint64_t* aempty = afull + 1;               // commit of the unit's GEMV MMAs
+  uint64_t* xfull = aempty + 1;               // [2] bulk copy of an X' unit
+  uint64_t* xempty = xfull + 2;               // [2] commit of the GEMV that read it
+  uint64_t* yfull = xempty + 2;               // commit of the last GEMV
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yfull + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const int mt = cta / p.splits, sp = cta % p.splits;
+  const int q0 = (int)((long long)p.nq * sp / p.splits), q1 = (int)((long long)p.nq * (sp + 1) / p.splits);
+  const int n = p.n;
+  const int T = (q1 - q0) * n;                // stages of this CTA
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRgStages; ++s) {
+      mbar_init(&full[s], 33);
+      mbar_init(&sempty[s], 2);   // the P MMA's commit + the restore warps' representative
+    }
+    for (int b = 0; b < kRgPBuf; ++b) {
+      mbar_init(&pfull[b], 1);
+      mbar_init(&pempty[b], 1);
+    }
+    mbar_init(afull, kRgNR);
+    mbar_init(aempty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&xfull[b], 1);
+      mbar_init(&xempty[b], 1);
+    }
+    mbar_init(yfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == kRgWarpProd) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  constexpr uint32_t kColY = kRgPBuf * 128;
+
+  if (warp == kRgWarpProd) {
+    // ================= producer: stage t = (unit q0 + t / n, block t % n).  A lane's cp.async
+    // pieces of stage t are published (fence.proxy.async + arrive on full) LAG stages later, or at
+    // once before any wait that may depend on them (flush), so the pipeline never waits on itself.
+    const uint64_t pol = policy_evict_first();
+    const long long dpad = (long long)p.nq * 128;
+    // LAG < kRgStages: a full ring still holds kRgStages - LAG published stages, so waiting on a
+    // stage's release never depends on this warp's unpublished copies; only the X' wait may
+    // (a unit of n <= LAG blocks) and flushes first
+    constexpr int LAG = 4;
+    int issued = 0, arrived = 0;
+    auto flush = [&]() {
+      cp_async_wait<0>();
+      fence_proxy_async_smem();
+      for (; arrived < issued; ++arrived) mbar_arrive(&full[arrived % kRgStages]);
+    };
+    auto wait_or_flush = [&](uint64_t* bar, uint32_t parity) {   // warp-uniform decision
+      if (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
+        flush();
+        mbar_wait_sleep(bar, parity);
+      }
+    };
+    auto issue_x = [&](int u) {   // X' unit u of this CTA into buffer u & 1
+      if (u >= 2) wait_or_flush(&xempty[u & 1], (uint32_t)(((u >> 1) - 1) & 1));
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&xfull[u & 1], C::kXImg);
+        bulk_g2s(ximg + (u & 1) * C::kXImg, p.ximg + (long long)(q0 + u) * C::kXImg, C::kXImg, &xfull[u & 1], pol);
+      }
+    };
+    if (q1 > q0) issue_x(0);
+    if (q1 > q0 + 1) issue_x(1);
+    int s = 0, u = 0, i = 0;
+    uint32_t sph = 0;
+    for (int t = 0; t < T; ++t) {
+      const int qq = q0 + u;
+      if (i == 0 && u >= 2) issue_x(u);
+      if (t >= kRgStages) mbar_wait_sleep(&sempty[s], sph ^ 1u);
+      uint8_t* st = stages + s * kRgStage;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[s], 2048);
+        bulk_g2s(st + 8192, p.signs + ((long long)(i >> p.ksh) * p.nq + qq) * p.rows_pad + mt * 128, 2048, &full[s], pol);
+      }
+      // U'_i tile (rows mt*128 ..) and V'_i chunk (columns qq*128 ..): 2 x 256 pieces of 16 B
+      const uint8_t* ug = reinterpret_cast<const uint8_t*>(p.u) + ((long long)i * p.rows_pad + mt * 128) * 32;
+      const uint8_t* vg = reinterpret_cast<const uint8_t*>(p.v) + ((long long)i * dpad + (long long)qq * 128) * 32;
+#ifndef BS_RG_EXP_NOCOPY   // timing experiment: no U' / V' copies (wrong values)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int x = lane + 32 * r;                 // piece: row jj = x >> 1, K half kk = x & 1
+        const int jj = x >> 1, kk = x & 1;
+        const int off = ((jj >> 3) * 2 + kk) * 128 + (jj & 7) * 16;
+        cp_async16(st + off, ug + jj * 32 + kk * 16);
+        cp_async16(st + 4096 + off, vg + jj * 32 + kk * 16);
+      }
+#endif
+      cp_async_commit();
+      ++issued;
+      if (++i == n) { i = 0; ++u; }
+      if (++s == kRgStages) { s = 0; sph ^= 1u; }
+      if (issued - arrived > LAG) {   // groups older than the last LAG have landed
+        cp_async_wait<LAG>();
+        fence_proxy_async_smem();
+        for (; arrived < issued - LAG; ++arrived) mbar_arrive(&full[arrived % kRgStages]);
+      }
+    }
+    flush();
+  } else if (warp == kRgWarpMma) {
+    // ================= MMA warp
+    const uint32_t idp = idesc_f16_f32(128, 128, p.f16 ? 0u : 1u);
+    const uint32_t idg = idesc_f16_f32(128, BP, 2u);   // kind::tf32
+    int gpend = -1;   // unit (CTA-local) whose GEMV is pending
+    auto gemv = [&](int j) {
+      mbar_wait_sleep(afull, (uint32_t)(j & 1));
+      mbar_wait_sleep(&xfull[j & 1], (uint32_t)((j >> 1) & 1));
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t a0 = smem_u32(aimg), x0 = smem_u32(ximg + (j & 1) * C::kXImg);
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+          mma_tf32_ss(tbase + kColY, smem_desc_kmajor(a0 + kk * 256, 128, 4096),
+                      smem_desc_kmajor(x0 + kk * 256, 128, 4096), idg, (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(aempty);
+        mma_commit(&xempty[j & 1]);
+      }
+      __syncwarp();
+    };
+    int s = 0, pb = 0, u = 0, i = 0;
+    uint32_t sph = 0, pph = 0;
+    for (int t = 0; t < T; ++t) {
+      mbar_wait_sleep(&full[s], sph);
+      if (t >= kRgPBuf) mbar_wait_sleep(&pempty[pb], pph ^ 1u);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sa = smem_u32(stages + s * kRgStage);
+        mma_f16_ss(tbase + (uint32_t)(pb * 128), smem_desc_kmajor(sa, 128, 256),
+                   smem_desc_kmajor(sa + 4096, 128, 256), idp, 0u);
+        mma_commit(&pfull[pb]);
+        mma_commit(&sempty[s]);
+      }
+      __syncwarp();
+      if (gpend >= 0) {   // the previous unit's GEMV, once the next unit's first product is queued
+        gemv(gpend);
+        gpend = -1;
+      }
+      if (++i == n) { gpend = u; i = 0; ++u; }
+      if (++s == kRgStages) { s = 0; sph ^= 1u; }
+      if (++pb == kRgPBuf) { pb = 0; pph ^= 1u; }
+    }
+    if (gpend >= 0) gemv(gpend);
+    if (elect_one()) mma_commit(yfull);
+    __syncwarp();
+  } else {
+    // ================= restore warps: lane quadrant qd, column group h (kRgCols columns)
+    constexpr int NC = kRgCols, NW = NC / 32;
+    const int qd = warp & 3, h = warp >> 2;
+    const int j = qd * 32 + lane;
+    const uint32_t lq = (uint32_t)(qd * 32) << 16;
+    float acc[NC];
+#pragma unroll
+    for (int l = 0; l < NC; ++l) acc[l] = 0.f;
+    int s = 0, pb = 0, u = 0, i = 0;
+    uint32_t sph = 0, pph = 0;
+    for (int t = 0; t < T; ++t) {
+      mbar_wait_sleep(&pfull[pb], pph);
+      tc_fence_after();
+      uint32_t m[NC];
+#pragma unroll
+      for (int g = 0; g < NW; ++g)
+        tmem_ld32(tbase + lq + (uint32_t)(pb * 128 + h * NC + g * 32), *reinterpret_cast<uint32_t(*)[32]>(m + 32 * g));
+      mbar_wait(&full[s], sph);   // completed (the MMA warp waited on it): its sign tile is here
+      uint32_t nw[NW];
+#pragma unroll
+      for (int g = 0; g < NW; ++g)
+        nw[g] = ~*reinterpret_cast<const uint32_t*>(stages + s * kRgStage + 8192 + j * 16 + (h * NW + g) * 4);
+      tmem_ld_wait();
+      tc_fence_before();
+      // the restore warps meet once per stage; one thread then frees the P buffer and the
+      // stage's sign tile (2 mbarrier arrivals per stage instead of one per warp)
+      asm volatile("bar.sync 1, %0;" ::"n"(kRgNR * 32) : "memory");
+      if (threadIdx.x == 0) {
+        mbar_arrive(&pempty[pb]);
+        mbar_arrive(&sempty[s]);
+      }
+#ifdef BS_RG_EXP_NOAPPLY   // timing experiment: no sign application (wrong values)
+#pragma unroll
+      for (int l = 0; l < NC; ++l) acc[l] += __uint_as_float(m[l]);
+#else
+#pragma unroll
+      for (int l = 0; l < NC; l += 2) {   // F8 layout: column c of a word is bit (c & 3) 8 + (c >> 2)
+        const int c0 = l & 31, c1 = (l + 1) & 31;
+        const uint32_t w = nw[l >> 5];
+        const int b0 = (c0 & 3) * 8 + (c0 >> 2), b1 = (c1 & 3) * 8 + (c1 >> 2);
+        const float2 tv = make_float2(__uint_as_float(m[l] ^ ((w << (31 - b0)) & 0x80000000u)),
+                                      __uint_as_float(m[l + 1] ^ ((w << (31 - b1)) & 0x80000000u)));
+        const float2 a = __fadd2_rn(make_float2(acc[l], acc[l + 1]), tv);
+        acc[l] = a.x;
+        acc[l + 1] = a.y;
+      }
+#endif
+      if (++i == n) {   // W'[j, unit] complete: tf32 A image (after the previous GEMV read it)
+        if (u > 0) mbar_wait_sleep(aempty, (uint32_t)((u - 1) & 1));
+#pragma unroll
+        for (int mq = 0; mq < NC / 4; ++mq) {
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(o[e]) : "f"(acc[4 * mq + e]));
+          *reinterpret_cast<uint4*>(aimg + ((j >> 3) * 32 + h * (NC / 4) + mq) * 128 + (j & 7) * 16) =
+              make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(afull);
+#pragma unroll
+        for (int l = 0; l < NC; ++l) acc[l] = 0.f;
+        i = 0;
+        ++u;
+      }
+      if (++s == kRgStages) { s = 0; sph ^= 1u; }
+      if (++pb == kRgPBuf) { pb = 0; pph ^= 1u; }
+    }
+    if (h == 0) {   // y_acc -> this CTA's partial slot
+      mbar_wait_sleep(yfull, 0u);
+      tc_fence_after();
+      float* slot = p.part + (long long)cta * BP * 128;
+#pragma unroll
+      for (int b0 = 0; b0 < BP; b0 += 16) {
+        uint32_t yv[16];
+        tmem_ld16(tbase + lq + kColY + (uint32_t)b0, yv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int b = 0; b < 16; ++b) slot[(b0 + b) * 128 + j] = __uint_as_float(yv[b]);
+      }
+    }
+  }
+
+  // ---- teardown; the row tile's last CTA sums the partial slots in CTA order and writes y
+  __threadfence();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kRgWarpProd) tmem_dealloc<512>(tbase);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int prev = atomicAdd(p.counters + mt, 1);
+    *last_flag = (prev == p.splits - 1);
+  }
+  __syncthreads();
+  if (*last_flag) {
+    __threadfence();
+    const float* base = p.part + (long long)mt * p.splits * BP * 128;
+    for (int e = threadIdx.x; e < 128 * p.batch; e += blockDim.x) {
+      const int b = e / 128, r = e % 128;
+      const long long row = (long long)mt * 128 + r;
+      float a = 0.f;
+      for (int k = 0; k < p.splits; ++k) a += __ldcg(base + (long long)k * BP * 128 + b * 128 + r);
+      if (row < p.rows_local) {
+        const long long o = (long long)b * p.y_stride + row;
+        if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = a;
+        else reinterpret_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(a);
+      }
+    }
+    if (threadIdx.x == 0) p.counters[mt] = 0;
+  }
+}
+
+}  // namespace bs

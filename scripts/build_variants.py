@@ -16,6 +16,10 @@ VARIANTS = {
     "r1s8": ["-DBS_MX_R1=1", "-DBS_MX_NSLOT=8"],
     "r1s12": ["-DBS_MX_R1=1", "-DBS_MX_NSLOT=12"],
     "r2s4": ["-DBS_MX_R1=2"],
+    "rg32": ["-DBS_RG_COLS=32"],
+    "rgnoapply": ["-DBS_RG_EXP_NOAPPLY"],
+    "rgnocopy": ["-DBS_RG_EXP_NOCOPY"],
+    "rgnoboth": ["-DBS_RG_EXP_NOAPPLY", "-DBS_RG_EXP_NOCOPY"],
     "skel": ["-DBS_MX_EXP_NOST", "-DBS_MX_EXP_NOMMA", "-DBS_MX_EXP_NOEXP"],
 }
 if __name__ == "__main__":

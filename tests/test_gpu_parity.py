@@ -753,3 +753,51 @@ def test_store_load_range_matches_memory_load(bs, tmp_path, dtype):
         lay.set_num_blocks(4)
         y, xr = gpu_y(lay, x)
         assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 1e-3
+
+
+# ------------------------------------------------------------------ restore-and-multiply path
+@pytest.mark.parametrize("shape", [(256, 384, 3, 16, "bf16"), (300, 520, 5, 16, "bf16"), (1100, 264, 2, 16, "f16"),
+                                   (128, 1000, 4, 32, "bf16"), (640, 640, 17, 16, "bf16")])
+@pytest.mark.parametrize("batch", [1, 3, 8, 16, 17, 32])
+def test_rgemv_parity_ragged(bs, shape, batch):
+    """bitstack_matmul through the restore-and-multiply kernel (W' restored per 128 x 128 unit in
+    the SM, y += W' X'^T in tf32) against the oracle: ragged rows / d_in, k = 32 halves, fp16
+    factors, n above the prefill's 16, batch 1..32 (both token paddings, 16 and 32)."""
+    d_out, d_in, n, k, dt = shape
+    g, s32, blocks = compress_case(d_out, d_in, n, dt, 9300 + d_out + n, k=k)
+    lay = make_layer(bs, d_out, d_in, blocks, s32, dt)
+    lay.set_kernel("rgemv")
+    x = make_x(batch, g, 60 + batch)
+    c0 = bs.launch_count()
+    y, xr = gpu_y(lay, x)
+    assert bs.launch_count() - c0 == 2            # rg_xprep + rgemv
+    assert O.relative_l2(y, oracle_y(blocks, s32, n, xr)) <= 1e-3
+    for lvl in (1, max(1, n // 2)):               # lower levels of the same stack
+        lay.set_num_blocks(lvl)
+        y, xr = gpu_y(lay, x)
+        assert O.relative_l2(y, oracle_y(blocks, s32, lvl, xr)) <= 1e-3
+
+
+def test_rgemv_dispatch_bf16_y_and_determinism(bs):
+    """AUTO never takes the restore-and-multiply path (decode up to 8 tokens, prefill above);
+    forced, it gives bf16 y within the bf16-y bar and bitwise identical repeated calls, and it
+    refuses more than 32 tokens (E_UNSUPPORTED)."""
+    g, s32, blocks = compress_case(512, 768, 4, "bf16", 9400)
+    lay = make_layer(bs, 512, 768, blocks, s32, "bf16")
+    for batch, launches in [(3, 2), (8, 2), (9, 4)]:
+        x = make_x(batch, g, 70 + batch)
+        c0 = bs.launch_count()
+        y, xr = gpu_y(lay, x)
+        assert bs.launch_count() - c0 == launches, batch
+        assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 1e-3
+    lay.set_kernel("rgemv")
+    x = make_x(12, g, 80)
+    y, xr = gpu_y(lay, x, y_dtype=torch.bfloat16)
+    assert O.relative_l2(y, oracle_y(blocks, s32, 4, xr)) <= 4e-3
+    y1, _ = gpu_y(lay, x)
+    for _ in range(5):
+        y2, _ = gpu_y(lay, x)
+        assert np.array_equal(y1, y2)
+    with pytest.raises(bs.BitStackError) as e:
+        gpu_y(lay, make_x(33, g, 81))
+    assert e.value.name == "E_UNSUPPORTED"
