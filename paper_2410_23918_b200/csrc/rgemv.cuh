@@ -126,11 +126,19 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRgStages; ++s) {
       mbar_init(&full[s], 33);
+#ifdef BS_RG_BARSYNC
       mbar_init(&sempty[s], 2);   // the P MMA's commit + the restore warps' representative
+#else
+      mbar_init(&sempty[s], 1 + kRgNR);   // the P MMA's commit + every restore warp
+#endif
     }
     for (int b = 0; b < kRgPBuf; ++b) {
       mbar_init(&pfull[b], 1);
+#ifdef BS_RG_BARSYNC
       mbar_init(&pempty[b], 1);
+#else
+      mbar_init(&pempty[b], kRgNR);
+#endif
     }
     mbar_init(afull, kRgNR);
     mbar_init(aempty, 1);
@@ -271,7 +279,11 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
     int s = 0, pb = 0, u = 0, i = 0;
     uint32_t sph = 0, pph = 0;
     for (int t = 0; t < T; ++t) {
+#ifdef BS_RG_SPIN
+      mbar_wait(&pfull[pb], pph);
+#else
       mbar_wait_sleep(&pfull[pb], pph);
+#endif
       tc_fence_after();
       uint32_t m[NC];
 #pragma unroll
@@ -284,6 +296,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
         nw[g] = ~*reinterpret_cast<const uint32_t*>(stages + s * kRgStage + 8192 + j * 16 + (h * NW + g) * 4);
       tmem_ld_wait();
       tc_fence_before();
+#ifdef BS_RG_BARSYNC
       // the restore warps meet once per stage; one thread then frees the P buffer and the
       // stage's sign tile (2 mbarrier arrivals per stage instead of one per warp)
       asm volatile("bar.sync 1, %0;" ::"n"(kRgNR * 32) : "memory");
@@ -291,6 +304,15 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
         mbar_arrive(&pempty[pb]);
         mbar_arrive(&sempty[s]);
       }
+#else
+      // each warp frees its share of the P buffer and the stage's sign tile as soon as it holds
+      // them in registers, so fast warps run ahead instead of meeting the slowest every stage
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&pempty[pb]);
+        mbar_arrive(&sempty[s]);
+      }
+#endif
 #ifdef BS_RG_EXP_NOAPPLY   // timing experiment: no sign application (wrong values)
 #pragma unroll
       for (int l = 0; l < NC; ++l) acc[l] += __uint_as_float(m[l]);

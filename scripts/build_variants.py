@@ -17,6 +17,8 @@ VARIANTS = {
     "r1s12": ["-DBS_MX_R1=1", "-DBS_MX_NSLOT=12"],
     "r2s4": ["-DBS_MX_R1=2"],
     "rg32": ["-DBS_RG_COLS=32"],
+    "rgbar": ["-DBS_RG_BARSYNC"],
+    "rgspin": ["-DBS_RG_SPIN"],
     "rgnoapply": ["-DBS_RG_EXP_NOAPPLY"],
     "rgnocopy": ["-DBS_RG_EXP_NOCOPY"],
     "rgnoboth": ["-DBS_RG_EXP_NOAPPLY", "-DBS_RG_EXP_NOCOPY"],
