@@ -801,3 +801,26 @@ def test_rgemv_dispatch_bf16_y_and_determinism(bs):
     with pytest.raises(bs.BitStackError) as e:
         gpu_y(lay, make_x(33, g, 81))
     assert e.value.name == "E_UNSUPPORTED"
+
+
+# ------------------------------------------------------------------ output bounds (guard bands)
+@pytest.mark.parametrize("kernel,batch,dtype", [("auto", 1, "bf16"), ("auto", 3, "bf16"), ("auto", 8, "f16"),
+                                                ("auto", 20, "bf16"), ("rgemv", 5, "bf16"), ("simt", 2, "bf16"),
+                                                ("auto", 2, "f32")])
+def test_outputs_stay_inside_y(bs, kernel, batch, dtype):
+    """Every path writes exactly y[batch][rows_local]: guard bands of NaN before and after y in the
+    same allocation come back untouched (compute-sanitizer is not available on the GPU pool, so
+    out-of-bounds writes are checked this way), and y itself matches the oracle."""
+    g, s32, blocks = compress_case(300, 392, 3, dtype, 9500 + batch)
+    lay = make_layer(bs, 300, 392, blocks, s32, dtype)
+    if kernel != "auto":
+        lay.set_kernel(kernel)
+    guard = 4096
+    buf = torch.full((guard + batch * 300 + guard,), float("nan"), dtype=torch.float32, device="cuda")
+    y = buf[guard:guard + batch * 300].view(batch, 300)
+    x = torch.from_numpy(make_x(batch, g, 90).astype(np.float32)).cuda()
+    lay.matmul_raw(x.data_ptr(), bs.F32, y.data_ptr(), bs.F32, batch, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.isnan(buf[:guard]).all() and torch.isnan(buf[guard + batch * 300:]).all()
+    ref = oracle_y(blocks, s32, 3, x.double().cpu().numpy())
+    assert O.relative_l2(y.double().cpu().numpy(), ref) <= (1e-5 if dtype == "f32" else 1e-3)
