@@ -930,7 +930,7 @@ def main():
         peak, peak_src = sms * 128 * mhz * 1e6 / 1e12, "derived: SMs x 128 lane-instr/clk x max SM clock (B300_MICROARCH.md pipe rates)"
     else:
         peak, peak_src = peaks("decode" if decode_path else "prefill")
-    traffic = traffic_key(f"{args.workload}_n{n}_b{batch}_g{world}")
+    traffic = traffic_key(f"{args.workload}_n{n}_b{batch}_g{world}" + ("_rgemv" if path == "rgemv" else ""))
 
     # ---- e2e: public API with host buffers (pinned), copies inside the timed region
     x_h = x.cpu().pin_memory()

@@ -105,10 +105,6 @@ def ncu_summary(rep, title, dst, traffic_key=None, regex=None):
         tp = os.path.join(PROF, "traffic.json")
         tj = json.load(open(tp)) if os.path.exists(tp) else {}
         tj[traffic_key] = traffic
-        tj["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per call of the roofline's dominant kernel(s), "
-                       "from one ncu --set full capture (round 2: decode keys = zq_mx_kernel + decode_mx_kernel, "
-                       "prefill keys = wtile_kernel + prefill_gemm_kernel is NOT summed: the GEMM alone); "
-                       "keys <workload>_n<n>_b<batch>_g<world>")
         json.dump(tj, open(tp, "w"), indent=1, sort_keys=True)
     return traffic
 
@@ -179,7 +175,7 @@ def main():
     ncu_summary(os.path.join(R02, "prefill_c3_up.ncu-rep"), "C3 up/gate prefill: wtile + GEMM, one launch each",
                 "r02_ncu_prefill_c3_up.txt", "c3_up_n8_b2048_g1", regex="prefill_gemm")
     ncu_summary(os.path.join(RG, "rg_c2.ncu-rep"), "C2 restore-and-multiply (rgemv_kernel<16>, B=8), one launch",
-                "r02_ncu_rgemv_c2.txt", "c2_n16_b8_g1", regex="rgemv")
+                "r02_ncu_rgemv_c2.txt", "c2_n16_b8_g1_rgemv", regex="rgemv")
     # tests, smoke, sanitizer
     for src, dst in [("pytest_gpu.log", "r02_gpu_tests.txt"), ("smoke.log", "r02_smoke.txt")]:
         p = os.path.join(R02, src)
