@@ -168,8 +168,8 @@ def c4_launches(r):
         zq[g].append(t0)
         dec[g].append(t1)
     tot = sum(t for _, t in us)
-    lines = ["# ncu launch list of `python bench.py --workload c4 --steps 3 --warmup 3 --no-cpu-baseline --no-graph`",
-             "# (-k regex:'zq_grouped|decode_f8i_grouped', 128 launch pairs = 32 layers x 4 groups; --clock-control none,",
+    lines = ["# ncu launch list of one eager C4 token-step (`python bench.py --workload c4 --steps 1 --warmup 3 --no-cpu-baseline --no-graph`)",
+             "# (-k regex:'zq_mx|decode_mx', 128 launch pairs = 32 layers x 4 groups; --clock-control none,",
              "#  cold-cache and serialised: compare shares). Per group type, average over the layers:",
              f"{'group':14s} {'zq_us':>6s} {'decode_us':>10s} {'share':>7s}"]
     for g in groups:
