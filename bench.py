@@ -877,9 +877,9 @@ def main():
     per_step_launches = pkg.launch_count() - l0   # our kernels per bitstack_matmul call
     torch.cuda.synchronize()
     # bitstack_matmul AUTO with bf16 factors (csrc/bitstack.cu choose_path): the e4m3 decode up to
-    # 8 tokens, the prefill GEMM above (shards of >= 128 rows); --kernel rgemv forces restore-and-multiply
+    # 5 tokens, restore-and-multiply for 6..32, the prefill GEMM above (shards of >= 128 rows)
     if args.kernel == "auto":
-        path = "decode" if (batch <= 8 or rows < 128) else "prefill"
+        path = "decode" if (batch <= 5 or rows < 128) else ("rgemv" if batch <= 32 else "prefill")
     else:
         path = {"tc": "decode", "simt": "decode"}.get(args.kernel, args.kernel)
     decode_path = path == "decode"

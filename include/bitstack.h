@@ -70,10 +70,11 @@ typedef enum {
 
 /* Kernel selection for bitstack_matmul (bitstack_set_kernel). */
 typedef enum {
-  BITSTACK_KERNEL_AUTO = 0,   /* bf16 / f16 factors: up to 8 tokens the tcgen05 e4m3 decode kernel,
-                                 more the restored-tile GEMM (prefill; >= 128 local rows, n <= 16);
-                                 fp32 factors the tcgen05 fp16 decode kernel when supported, else
-                                 SIMT */
+  BITSTACK_KERNEL_AUTO = 0,   /* bf16 / f16 factors: 1-5 tokens the tcgen05 e4m3 decode kernel; with
+                                 >= 128 local rows, 6-32 tokens the restore-and-multiply kernel and
+                                 more the restored-tile GEMM (prefill, n <= 16), else the decode
+                                 kernel; fp32 factors the tcgen05 fp16 decode kernel when supported,
+                                 else SIMT */
   BITSTACK_KERNEL_TC = 1,     /* force the tcgen05/TMEM decode kernel (E_UNSUPPORTED if not possible) */
   BITSTACK_KERNEL_SIMT = 2,   /* force the CUDA-core FP32 reference kernel (any shape) */
   BITSTACK_KERNEL_PREFILL = 3,/* force the prefill path: W' = sum_i S_i (.) U_i V_i^T restored per
@@ -168,14 +169,16 @@ BITSTACK_API bitstack_status bitstack_set_num_blocks(bitstack_layer layer, int32
  * x and y must not alias.  batch == 0 is a no-op; n == 0 writes y = 0.
  * Asynchronous on `stream`; argument errors are reported synchronously.
  * Numerics, tensor-core paths, accumulation in fp32 throughout:
- *   - BF16/F16 factors, decode (batch <= 8): S as exact e4m3 +-1, the product
+ *   - BF16/F16 factors, decode (batch <= 5): S as exact e4m3 +-1, the product
  *     Z = V (.) (x/s) as three e4m3 digits per (rank, token) with power-of-two
  *     scales per 32-channel block (MX block scaling: digit 0 puts the block
  *     maximum in [128, 256), digit d is scaled 2^-4d further): error <= 2^-13 of
  *     the block maximum per element, whatever the range of x, s or the batch.
  *   - F32 factors: Z as two fp16 digits after a per-token power-of-two scale of
  *     x/s (~22 bits).
- *   - BF16/F16 factors, batch > 8 (prefill): the restored tile W' = W diag(s)
+ *   - BF16/F16 factors, 6..32 tokens (restore-and-multiply): W' summed in fp32,
+ *     W' and x/s rounded once to tf32 for the tcgen05 MMA (~1e-4 .. 4e-4).
+ *   - BF16/F16 factors, batch > 32 (prefill): the restored tile W' = W diag(s)
  *     and x/s as fp16 GEMM operands, each with power-of-two scales (per row of W',
  *     per token of x/s) so that neither overflows nor underflows.
  *   Every scale is exact; non-finite x propagates to y.
@@ -188,13 +191,13 @@ BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x
  * layer of the model is a BitStack stack):  ys[i] = W_hat_{n_i}(layers[i]) xs[i], i < count.
  * Each member keeps its own level n_i, dtypes of x / y are shared, xs[i] / ys[i] follow
  * bitstack_matmul's layouts (xs[i] may be the same buffer for several members).
- * When count <= 8, 1 <= batch <= 8, the members are distinct handles on one device on the
+ * When count <= 8, 1 <= batch <= 5, the members are distinct handles on one device on the
  * MX e4m3 decode path (bf16/f16 factors, d_in % 8 == 0, AUTO or TC kernel) and all xs / ys are
  * 16-byte aligned device buffers, the whole group runs as ONE Zq launch and ONE decode launch
  * per chunk of <= 8 tokens, whose CTAs are shared out among the members in proportion to their
  * work; members at level n_i == 0 get ys[i] = 0 (a memset) and no share of the launches (no
  * launch at all when every member is at level 0); otherwise the members run one after another through
- * bitstack_matmul (from 9 tokens that is the prefill path of each member).  Results are
+ * bitstack_matmul (from 6 tokens that is the restore-and-multiply path of each member).  Results are
  * identical to the individual calls either way.  With profiling enabled the fused pair is
  * bracketed once.  count == 0 or batch == 0 is a no-op.
  * Errors: E_INVALID_ARG (NULL arrays) and every error of bitstack_matmul. */

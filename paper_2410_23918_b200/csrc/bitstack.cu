@@ -2,6 +2,7 @@
 // validation, the device block store, and stream-ordered kernel launches.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -shared (see build.py).
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
@@ -54,6 +55,8 @@ struct bitstack_layer_s {
   uint8_t* pf_w = nullptr; // prefill path: W' operand image (transient workspace, grown on demand)
   uint8_t* pf_x = nullptr; // prefill path: X' operand image
   int64_t pf_w_bytes = 0, pf_x_bytes = 0;
+  CUtensorMap rg_tmu, rg_tmv;  // restore-and-multiply path: TMA maps of U' and V' (built once)
+  bool rg_maps = false;
   uint8_t* rg_x = nullptr;     // restore-and-multiply path: X' unit images (grown on demand)
   uint8_t* rg_part = nullptr;  // restore-and-multiply path: per-CTA partial y slots
   int64_t rg_x_bytes = 0, rg_part_bytes = 0;
@@ -167,24 +170,27 @@ bitstack_status launch_decode(const bs::DecodeParams& prm, int grid, cudaStream_
   return BITSTACK_OK;
 }
 
-constexpr int64_t kPrefillMinBatch = 9;    // AUTO: restored-tile GEMM path from this batch on
+constexpr int64_t kPrefillMinBatch = 33;   // AUTO: restored-tile GEMM path from this batch on
 
-// AUTO takes the restored-tile GEMM (fp16 operands, ~3e-4 relative error) from kPrefillMinBatch
-// tokens on -- past one MX decode pass (<= 8 tokens), where the decode's tensor work (48 Zq
-// columns per token) costs more than restoring W' (measured crossover) -- for shards of at least one full 128-row tile; tiny shards stay on the decode path
-// (one tile of GEMM work is not worth the restore, and y over a handful of rows is where the fp16
-// operand rounding shows most).
+// AUTO takes the restored-tile GEMM (fp16 operands, ~3e-4 relative error) above the
+// restore-and-multiply path's 32 tokens, for shards of at least one full 128-row tile; tiny shards
+// stay on the decode path (one tile of GEMM work is not worth the restore, and y over a handful of
+// rows is where the fp16 operand rounding shows most).
 bool prefill_auto(bitstack_layer L, int64_t batch) { return batch >= kPrefillMinBatch && L->rows_local >= 128; }
 
-// The restore-and-multiply path (rgemv.cuh) is selected explicitly (BITSTACK_KERNEL_RGEMV): it
-// measured between the decode and the prefill paths, so AUTO keeps the e4m3
-// decode up to 8 tokens and the restored-tile GEMM above.
+// AUTO takes the restore-and-multiply path (rgemv.cuh) for kRgMinBatch..32 tokens with 16-bit
+// factors: there the e4m3 decode's tensor work (48 Zq columns per token) exceeds restoring W'
+// inside the SM, and the prefill path's W' round trip and 128-token GEMM tiles are not paid back
+// (measured crossovers on C2 and C5).
+constexpr int64_t kRgMinBatch = 6;
 enum MatmulPath { kPathDecode, kPathRgemv, kPathPrefill };
 MatmulPath choose_path(bitstack_layer L, int64_t batch) {
   const bool fp16ok = L->dev_fdt != 0 && L->layout == 1;
   if (L->kernel == BITSTACK_KERNEL_PREFILL) return kPathPrefill;
   if (L->kernel == BITSTACK_KERNEL_RGEMV) return kPathRgemv;
   if (L->kernel != BITSTACK_KERNEL_AUTO || !fp16ok) return kPathDecode;
+  // (shards of >= one 128-row tile: over a handful of rows the tf32 operand rounding shows most)
+  if (batch >= kRgMinBatch && batch <= bs::kRgMaxBatch && L->rows_local >= 128) return kPathRgemv;
   if (L->n_act * L->kh <= 16 && prefill_auto(L, batch)) return kPathPrefill;
   return kPathDecode;
 }
@@ -488,6 +494,28 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   return record_prof(st, false, &slot);
 }
 
+// TMA maps of a [rows][16] 16-bit factor array: box 128 rows x 16, 32-byte swizzle (the UMMA
+// K-major SW32 layout).  The encoder comes from the driver at run time (no libcuda link).
+bitstack_status encode_factor_map(CUtensorMap* map, const void* base, int64_t rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(BITSTACK_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {16, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {32};
+  const cuuint32_t box[2] = {16, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BITSTACK_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return BITSTACK_OK;
+}
+
 // Restore-and-multiply path (rgemv.cuh): X' images, then one kernel; 2 launches on `st`.
 template <int BP>
 bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
@@ -512,7 +540,16 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
                                             reinterpret_cast<uint4*>(L->rg_x));
   count_launch();
   CK(cudaGetLastError());
+  if (!L->rg_maps) {
+    rs = encode_factor_map(&L->rg_tmu, L->u, (int64_t)L->n_cap * L->kh * L->rows_pad);
+    if (rs) return rs;
+    rs = encode_factor_map(&L->rg_tmv, L->v, (int64_t)L->n_cap * L->kh * L->d_in_pad);
+    if (rs) return rs;
+    L->rg_maps = true;
+  }
   bs::RgParams rp;
+  rp.tmu = L->rg_tmu;
+  rp.tmv = L->rg_tmv;
   rp.signs = L->signs;
   rp.u = reinterpret_cast<const uint16_t*>(L->u);
   rp.v = reinterpret_cast<const uint16_t*>(L->v);
@@ -531,6 +568,7 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
   rp.splits = splits;
   rp.batch = (int)batch;
   rp.f16 = L->dev_fdt == 2 ? 1 : 0;
+  rp.trace = reinterpret_cast<long long*>(g_dbg_acc);
   int slot = -1;   // measurement hooks bracket the dominant kernel
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
@@ -1280,7 +1318,7 @@ bitstack_status bitstack_matmul_grouped(const bitstack_layer* layers, int32_t co
   if (count == 0 || batch == 0) return BITSTACK_OK;
   // One launch pair when every member can take the e4m3 decode kernel on device buffers;
   // otherwise the members run one after another through bitstack_matmul (same results).
-  bool fused = count <= bs::kMaxMxGroup && batch >= 1 && batch < kPrefillMinBatch &&
+  bool fused = count <= bs::kMaxMxGroup && batch >= 1 && batch < kRgMinBatch &&
                valid_dtype(x_dtype) && (y_dtype == BITSTACK_F32 || y_dtype == BITSTACK_BF16);
   // members at level 0 (possible under any budget below one level, and common under the Random
   // and Greedy sortings) get y = 0 and stay out of the launches; the rest run fused

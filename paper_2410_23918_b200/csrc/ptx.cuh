@@ -64,10 +64,16 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Watchdog by wall time (a suspended wait can last up to its hint): trap after ~10 s.
 __device__ __noinline__ void mbar_wait_sleep_slow(uint64_t* bar, uint32_t parity) {
-  uint32_t spins = 0;
+  const uint64_t t0 = global_ns();
   while (!mbar_try_wait_sleep(bar, parity)) {
-    if (++spins > BS_WATCHDOG_SPINS) __trap();
+    if (global_ns() - t0 > 10000000000ull) __trap();
   }
 }
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {

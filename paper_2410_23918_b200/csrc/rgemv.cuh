@@ -9,8 +9,8 @@
 // plus a K = 16 MMA); the prefill path restores W' once but writes and re-reads it through HBM
 // as an fp16 operand and pads the GEMM to 128 tokens.  Here each CTA owns one 128-row tile and a
 // contiguous range of 128-column units and, per (unit, block):
-//   producer warp   cp.async of the U'_i tile and the V'_i chunk (16-byte pieces into the UMMA
-//                   K-major core layout), one bulk copy of the 128 x 128 sign tile; stage ring
+//   producer warp   TMA tensor copies of the U'_i tile and the V'_i chunk (32-byte swizzle = the
+//                   UMMA K-major layout), one bulk copy of the 128 x 128 sign tile; stage ring
 //   MMA warp        P_i = U'_i V'_i^T (tcgen05 kind::f16, M128 N128 K16: exact products, fp32
 //                   TMEM, triple-buffered); per unit, after its restore: y_acc += W' X'^T
 //                   (kind::tf32, 16 x K8 MMAs, A = W' from SMEM, B = the unit's X' image)
@@ -21,11 +21,15 @@
 // order (deterministic) and writes y.  Numerics: W' and X' rounded once to tf32 (10 explicit
 // mantissa bits, fp32 range: no operand scaling), fp32 accumulation.
 #pragma once
+#include <cuda.h>   // CUtensorMap (the encoder is fetched at run time: no libcuda link)
+
 #include "decode_tc.cuh"
 
 namespace bs {
 
 struct RgParams {
+  CUtensorMap tmu;        // U' as [n x kh x rows_pad][16] 16-bit, box 128 x 16, 32-byte swizzle
+  CUtensorMap tmv;        // V' as [n x kh x d_in_pad][16] 16-bit, box 128 x 16, 32-byte swizzle
   const uint4* signs;     // [n_cap][nq][rows_pad] F8 layout
   const uint16_t* u;      // [n x kh][rows_pad][16] U' (bf16 / f16 storage)
   const uint16_t* v;      // [n x kh][d_in_pad][16] V'
@@ -38,17 +42,23 @@ struct RgParams {
   int n;                  // active 16-rank blocks (halves)
   int ksh;                // sign tile of block i is i >> ksh
   int nq, rows_pad, rows_local, row_tiles, splits, batch, f16;
+  long long* trace;       // timing build (-DBS_RG_TRACE, scripts/rg_trace.py): per-stage stamps of CTA 0
 };
 
 constexpr int kRgStages = 10;
 constexpr int kRgPBuf = 3;                      // TMEM P buffers (128 columns each)
 #ifndef BS_RG_COLS
-#define BS_RG_COLS 64
+#define BS_RG_COLS 32
 #endif
 constexpr int kRgCols = BS_RG_COLS;             // columns of a unit per restore warp (32 or 64)
 constexpr int kRgNR = 4 * (128 / kRgCols);      // restore warps (4 lane quadrants x column groups)
+#ifdef BS_RG_SAMESMSP   // MMA and producer warps on one SMSP (3 idle warps in between)
+constexpr int kRgWarpMma = kRgNR, kRgWarpProd = kRgNR + 4;
+constexpr int kRgWarps = kRgNR + 5;
+#else
 constexpr int kRgWarpMma = kRgNR, kRgWarpProd = kRgNR + 1;
 constexpr int kRgWarps = kRgNR + 2;             // restore warps + MMA + producer
+#endif
 constexpr int kRgMaxBatch = 32;
 constexpr int kRgStage = 4096 + 4096 + 2048;    // U' tile, V' chunk, sign tile
 constexpr int kRgAImg = 128 * 128 * 4;          // W' unit, tf32
@@ -85,6 +95,25 @@ __global__ void __launch_bounds__(256) rg_xprep_kernel(const void* __restrict__ 
   }
 }
 
+// TMA 2D tile copy (box 16 x 128 of 16-bit elements, 32-byte swizzle) -> shared, tx on `bar`.
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// UMMA shared-memory descriptor, K-major, 32-byte swizzle: rows of 32 B (16 x 16-bit, the whole
+// K = 16), 8-row groups 256 B apart (SBO); LBO unused for a K extent within one swizzle span.
+__device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;   // SWIZZLE_32B
+  return d;
+}
+
 __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
   asm volatile(
@@ -95,8 +124,13 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
       : "memory");
 }
 
+#ifdef BS_RG_TRACE
+#define RG_TR(t_, c_) do { if (p.trace && blockIdx.x == 0 && (t_) < 2048) p.trace[(t_) * 8 + (c_)] = clock64(); } while (0)
+#else
+#define RG_TR(t_, c_) do { } while (0)
+#endif
 template <int BP>
-__global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams p) {
+__global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_constant__ RgParams p) {
   using C = RgCfg<BP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -104,7 +138,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
   uint8_t* aimg = smem + kRgStages * kRgStage;              // W' unit (tf32 A image)
   uint8_t* ximg = aimg + kRgAImg;                           // [2] X' units
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
-  uint64_t* full = bars;                      // [S] 32 producer lanes (after their cp.async) + 1 sign tx
+  uint64_t* full = bars;                      // [S] producer arrive + tx (U', V' tensor copies, sign tile)
   uint64_t* sempty = full + kRgStages;        // [S] MMA commit + the restore warps (signs read)
   uint64_t* pfull = sempty + kRgStages;       // [3] commit of P_i
   uint64_t* pempty = pfull + kRgPBuf;         // [3] the restore warps (after a named barrier)
@@ -125,7 +159,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRgStages; ++s) {
-      mbar_init(&full[s], 33);
+      mbar_init(&full[s], 1);   // the producer's arrive + tx bytes
 #ifdef BS_RG_BARSYNC
       mbar_init(&sempty[s], 2);   // the P MMA's commit + the restore warps' representative
 #else
@@ -157,71 +191,35 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
   constexpr uint32_t kColY = kRgPBuf * 128;
 
   if (warp == kRgWarpProd) {
-    // ================= producer: stage t = (unit q0 + t / n, block t % n).  A lane's cp.async
-    // pieces of stage t are published (fence.proxy.async + arrive on full) LAG stages later, or at
-    // once before any wait that may depend on them (flush), so the pipeline never waits on itself.
-    const uint64_t pol = policy_evict_first();
-    const long long dpad = (long long)p.nq * 128;
-    // LAG < kRgStages: a full ring still holds kRgStages - LAG published stages, so waiting on a
-    // stage's release never depends on this warp's unpublished copies; only the X' wait may
-    // (a unit of n <= LAG blocks) and flushes first
-    constexpr int LAG = 4;
-    int issued = 0, arrived = 0;
-    auto flush = [&]() {
-      cp_async_wait<0>();
-      fence_proxy_async_smem();
-      for (; arrived < issued; ++arrived) mbar_arrive(&full[arrived % kRgStages]);
-    };
-    auto wait_or_flush = [&](uint64_t* bar, uint32_t parity) {   // warp-uniform decision
-      if (!__all_sync(0xffffffffu, mbar_try_wait(bar, parity))) {
-        flush();
-        mbar_wait_sleep(bar, parity);
-      }
-    };
-    auto issue_x = [&](int u) {   // X' unit u of this CTA into buffer u & 1
-      if (u >= 2) wait_or_flush(&xempty[u & 1], (uint32_t)(((u >> 1) - 1) & 1));
-      if (lane == 0) {
+    // ================= producer (one lane): stage t = (unit q0 + t / n, block t % n): the U'_i
+    // tile and the V'_i chunk by TMA tensor copies (32-byte swizzle: the UMMA K-major layout),
+    // the sign tile by a bulk copy, all completing as tx bytes on full[s]
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const int dpad = p.nq * 128;
+      auto issue_x = [&](int u) {   // X' unit u of this CTA into buffer u & 1
+        if (u >= 2) mbar_wait_sleep(&xempty[u & 1], (uint32_t)(((u >> 1) - 1) & 1));
         mbar_arrive_expect_tx(&xfull[u & 1], C::kXImg);
         bulk_g2s(ximg + (u & 1) * C::kXImg, p.ximg + (long long)(q0 + u) * C::kXImg, C::kXImg, &xfull[u & 1], pol);
-      }
-    };
-    if (q1 > q0) issue_x(0);
-    if (q1 > q0 + 1) issue_x(1);
-    int s = 0, u = 0, i = 0;
-    uint32_t sph = 0;
-    for (int t = 0; t < T; ++t) {
-      const int qq = q0 + u;
-      if (i == 0 && u >= 2) issue_x(u);
-      if (t >= kRgStages) mbar_wait_sleep(&sempty[s], sph ^ 1u);
-      uint8_t* st = stages + s * kRgStage;
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&full[s], 2048);
+      };
+      if (q1 > q0) issue_x(0);
+      if (q1 > q0 + 1) issue_x(1);
+      int s = 0, u = 0, i = 0;
+      uint32_t sph = 0;
+      for (int t = 0; t < T; ++t) {
+        const int qq = q0 + u;
+        if (i == 0 && u >= 2) issue_x(u);
+        if (t >= kRgStages) mbar_wait_sleep(&sempty[s], sph ^ 1u);
+        RG_TR(t, 0);
+        uint8_t* st = stages + s * kRgStage;
+        mbar_arrive_expect_tx(&full[s], 4096 + 4096 + 2048);
+        tma_2d(st, &p.tmu, 0, i * p.rows_pad + mt * 128, &full[s]);
+        tma_2d(st + 4096, &p.tmv, 0, i * dpad + qq * 128, &full[s]);
         bulk_g2s(st + 8192, p.signs + ((long long)(i >> p.ksh) * p.nq + qq) * p.rows_pad + mt * 128, 2048, &full[s], pol);
-      }
-      // U'_i tile (rows mt*128 ..) and V'_i chunk (columns qq*128 ..): 2 x 256 pieces of 16 B
-      const uint8_t* ug = reinterpret_cast<const uint8_t*>(p.u) + ((long long)i * p.rows_pad + mt * 128) * 32;
-      const uint8_t* vg = reinterpret_cast<const uint8_t*>(p.v) + ((long long)i * dpad + (long long)qq * 128) * 32;
-#ifndef BS_RG_EXP_NOCOPY   // timing experiment: no U' / V' copies (wrong values)
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int x = lane + 32 * r;                 // piece: row jj = x >> 1, K half kk = x & 1
-        const int jj = x >> 1, kk = x & 1;
-        const int off = ((jj >> 3) * 2 + kk) * 128 + (jj & 7) * 16;
-        cp_async16(st + off, ug + jj * 32 + kk * 16);
-        cp_async16(st + 4096 + off, vg + jj * 32 + kk * 16);
-      }
-#endif
-      cp_async_commit();
-      ++issued;
-      if (++i == n) { i = 0; ++u; }
-      if (++s == kRgStages) { s = 0; sph ^= 1u; }
-      if (issued - arrived > LAG) {   // groups older than the last LAG have landed
-        cp_async_wait<LAG>();
-        fence_proxy_async_smem();
-        for (; arrived < issued - LAG; ++arrived) mbar_arrive(&full[arrived % kRgStages]);
+        if (++i == n) { i = 0; ++u; }
+        if (++s == kRgStages) { s = 0; sph ^= 1u; }
       }
     }
-    flush();
   } else if (warp == kRgWarpMma) {
     // ================= MMA warp
     const uint32_t idp = idesc_f16_f32(128, 128, p.f16 ? 0u : 1u);
@@ -246,12 +244,13 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
     uint32_t sph = 0, pph = 0;
     for (int t = 0; t < T; ++t) {
       mbar_wait_sleep(&full[s], sph);
+      if (lane == 0) RG_TR(t, 2);
       if (t >= kRgPBuf) mbar_wait_sleep(&pempty[pb], pph ^ 1u);
+      if (lane == 0) RG_TR(t, 3);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sa = smem_u32(stages + s * kRgStage);
-        mma_f16_ss(tbase + (uint32_t)(pb * 128), smem_desc_kmajor(sa, 128, 256),
-                   smem_desc_kmajor(sa + 4096, 128, 256), idp, 0u);
+        mma_f16_ss(tbase + (uint32_t)(pb * 128), smem_desc_sw32(sa), smem_desc_sw32(sa + 4096), idp, 0u);
         mma_commit(&pfull[pb]);
         mma_commit(&sempty[s]);
       }
@@ -267,7 +266,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
     if (gpend >= 0) gemv(gpend);
     if (elect_one()) mma_commit(yfull);
     __syncwarp();
-  } else {
+  } else if (warp < kRgNR) {
     // ================= restore warps: lane quadrant qd, column group h (kRgCols columns)
     constexpr int NC = kRgCols, NW = NC / 32;
     const int qd = warp & 3, h = warp >> 2;
@@ -284,6 +283,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
 #else
       mbar_wait_sleep(&pfull[pb], pph);
 #endif
+      if (lane == 0 && (warp == 0 || warp == kRgNR - 1)) RG_TR(t, warp == 0 ? 4 : 6);
       tc_fence_after();
       uint32_t m[NC];
 #pragma unroll
@@ -329,6 +329,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
         acc[l + 1] = a.y;
       }
 #endif
+      if (lane == 0 && (warp == 0 || warp == kRgNR - 1)) RG_TR(t, warp == 0 ? 5 : 7);
       if (++i == n) {   // W'[j, unit] complete: tf32 A image (after the previous GEMV read it)
         if (u > 0) mbar_wait_sleep(aempty, (uint32_t)((u - 1) & 1));
 #pragma unroll
@@ -395,4 +396,5 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const RgParams 
   }
 }
 
+#undef RG_TR
 }  // namespace bs

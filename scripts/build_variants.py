@@ -18,6 +18,8 @@ VARIANTS = {
     "r2s4": ["-DBS_MX_R1=2"],
     "rg32": ["-DBS_RG_COLS=32"],
     "rgbar": ["-DBS_RG_BARSYNC"],
+    "rgsame": ["-DBS_RG_SAMESMSP"],
+    "rg32same": ["-DBS_RG_COLS=32", "-DBS_RG_SAMESMSP"],
     "rgspin": ["-DBS_RG_SPIN"],
     "rgnoapply": ["-DBS_RG_EXP_NOAPPLY"],
     "rgnocopy": ["-DBS_RG_EXP_NOCOPY"],

@@ -5,7 +5,8 @@ The oracle is scale-equivariant (Eq.4: y = W_s (x / s)), so ever
 the same relative-L2 bar as the ordinary parity tests (reading R16): 1e-3 with bf16 / f16
 factors, 1e-5 with fp32 factors, y in fp32.  Paths: the MX e4m3 decode (per-(K-block, column,
 digit) scales), the fp16 decode of fp32-factor layers and the prefill GEMM (power-of-two
-operand scales from the call's max |x / s|), and the SIMT kernel (fp32 throughout).
+operand scales from the call's max |x / s|), the restore-and-multiply kernel (tf32 operands, fp32
+range), and the SIMT kernel (fp32 throughout).
 
 Also the bit-exact pin of the decode kernel's sign expansion ("unpacked ... for
 use during inference"): with U_i[:, 0] = 2^i, V_i[:, 0] = 1, s = 1 and a one-hot x = e_c,
@@ -77,7 +78,7 @@ TOL = {"bf16": 1e-3, "f16": 1e-3, "f32": 1e-5}
 # (path name, factor dtype, kernel): the MX e4m3 decode, the fp16 decode (fp32 factors), the
 # prefill GEMM (forced at small batches), the SIMT kernel
 PATHS = [("mx", "bf16", "tc"), ("mx16", "f16", "tc"), ("fp16dec", "f32", "tc"), ("prefill", "bf16", "prefill"),
-         ("prefill16", "f16", "prefill"), ("simt", "bf16", "simt")]
+         ("prefill16", "f16", "prefill"), ("rgemv", "bf16", "rgemv"), ("rgemv16", "f16", "rgemv"), ("simt", "bf16", "simt")]
 
 
 @pytest.mark.parametrize("path,dtype,kernel", PATHS)
