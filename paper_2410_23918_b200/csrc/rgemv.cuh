@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       for (int g = 0; g < NW; ++g)
         nw[g] = ~*reinterpret_cast<const uint32_t*>(stages + s * kRgStage + 8192 + j * 16 + (h * NW + g) * 4);
       tmem_ld_wait();
+      if (lane == 0 && warp == 0) RG_TR(t, 1);
       tc_fence_before();
 #ifdef BS_RG_BARSYNC
       // the restore warps meet once per stage; one thread then frees the P buffer and the

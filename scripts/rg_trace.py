@@ -28,11 +28,12 @@ t = tr.cpu().numpy().reshape(-1, 8)
 T = int((t[:, 2] != 0).sum())
 t0 = t[0, 0]
 t = t[:T] - t0
-print("stage | prod_issue prod_publish | mma_full mma_issue | r0_P r0_done | rL_P rL_done   (cycles from stage 0 issue)")
+print("stage | prod_issue r0_ld_done | mma_full mma_issue | r0_P r0_done | rL_P rL_done   (cycles from stage 0 issue)")
 for k in list(range(min(T, 40))) + list(range(max(40, T - 8), T)):
     print(f"{k:4d}", *[f"{v:8d}" for v in t[k]])
 d = np.diff(t[:, 3])
 print("MMA issue interval median", np.median(d[8:]), "; restore warp0 per-stage median", np.median(np.diff(t[:, 5])[8:]))
-print("median lags: publish-issue", np.median(t[8:, 1] - t[8:, 0]), " mma_full-publish", np.median(t[8:, 2] - t[8:, 1]),
+print("median lags: mma_full-issue", np.median(t[8:, 2] - t[8:, 0]),
       " mma_issue-full", np.median(t[8:, 3] - t[8:, 2]), " r0_P-mma_issue", np.median(t[8:, 4] - t[8:, 3]),
-      " r0 work", np.median(t[8:, 5] - t[8:, 4]))
+      " r0 P->ld done", np.median(t[8:, 1] - t[8:, 4]), " r0 ld done->done", np.median(t[8:, 5] - t[8:, 1]),
+      " r0 done->next P", np.median(t[9:, 4] - t[8:-1, 5]))
