@@ -17,6 +17,7 @@ from collections import OrderedDict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 R02 = os.path.join(ROOT, "gpurun_out", "r02")
 RG = os.path.join(ROOT, "gpurun_out", "rg")
+R02B = os.path.join(ROOT, "gpurun_out", "r02b")
 PROF = os.path.join(ROOT, "profiles")
 KEYS = [
     "gpu__time_duration.sum", "sm__cycles_elapsed.avg", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -143,15 +144,18 @@ def main():
         write("r02_shard_c5.json", "\n".join(json.dumps(d) for d in sh))
     # batch sweeps: AUTO, forced prefill, forced restore-and-multiply
     parts = []
+    bb = json_lines(os.path.join(R02B, "bsweep.jsonl"))
+    if bb:
+        parts.append(sweep_table(bb, "AUTO path by batch, final dispatch (e4m3 decode B <= 5, restore-and-multiply 6..32, prefill above)"))
     bs = json_lines(os.path.join(R02, "bsweep.jsonl"))
     if bs:
-        parts.append(sweep_table(bs, "AUTO path by batch (e4m3 decode for B <= 8, prefill GEMM from 9)"))
+        parts.append(sweep_table(bs, "AUTO path by batch, earlier dispatch (e4m3 decode B <= 8, prefill GEMM from 9)"))
     bp = json_lines(os.path.join(R02, "bsweep_prefill.jsonl"))
     if bp:
         parts.append(sweep_table(bp, "prefill path forced (bench.py --kernel prefill)"))
     br = json_lines(os.path.join(RG, "rg.jsonl"))
     if br:
-        parts.append(sweep_table(br, "restore-and-multiply path forced (bench.py --kernel rgemv)"))
+        parts.append(sweep_table(br, "restore-and-multiply path forced (bench.py --kernel rgemv), first version (cp.async operand staging)"))
     if parts:
         write("r02_batch_sweep.txt", "\n\n".join(parts))
     # launch lists
@@ -174,7 +178,7 @@ def main():
                 "r02_ncu_decode_c5.txt", "c5_n12_b1_g1")
     ncu_summary(os.path.join(R02, "prefill_c3_up.ncu-rep"), "C3 up/gate prefill: wtile + GEMM, one launch each",
                 "r02_ncu_prefill_c3_up.txt", "c3_up_n8_b2048_g1", regex="prefill_gemm")
-    ncu_summary(os.path.join(RG, "rg_c2.ncu-rep"), "C2 restore-and-multiply (rgemv_kernel<16>, B=8), one launch",
+    ncu_summary(os.path.join(R02B, "rg_c2.ncu-rep"), "C2 restore-and-multiply (rgemv_kernel<16>, B=8), one launch",
                 "r02_ncu_rgemv_c2.txt", "c2_n16_b8_g1_rgemv", regex="rgemv")
     # tests, smoke, sanitizer
     for src, dst in [("pytest_gpu.log", "r02_gpu_tests.txt"), ("smoke.log", "r02_smoke.txt")]:
