@@ -129,6 +129,13 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
 #else
 #define RG_TR(t_, c_) do { } while (0)
 #endif
+// Every role waits with a suspend-time hint by default (a spinning MMA / producer warp measured no
+// faster: BS_RG_SPIN_FAST).
+#ifdef BS_RG_SPIN_FAST
+#define RG_WAIT_FAST mbar_wait
+#else
+#define RG_WAIT_FAST mbar_wait_sleep
+#endif
 template <int BP>
 __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_constant__ RgParams p) {
   using C = RgCfg<BP>;
@@ -209,7 +216,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       for (int t = 0; t < T; ++t) {
         const int qq = q0 + u;
         if (i == 0 && u >= 2) issue_x(u);
-        if (t >= kRgStages) mbar_wait_sleep(&sempty[s], sph ^ 1u);
+        if (t >= kRgStages) RG_WAIT_FAST(&sempty[s], sph ^ 1u);
         RG_TR(t, 0);
         uint8_t* st = stages + s * kRgStage;
         mbar_arrive_expect_tx(&full[s], 4096 + 4096 + 2048);
@@ -226,8 +233,8 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     const uint32_t idg = idesc_f16_f32(128, BP, 2u);   // kind::tf32
     int gpend = -1;   // unit (CTA-local) whose GEMV is pending
     auto gemv = [&](int j) {
-      mbar_wait_sleep(afull, (uint32_t)(j & 1));
-      mbar_wait_sleep(&xfull[j & 1], (uint32_t)((j >> 1) & 1));
+      RG_WAIT_FAST(afull, (uint32_t)(j & 1));
+      RG_WAIT_FAST(&xfull[j & 1], (uint32_t)((j >> 1) & 1));
       tc_fence_after();
       if (elect_one()) {
         const uint32_t a0 = smem_u32(aimg), x0 = smem_u32(ximg + (j & 1) * C::kXImg);
@@ -243,9 +250,9 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     int s = 0, pb = 0, u = 0, i = 0;
     uint32_t sph = 0, pph = 0;
     for (int t = 0; t < T; ++t) {
-      mbar_wait_sleep(&full[s], sph);
+      RG_WAIT_FAST(&full[s], sph);
       if (lane == 0) RG_TR(t, 2);
-      if (t >= kRgPBuf) mbar_wait_sleep(&pempty[pb], pph ^ 1u);
+      if (t >= kRgPBuf) RG_WAIT_FAST(&pempty[pb], pph ^ 1u);
       if (lane == 0) RG_TR(t, 3);
       tc_fence_after();
       if (elect_one()) {
@@ -398,4 +405,5 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
 }
 
 #undef RG_TR
+#undef RG_WAIT_FAST
 }  // namespace bs

@@ -19,6 +19,7 @@ VARIANTS = {
     "rg32": ["-DBS_RG_COLS=32"],
     "rgbar": ["-DBS_RG_BARSYNC"],
     "rgsame": ["-DBS_RG_SAMESMSP"],
+    "rgspinfast": ["-DBS_RG_SPIN_FAST"],
     "rg32same": ["-DBS_RG_COLS=32", "-DBS_RG_SAMESMSP"],
     "rgspin": ["-DBS_RG_SPIN"],
     "rgnoapply": ["-DBS_RG_EXP_NOAPPLY"],
