@@ -46,7 +46,15 @@ struct RgParams {
 };
 
 constexpr int kRgStages = 10;
-constexpr int kRgPBuf = 3;                      // TMEM P buffers (128 columns each)
+constexpr int kRgPBuf = 3;                      // TMEM P buffers per half
+#ifndef BS_RG_HALVES
+#define BS_RG_HALVES 2
+#endif
+// The 128 channels of a unit form kRgHV independent product pipelines (P MMA N = 128 / kRgHV,
+// their own buffers and barriers, their own restore warps), so the two groups of restore warps do
+// not wait for each other and one group's TMEM loads overlap the other's arithmetic.
+constexpr int kRgHV = BS_RG_HALVES;
+constexpr int kRgPCols = 128 / kRgHV;
 #ifndef BS_RG_COLS
 #define BS_RG_COLS 32
 #endif
@@ -147,9 +155,9 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* full = bars;                      // [S] producer arrive + tx (U', V' tensor copies, sign tile)
   uint64_t* sempty = full + kRgStages;        // [S] MMA commit + the restore warps (signs read)
-  uint64_t* pfull = sempty + kRgStages;       // [3] commit of P_i
-  uint64_t* pempty = pfull + kRgPBuf;         // [3] the restore warps (after a named barrier)
-  uint64_t* afull = pempty + kRgPBuf;         // 16 restore warps wrote the W' unit
+  uint64_t* pfull = sempty + kRgStages;       // [HV][3] commit of P_i (one channel half)
+  uint64_t* pempty = pfull + kRgHV * kRgPBuf; // [HV][3] the half's restore warps
+  uint64_t* afull = pempty + kRgHV * kRgPBuf; // the restore warps wrote the W' unit
   uint64_t* aempty = afull + 1;               // commit of the unit's GEMV MMAs
   uint64_t* xfull = aempty + 1;               // [2] bulk copy of an X' unit
   uint64_t* xempty = xfull + 2;               // [2] commit of the GEMV that read it
@@ -173,12 +181,12 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       mbar_init(&sempty[s], 1 + kRgNR);   // the P MMA's commit + every restore warp
 #endif
     }
-    for (int b = 0; b < kRgPBuf; ++b) {
+    for (int b = 0; b < kRgHV * kRgPBuf; ++b) {
       mbar_init(&pfull[b], 1);
 #ifdef BS_RG_BARSYNC
       mbar_init(&pempty[b], 1);
 #else
-      mbar_init(&pempty[b], kRgNR);
+      mbar_init(&pempty[b], kRgNR / kRgHV);
 #endif
     }
     mbar_init(afull, kRgNR);
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  constexpr uint32_t kColY = kRgPBuf * 128;
+  constexpr uint32_t kColY = kRgHV * kRgPBuf * kRgPCols;
 
   if (warp == kRgWarpProd) {
     // ================= producer (one lane): stage t = (unit q0 + t / n, block t % n): the U'_i
@@ -229,7 +237,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     }
   } else if (warp == kRgWarpMma) {
     // ================= MMA warp
-    const uint32_t idp = idesc_f16_f32(128, 128, p.f16 ? 0u : 1u);
+    const uint32_t idp = idesc_f16_f32(128, kRgPCols, p.f16 ? 0u : 1u);
     const uint32_t idg = idesc_f16_f32(128, BP, 2u);   // kind::tf32
     int gpend = -1;   // unit (CTA-local) whose GEMV is pending
     auto gemv = [&](int j) {
@@ -252,16 +260,20 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     for (int t = 0; t < T; ++t) {
       RG_WAIT_FAST(&full[s], sph);
       if (lane == 0) RG_TR(t, 2);
-      if (t >= kRgPBuf) RG_WAIT_FAST(&pempty[pb], pph ^ 1u);
-      if (lane == 0) RG_TR(t, 3);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sa = smem_u32(stages + s * kRgStage);
-        mma_f16_ss(tbase + (uint32_t)(pb * 128), smem_desc_sw32(sa), smem_desc_sw32(sa + 4096), idp, 0u);
-        mma_commit(&pfull[pb]);
-        mma_commit(&sempty[s]);
+#pragma unroll
+      for (int hv = 0; hv < kRgHV; ++hv) {
+        if (t >= kRgPBuf) RG_WAIT_FAST(&pempty[hv * kRgPBuf + pb], pph ^ 1u);
+        if (lane == 0 && hv == 0) RG_TR(t, 3);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(stages + s * kRgStage);
+          mma_f16_ss(tbase + (uint32_t)((hv * kRgPBuf + pb) * kRgPCols), smem_desc_sw32(sa),
+                     smem_desc_sw32(sa + 4096 + hv * kRgPCols * 32), idp, 0u);
+          mma_commit(&pfull[hv * kRgPBuf + pb]);
+          if (hv == kRgHV - 1) mma_commit(&sempty[s]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
       if (gpend >= 0) {   // the previous unit's GEMV, once the next unit's first product is queued
         gemv(gpend);
         gpend = -1;
@@ -277,6 +289,8 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     // ================= restore warps: lane quadrant qd, column group h (kRgCols columns)
     constexpr int NC = kRgCols, NW = NC / 32;
     const int qd = warp & 3, h = warp >> 2;
+    const int hv = (h * NC) / kRgPCols;                // channel half of this warp's columns
+    const int pcol = (h * NC) % kRgPCols;              // its columns inside the half's P buffer
     const int j = qd * 32 + lane;
     const uint32_t lq = (uint32_t)(qd * 32) << 16;
     float acc[NC];
@@ -286,16 +300,17 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     uint32_t sph = 0, pph = 0;
     for (int t = 0; t < T; ++t) {
 #ifdef BS_RG_SPIN
-      mbar_wait(&pfull[pb], pph);
+      mbar_wait(&pfull[hv * kRgPBuf + pb], pph);
 #else
-      mbar_wait_sleep(&pfull[pb], pph);
+      mbar_wait_sleep(&pfull[hv * kRgPBuf + pb], pph);
 #endif
       if (lane == 0 && (warp == 0 || warp == kRgNR - 1)) RG_TR(t, warp == 0 ? 4 : 6);
       tc_fence_after();
       uint32_t m[NC];
 #pragma unroll
       for (int g = 0; g < NW; ++g)
-        tmem_ld32(tbase + lq + (uint32_t)(pb * 128 + h * NC + g * 32), *reinterpret_cast<uint32_t(*)[32]>(m + 32 * g));
+        tmem_ld32(tbase + lq + (uint32_t)((hv * kRgPBuf + pb) * kRgPCols + pcol + g * 32),
+                  *reinterpret_cast<uint32_t(*)[32]>(m + 32 * g));
       mbar_wait(&full[s], sph);   // completed (the MMA warp waited on it): its sign tile is here
       uint32_t nw[NW];
 #pragma unroll
@@ -309,7 +324,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       // stage's sign tile (2 mbarrier arrivals per stage instead of one per warp)
       asm volatile("bar.sync 1, %0;" ::"n"(kRgNR * 32) : "memory");
       if (threadIdx.x == 0) {
-        mbar_arrive(&pempty[pb]);
+        for (int v = 0; v < kRgHV; ++v) mbar_arrive(&pempty[v * kRgPBuf + pb]);
         mbar_arrive(&sempty[s]);
       }
 #else
@@ -317,7 +332,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       // them in registers, so fast warps run ahead instead of meeting the slowest every stage
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&pempty[pb]);
+        mbar_arrive(&pempty[hv * kRgPBuf + pb]);
         mbar_arrive(&sempty[s]);
       }
 #endif
