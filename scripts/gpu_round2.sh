@@ -18,12 +18,18 @@ timeout 600 python bench.py --workload load --steps 10 --warmup 3 > $O/bench_loa
 timeout 600 python bench.py --workload compress --steps 5 --warmup 2 > $O/bench_compress.json 2> $O/bench_compress.err; echo b8=$?
 for wl in c3_up c3_down; do timeout 600 python bench.py --workload $wl --steps 300 --warmup 5 > $O/bench_$wl.json 2> $O/bench_$wl.err; echo pf=$?; done
 for G in 2 4 8; do timeout 300 python bench.py --workload c5 --shard $G --steps 2000 --warmup 20 --no-cpu-baseline; done > $O/shard_c5.jsonl 2> $O/shard.err
-for W in c2 c5; do for B in 1 2 3 4 5 6 7 8 9 12 16; do
+for W in c2 c5; do for B in 1 2 3 4 5 6 8 12 16 24 32 48; do
   timeout 300 python bench.py --workload $W --batch $B --steps 1000 --warmup 20 --no-cpu-baseline
 done; done > $O/bsweep.jsonl 2> $O/bsweep.err
-for W in c2 c5; do for B in 2 4 8; do
-  timeout 300 python bench.py --workload $W --batch $B --kernel $K --steps 1000 --warmup 20 --no-cpu-baseline
+for W in c2 c5; do for B in 2 4 8 16; do
+  timeout 300 python bench.py --workload $W --batch $B --kernel prefill --steps 1000 --warmup 20 --no-cpu-baseline
 done; done > $O/bsweep_prefill.jsonl 2>> $O/bsweep.err
+for W in c2 c5; do for B in 1 3 8 16 32; do
+  timeout 300 python bench.py --workload $W --batch $B --kernel rgemv --steps 1000 --warmup 20 --no-cpu-baseline
+done; done > $O/bsweep_rgemv.jsonl 2>> $O/bsweep.err
+for W in c2 c5; do for B in 6 8 16; do
+  timeout 300 python bench.py --workload $W --batch $B --kernel tc --steps 1000 --warmup 20 --no-cpu-baseline
+done; done > $O/bsweep_decode.jsonl 2>> $O/bsweep.err
 python scripts/bline.py < $O/bsweep.jsonl
 # ncu: launch lists (cold-cache, serialised) and one --set full capture per dominant kernel,
 # each after the same command exited 0 without ncu
@@ -38,4 +44,6 @@ timeout 300 $PCMD > $O/plain_pf.log 2>&1 && timeout 600 ncu --metrics gpu__time_
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"wtile|prefill_gemm" -s 6 -c 2 -o $O/prefill_c3_up $PCMD > $O/ncu_pf.log 2>&1; echo ncu6=$?
 C4CMD="python bench.py --workload c4 --steps 1 --warmup 3 --no-cpu-baseline --no-graph"
 timeout 300 $C4CMD > $O/plain_c4.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"zq_mx|decode_mx" -c 256 --csv --log-file $O/launches_c4.csv $C4CMD > /dev/null 2>&1; echo ncu7=$?
+RCMD="python bench.py --workload c2 --batch 8 --steps 20 --warmup 3 --no-cpu-baseline --no-graph"
+timeout 300 $RCMD > /dev/null 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"rgemv" -s 5 -c 1 -o $O/rg_c2 $RCMD > $O/ncu_rg.log 2>&1; echo ncu8=$?
 echo done

@@ -142,20 +142,15 @@ def main():
             out.append(f"{s['of']:2d} {s['rows']:5d} {d['ms_per_step'] * 1e3:9.2f} {s['hbm_floor_us']:9.2f} {d['roofline']['frac']:6.3f}")
         write("r02_shard_c5.txt", "\n".join(out))
         write("r02_shard_c5.json", "\n".join(json.dumps(d) for d in sh))
-    # batch sweeps: AUTO, forced prefill, forced restore-and-multiply
+    # batch sweeps: AUTO, and each path forced
     parts = []
-    bb = json_lines(os.path.join(R02B, "bsweep.jsonl"))
-    if bb:
-        parts.append(sweep_table(bb, "AUTO path by batch, final dispatch (e4m3 decode B <= 5, restore-and-multiply 6..32, prefill above)"))
-    bs = json_lines(os.path.join(R02, "bsweep.jsonl"))
-    if bs:
-        parts.append(sweep_table(bs, "AUTO path by batch, earlier dispatch (e4m3 decode B <= 8, prefill GEMM from 9)"))
-    bp = json_lines(os.path.join(R02, "bsweep_prefill.jsonl"))
-    if bp:
-        parts.append(sweep_table(bp, "prefill path forced (bench.py --kernel prefill)"))
-    br = json_lines(os.path.join(RG, "rg.jsonl"))
-    if br:
-        parts.append(sweep_table(br, "restore-and-multiply path forced (bench.py --kernel rgemv), first version (cp.async operand staging)"))
+    for fname, title in [("bsweep.jsonl", "AUTO path by batch (e4m3 decode B <= 5, restore-and-multiply 6..32, prefill above)"),
+                         ("bsweep_decode.jsonl", "e4m3 decode forced (bench.py --kernel tc)"),
+                         ("bsweep_rgemv.jsonl", "restore-and-multiply forced (bench.py --kernel rgemv)"),
+                         ("bsweep_prefill.jsonl", "prefill forced (bench.py --kernel prefill)")]:
+        ls = json_lines(os.path.join(R02, fname))
+        if ls:
+            parts.append(sweep_table(ls, title))
     if parts:
         write("r02_batch_sweep.txt", "\n\n".join(parts))
     # launch lists
@@ -178,7 +173,7 @@ def main():
                 "r02_ncu_decode_c5.txt", "c5_n12_b1_g1")
     ncu_summary(os.path.join(R02, "prefill_c3_up.ncu-rep"), "C3 up/gate prefill: wtile + GEMM, one launch each",
                 "r02_ncu_prefill_c3_up.txt", "c3_up_n8_b2048_g1", regex="prefill_gemm")
-    ncu_summary(os.path.join(R02B, "rg_c2.ncu-rep"), "C2 restore-and-multiply (rgemv_kernel<16>, B=8), one launch",
+    ncu_summary(os.path.join(R02, "rg_c2.ncu-rep"), "C2 restore-and-multiply (rgemv_kernel<16>, B=8), one launch",
                 "r02_ncu_rgemv_c2.txt", "c2_n16_b8_g1_rgemv", regex="rgemv")
     # tests, smoke, sanitizer
     for src, dst in [("pytest_gpu.log", "r02_gpu_tests.txt"), ("smoke.log", "r02_smoke.txt")]:
