@@ -154,10 +154,10 @@ __device__ __forceinline__ void zq_load_v(const ZqMxParams& p, long long blk, in
 }
 
 template <int NB>
-__device__ __forceinline__ void zq_mx_unit(const ZqMxParams& p, const int unit, uint8_t* tile, const uint2 (&raw0)[4]) {
+__device__ __forceinline__ void zq_mx_unit(const ZqMxParams& p, const int i, const int q, uint8_t* tile,
+                                           const uint2 (&raw0)[4]) {
   using C = MxCfg<NB>;
   constexpr int N = C::N, TG = ZqTG<NB>::value;
-  const int i = unit / p.nq, q = unit % p.nq;
   const int t = threadIdx.x & 127, tg = threadIdx.x >> 7;
   const int lane = t & 31, rg = t & 3, cq = t >> 2, kb = cq >> 3;
   const int c0 = 4 * cq, col0 = q * kSubK + c0;
@@ -258,20 +258,23 @@ __device__ __forceinline__ void zq_mx_loop(const int units, Locate locate) {
   const ZqMxParams* p;
   int lu;
   locate(u, p, lu);
+  int bi = lu / p->nq, bq = lu - bi * p->nq;   // (block half, chunk) of the unit, once per unit
   uint2 raw[4];
-  if (!p->kfuse) zq_load_v(*p, lu / p->nq, lu % p->nq, raw);
+  if (!p->kfuse) zq_load_v(*p, bi, bq, raw);
 #pragma unroll 1
   for (int it = 0;; ++it) {
     const int un = u + gridDim.x;
     const ZqMxParams* pn = p;
-    int lun = 0;
+    int lun = 0, bin = 0, bqn = 0;
     uint2 rawn[4];
     if (un < units) {   // next unit's V' in flight while this one is computed
       locate(un, pn, lun);
-      if (!pn->kfuse) zq_load_v(*pn, lun / pn->nq, lun % pn->nq, rawn);
+      bin = lun / pn->nq;
+      bqn = lun - bin * pn->nq;
+      if (!pn->kfuse) zq_load_v(*pn, bin, bqn, rawn);
     }
     uint8_t* tile = zq_tiles + (it & 1) * C::kUnit;
-    zq_mx_unit<NB>(*p, lu, tile, raw);
+    zq_mx_unit<NB>(*p, bi, bq, tile, raw);
     __syncthreads();
     uint4* dst = reinterpret_cast<uint4*>(p->zq + (long long)lu * C::kUnit);
     for (int e = threadIdx.x; e < C::kUnit / 16; e += NT) dst[e] = reinterpret_cast<const uint4*>(tile)[e];
@@ -279,6 +282,8 @@ __device__ __forceinline__ void zq_mx_loop(const int units, Locate locate) {
     u = un;
     p = pn;
     lu = lun;
+    bi = bin;
+    bq = bqn;
 #pragma unroll
     for (int j = 0; j < 4; ++j) raw[j] = rawn[j];
   }
