@@ -16,6 +16,9 @@ VARIANTS = {
     "r1s8": ["-DBS_MX_R1=1", "-DBS_MX_NSLOT=8"],
     "r1s12": ["-DBS_MX_R1=1", "-DBS_MX_NSLOT=12"],
     "r2s4": ["-DBS_MX_R1=2"],
+    "st4": ["-DBS_MX_STAGES=4"],
+    "st6": ["-DBS_MX_STAGES=6"],
+    "st12": ["-DBS_MX_STAGES=12"],
     "rg32": ["-DBS_RG_COLS=32"],
     "rgbar": ["-DBS_RG_BARSYNC"],
     "rgsame": ["-DBS_RG_SAMESMSP"],

@@ -152,3 +152,36 @@ def test_append_validation(lib, tmp_path):
         bad[-1] |= 0x80
         assert _err(lambda: st.append(0, 0, bad, u16, v16, s)) == "E_MALFORMED_BUFFER"
         st.append(0, 0, signs[0], u16, v16, s)
+
+
+@pytest.mark.parametrize("kind", ["average", "random"])
+def test_budget_prefix_is_a_contiguous_record_range(lib, tmp_path, kind):
+    """Records written in the universal stack's order (budget.py): the blocks a memory
+    budget admits (prefix_levels) are exactly records [0, L) for L = the prefix length, and each
+    record's size is the Eq.9 block size the budget counts (reading R20)."""
+    from paper_2410_23918_b200 import budget as BG
+    shapes = [(96, 160, 3), (64, 200, 4), (128, 64, 2)]
+    blocks = {}
+    for m, (do, di, nb) in enumerate(shapes):
+        signs, u, v, s = make_random_blocks(nb, do, di, 8, seed=70 + m)
+        blocks[m] = (signs, O.bf16_bits(u), O.bf16_bits(v), s)
+    stack = BG.universal_stack([nb for _, _, nb in shapes], kind=kind, seed=5)
+    p = tmp_path / "u.bstk"
+    with pkg.Store.create(str(p)) as st:
+        for m, i in stack:
+            signs, u, v, s = blocks[m]
+            st.append(m, i, signs[i], u[i], v[i], s if i == 0 else None, factor_dtype="bf16")
+    sizes = [BG.block_bytes(do, di, 8) for do, di, _ in shapes]
+    with pkg.Store.open(str(p)) as st:
+        for r, (m, i) in enumerate(stack):
+            info = st.info(r)
+            assert (info["stack"], info["block"]) == (m, i)
+            assert info["size_bits"] / 8 == sizes[m]
+        for budget in [0, sizes[0], 2.5 * max(sizes), 0.5 * sum(sizes[m] for m, _ in stack), 1e12]:
+            levels = BG.prefix_levels(stack, sizes, budget)
+            L = sum(levels)
+            got = {}
+            for sid, blk, *_ in st.read_range(0, L):
+                got[sid] = got.get(sid, 0) + 1
+                assert blk == got[sid] - 1                     # each stack's blocks in order
+            assert [got.get(m, 0) for m in range(len(shapes))] == levels
