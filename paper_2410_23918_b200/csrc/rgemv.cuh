@@ -60,13 +60,19 @@ constexpr int kRgPCols = 128 / kRgHV;
 #endif
 constexpr int kRgCols = BS_RG_COLS;             // columns of a unit per restore warp (32 or 64)
 constexpr int kRgNR = 4 * (128 / kRgCols);      // restore warps (4 lane quadrants x column groups)
-#ifdef BS_RG_SAMESMSP   // MMA and producer warps on one SMSP (3 idle warps in between)
-constexpr int kRgWarpMma = kRgNR, kRgWarpProd = kRgNR + 4;
-constexpr int kRgWarps = kRgNR + 5;
-#else
-constexpr int kRgWarpMma = kRgNR, kRgWarpProd = kRgNR + 1;
-constexpr int kRgWarps = kRgNR + 2;             // restore warps + MMA + producer
+#ifndef BS_RG_MMA2
+#define BS_RG_MMA2 1
 #endif
+#if BS_RG_MMA2
+// one MMA warp per channel half (warp kRgWarpMma + hv; the first also issues the GEMV), so a late
+// half never holds up the other half's products
+constexpr int kRgMmaWarps = 2;
+#else
+constexpr int kRgMmaWarps = 1;
+#endif
+static_assert(kRgMmaWarps <= kRgHV, "each MMA warp owns at least one channel part");
+constexpr int kRgWarpMma = kRgNR, kRgWarpProd = kRgNR + kRgMmaWarps;
+constexpr int kRgWarps = kRgNR + kRgMmaWarps + 1;   // restore warps + MMA warp(s) + producer
 constexpr int kRgMaxBatch = 32;
 constexpr int kRgStage = 4096 + 4096 + 2048;    // U' tile, V' chunk, sign tile
 constexpr int kRgAImg = 128 * 128 * 4;          // W' unit, tf32
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
 #ifdef BS_RG_BARSYNC
       mbar_init(&sempty[s], 2);   // the P MMA's commit + the restore warps' representative
 #else
-      mbar_init(&sempty[s], 1 + kRgNR);   // the P MMA's commit + every restore warp
+      mbar_init(&sempty[s], kRgMmaWarps + kRgNR);   // the P MMA commit(s) + every restore warp
 #endif
     }
     for (int b = 0; b < kRgHV * kRgPBuf; ++b) {
@@ -235,8 +241,9 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         if (++s == kRgStages) { s = 0; sph ^= 1u; }
       }
     }
-  } else if (warp == kRgWarpMma) {
-    // ================= MMA warp
+  } else if (warp >= kRgWarpMma && warp < kRgWarpMma + kRgMmaWarps) {
+    // ================= MMA warp(s)
+    const int mw = warp - kRgWarpMma;   // with two MMA warps: the channel half this one issues
     const uint32_t idp = idesc_f16_f32(128, kRgPCols, p.f16 ? 0u : 1u);
     const uint32_t idg = idesc_f16_f32(128, BP, 2u);   // kind::tf32
     int gpend = -1;   // unit (CTA-local) whose GEMV is pending
@@ -262,6 +269,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       if (lane == 0) RG_TR(t, 2);
 #pragma unroll
       for (int hv = 0; hv < kRgHV; ++hv) {
+        if (kRgMmaWarps > 1 && hv % kRgMmaWarps != mw) continue;
         if (t >= kRgPBuf) RG_WAIT_FAST(&pempty[hv * kRgPBuf + pb], pph ^ 1u);
         if (lane == 0 && hv == 0) RG_TR(t, 3);
         tc_fence_after();
@@ -270,11 +278,11 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
           mma_f16_ss(tbase + (uint32_t)((hv * kRgPBuf + pb) * kRgPCols), smem_desc_sw32(sa),
                      smem_desc_sw32(sa + 4096 + hv * kRgPCols * 32), idp, 0u);
           mma_commit(&pfull[hv * kRgPBuf + pb]);
-          if (hv == kRgHV - 1) mma_commit(&sempty[s]);
+          if (hv + kRgMmaWarps >= kRgHV) mma_commit(&sempty[s]);   // this warp's last product of the stage
         }
         __syncwarp();
       }
-      if (gpend >= 0) {   // the previous unit's GEMV, once the next unit's first product is queued
+      if (mw == 0 && gpend >= 0) {   // the previous unit's GEMV, once the next unit's first product is queued
         gemv(gpend);
         gpend = -1;
       }
@@ -282,8 +290,10 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       if (++s == kRgStages) { s = 0; sph ^= 1u; }
       if (++pb == kRgPBuf) { pb = 0; pph ^= 1u; }
     }
-    if (gpend >= 0) gemv(gpend);
-    if (elect_one()) mma_commit(yfull);
+    if (mw == 0) {
+      if (gpend >= 0) gemv(gpend);
+      if (elect_one()) mma_commit(yfull);
+    }
     __syncwarp();
   } else if (warp < kRgNR) {
     // ================= restore warps: lane quadrant qd, column group h (kRgCols columns)

@@ -23,7 +23,8 @@ VARIANTS = {
     "rgbar": ["-DBS_RG_BARSYNC"],
     "rgsame": ["-DBS_RG_SAMESMSP"],
     "rgspinfast": ["-DBS_RG_SPIN_FAST"],
-    "rghv1": ["-DBS_RG_HALVES=1"],
+    "rghv1": ["-DBS_RG_HALVES=1", "-DBS_RG_MMA2=0"],
+    "rgmma1": ["-DBS_RG_MMA2=0"],
     "rghv4": ["-DBS_RG_HALVES=4"],
     "rg32same": ["-DBS_RG_COLS=32", "-DBS_RG_SAMESMSP"],
     "rgspin": ["-DBS_RG_SPIN"],
