@@ -297,11 +297,11 @@ def test_zero_activation_segments(bs):
 
 
 # ------------------------------------------------------------------ host buffers (e2e path)
-@pytest.mark.parametrize("batch", [1, 3, 40])
+@pytest.mark.parametrize("batch", [1, 3, 12, 40])
 def test_host_buffers(bs, batch):
-    """bitstack_matmul with host x / y: pinned buffers (read / written in place by the decode
-    kernels, or staged for the prefill path) and pageable ones (staged) give the same y as
-    device buffers."""
+    """bitstack_matmul with host x / y: pinned buffers (read / written in place by the decode and
+    restore-and-multiply kernels, or staged for the prefill path) and pageable ones (staged) give
+    the same y as device buffers."""
     g, s32, blocks = compress_case(256, 384, 3, "bf16", 81)
     lay = make_layer(bs, 256, 384, blocks, s32, "bf16")
     x = torch.from_numpy(make_x(batch, g, 5).astype(np.float32)).to(torch.bfloat16)
@@ -801,6 +801,21 @@ def test_rgemv_dispatch_bf16_y_and_determinism(bs):
     with pytest.raises(bs.BitStackError) as e:
         gpu_y(lay, make_x(33, g, 81))
     assert e.value.name == "E_UNSUPPORTED"
+    # CUDA-graph capture of a warmed-up call, replayed: same bytes as the eager call
+    xg = torch.from_numpy(x.astype(np.float32)).cuda()
+    yg = torch.empty((12, 512), dtype=torch.float32, device="cuda")
+    lay.matmul_raw(xg.data_ptr(), bs.F32, yg.data_ptr(), bs.F32, 12, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    y_eager = yg.clone()
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(graph, stream=cap):
+        lay.matmul_raw(xg.data_ptr(), bs.F32, yg.data_ptr(), bs.F32, 12, cap.cuda_stream)
+    yg.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(yg, y_eager)
 
 
 # ------------------------------------------------------------------ output bounds (guard bands)
