@@ -55,12 +55,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait with a suspend-time hint: a warp whose phase is not complete is parked by the hardware
 // until the phase completes (or the hint expires) instead of re-issuing try_wait, so long waits
 // do not take issue slots from the working warps of the SMSP.
+#ifndef BS_SLEEP_NS
+#define BS_SLEEP_NS 1000000u
+#endif
 __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)BS_SLEEP_NS)
       : "memory");
   return ok != 0;
 }

@@ -325,7 +325,12 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       uint32_t nw[NW];
 #pragma unroll
       for (int g = 0; g < NW; ++g)
-        nw[g] = ~*reinterpret_cast<const uint32_t*>(stages + s * kRgStage + 8192 + j * 16 + (h * NW + g) * 4);
+      {   // explicit shared-space load (a generic load of this word measured as the loop's top stall)
+        uint32_t w;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w)
+                     : "r"(smem_u32(stages + s * kRgStage + 8192 + j * 16 + (h * NW + g) * 4)));
+        nw[g] = ~w;
+      }
       tmem_ld_wait();
       if (lane == 0 && warp == 0) RG_TR(t, 1);
       tc_fence_before();

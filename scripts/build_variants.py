@@ -25,6 +25,9 @@ VARIANTS = {
     "rgspinfast": ["-DBS_RG_SPIN_FAST"],
     "rghv1": ["-DBS_RG_HALVES=1", "-DBS_RG_MMA2=0"],
     "rgmma1": ["-DBS_RG_MMA2=0"],
+    "sl20k": ["-DBS_SLEEP_NS=20000u"],
+    "sl1k": ["-DBS_SLEEP_NS=1000u"],
+    "sl200": ["-DBS_SLEEP_NS=200u"],
     "rghv4": ["-DBS_RG_HALVES=4"],
     "rg32same": ["-DBS_RG_COLS=32", "-DBS_RG_SAMESMSP"],
     "rgspin": ["-DBS_RG_SPIN"],
