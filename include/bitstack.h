@@ -101,8 +101,8 @@ typedef struct {
  * rank k, factors stored as factor_dtype (Q7: the paper stores FP16).
  * Allocates all device memory up front on `device`.
  * k <= 16 is stored zero-padded to 16 ranks; 16 < k <= 32 (the paper's k ablation)
- * is stored as two 16-rank halves that share the block's sign tile (every path handles a
- * half as a block of its own, so the decode streams that sign tile once per half).
+ * is stored as two 16-rank halves that share the block's sign tile (at batch 1 the e4m3 decode
+ * contracts both halves in one pass over that tile; the other paths handle a half as a block).
  * Errors: E_INVALID_ARG (k<1, k>min(d_out,d_in), k>32, n_capacity<1, bad dtype, out==NULL),
  *         E_DIM_MISMATCH (bad row range), E_UNSUPPORTED (device not sm_100), E_OOM, E_CUDA. */
 BITSTACK_API bitstack_status bitstack_create(int64_t d_out, int64_t d_in, int32_t k, int32_t n_capacity,
@@ -162,14 +162,16 @@ BITSTACK_API bitstack_status bitstack_set_num_blocks(bitstack_layer layer, int32
  *   x : [batch, d_in] row-major, dtype F32 | BF16 | F16
  *   y : [batch, row_end-row_begin] row-major, dtype F32 | BF16, overwritten
  * x and y may be device or host memory.  Small (<= 1 MiB) pinned host buffers are read /
- * written in place by the decode kernels (their PCIe traffic is the transfer); other host
+ * written in place by the decode and restore-and-multiply kernels (their PCIe traffic is the
+ * transfer); other host
  * buffers are staged through device memory with cudaMemcpyAsync on `stream` (pageable host
- * memory makes those copies synchronous).  Staging and prefill workspaces are allocated on
- * the first call that needs them (which therefore must not be under CUDA-graph capture).
+ * memory makes those copies synchronous).  Staging and path workspaces (Zq units, prefill and
+ * restore-and-multiply images, TMA descriptors) are allocated on the first call that needs them
+ * (which therefore must not be under CUDA-graph capture).
  * x and y must not alias.  batch == 0 is a no-op; n == 0 writes y = 0.
  * Asynchronous on `stream`; argument errors are reported synchronously.
  * Numerics, tensor-core paths, accumulation in fp32 throughout:
- *   - BF16/F16 factors, decode (batch <= 5): S as exact e4m3 +-1, the product
+ *   - BF16/F16 factors, decode (batch <= 5, or any batch on < 128 local rows): S as exact e4m3 +-1, the product
  *     Z = V (.) (x/s) as three e4m3 digits per (rank, token) with power-of-two
  *     scales per 32-channel block (MX block scaling: digit 0 puts the block
  *     maximum in [128, 256), digit d is scaled 2^-4d further): error <= 2^-13 of
@@ -193,8 +195,8 @@ BITSTACK_API bitstack_status bitstack_matmul(bitstack_layer layer, const void* x
  * bitstack_matmul's layouts (xs[i] may be the same buffer for several members).
  * When count <= 8, 1 <= batch <= 5, the members are distinct handles on one device on the
  * MX e4m3 decode path (bf16/f16 factors, d_in % 8 == 0, AUTO or TC kernel) and all xs / ys are
- * 16-byte aligned device buffers, the whole group runs as ONE Zq launch and ONE decode launch
- * per chunk of <= 8 tokens, whose CTAs are shared out among the members in proportion to their
+ * 16-byte aligned device buffers, the whole group runs as ONE Zq launch and ONE decode launch,
+ * whose CTAs are shared out among the members in proportion to their
  * work; members at level n_i == 0 get ys[i] = 0 (a memset) and no share of the launches (no
  * launch at all when every member is at level 0); otherwise the members run one after another through
  * bitstack_matmul (from 6 tokens that is the restore-and-multiply path of each member).  Results are
