@@ -130,6 +130,9 @@ def main():
         ls = json_lines(src)
         if ls:
             write(f"r02_{name}.json", "\n".join(json.dumps(d) for d in ls))
+    rb = json_lines(os.path.join(R02, "bench_rgemv_b8.jsonl"))
+    if rb:
+        write("r02_bench_rgemv_b8.json", "\n".join(json.dumps(d) for d in rb))
     # C5 per-rank shards
     sh = json_lines(os.path.join(R02, "shard_c5.jsonl"))
     if sh:
@@ -144,7 +147,9 @@ def main():
         write("r02_shard_c5.json", "\n".join(json.dumps(d) for d in sh))
     # batch sweeps: AUTO, and each path forced
     parts = []
-    for fname, title in [("bsweep.jsonl", "AUTO path by batch (e4m3 decode B <= 5, restore-and-multiply 6..32, prefill above)"),
+    for fname, title in [("bsweep.jsonl", "AUTO path by batch (e4m3 decode B <= 5, restore-and-multiply 6..32, prefill above);\n"
+                          "# the rgemv rows here still carry the earlier issue roofline ('alu'); their TMEM-read\n"
+                          "# fraction is in the forced table below"),
                          ("bsweep_decode.jsonl", "e4m3 decode forced (bench.py --kernel tc)"),
                          ("bsweep_rgemv.jsonl", "restore-and-multiply forced (bench.py --kernel rgemv)"),
                          ("bsweep_prefill.jsonl", "prefill forced (bench.py --kernel prefill)")]:
