@@ -1011,12 +1011,15 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.shard == 1:
-        rows_s = 256
-        dt, _ = oracle_sample_time(w, n, batch, rows_s, 1, 0, seed_for(2, 0, "blocks"))
+        # bounded sample, ~10-15 s of CPU work: calibrate on 256 rows, then calls of ~3 s each
+        dt0, _ = oracle_sample_time(w, n, batch, 256, 1, 0, seed_for(2, 0, "blocks"))
+        rows_s = int(min(d_out, 256 * max(1, int(3.0 / max(dt0, 1e-3)))))
+        steps_s = int(max(1, min(10, round(12.0 / max(dt0 * rows_s / 256, 1e-3)))))
+        dt, _ = oracle_sample_time(w, n, batch, rows_s, steps_s, 0, seed_for(2, 0, "blocks"))
         cpu = {"value": step_units(w, d_out, batch, n) / (dt * d_out / rows_s), "unit": unit_name(w),
                "cores": cpu_cores(), "kind": "oracle",
                "sample": f"dense oracle (fp64 numpy, Eq.8+Eq.4) for {rows_s} of {d_out} output rows, "
-                         f"all {n} blocks, 1 call ({dt:.2f} s), scaled to the whole layer"}
+                         f"all {n} blocks, {steps_s} calls ({dt * steps_s:.1f} s of CPU work), scaled to the whole layer"}
 
     # N > 1: the NCCL all-gather of the output slices timed alone (kernel,
     # collective and end-to-end reported separately); all ranks take part
