@@ -527,12 +527,23 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
     return BITSTACK_OK;
   });
   if (rs) return rs;
-  // CTAs: each row tile split into `splits` contiguous unit ranges so that the grid fills the SMs
-  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(L->sm_count / std::max(1, L->row_tiles), L->nq));
-  const int grid = L->row_tiles * splits;
+  // CTAs: either each row tile split into `splits` unit ranges (whole row tiles per CTA), or one
+  // CTA per SM over a balanced contiguous range of the row_tiles x nq (row tile, unit) pairs,
+  // whichever has the shorter longest range (a range that spans row tiles costs about one unit
+  // more: a drain and a partial slot per segment); kmax = partial slots per CTA
+  const int64_t W = (int64_t)L->row_tiles * L->nq;
+  const int splits_r = (int)std::max<int64_t>(1, std::min<int64_t>(L->sm_count / std::max(1, L->row_tiles), L->nq));
+  const int64_t span_r = (L->nq + splits_r - 1) / splits_r;
+  const int grid_b = (int)std::min<int64_t>(W, L->sm_count);
+  const int64_t span_b = (W + grid_b - 1) / grid_b + 1;
+  static const int mode_env = [] { const char* e = getenv("BS_RG_MODE"); return e ? atoi(e) : 0; }();   // A/B override
+  const bool balanced = mode_env == 2 || (mode_env != 1 && span_b < span_r);
+  const int grid = balanced ? grid_b : L->row_tiles * splits_r;
+  const int kmax = balanced ? (int)((span_b - 1 + L->nq - 1) / L->nq + 1) : 1;
+  if (kmax > 32) return fail(BITSTACK_E_UNSUPPORTED, "restore-and-multiply: too many row tiles per CTA");
   rs = grow(L, &L->rg_x, &L->rg_x_bytes, (int64_t)L->nq * C::kXImg, st);
   if (rs) return rs;
-  rs = grow(L, &L->rg_part, &L->rg_part_bytes, (int64_t)grid * BP * 128 * 4, st);
+  rs = grow(L, &L->rg_part, &L->rg_part_bytes, (int64_t)grid * kmax * BP * 128 * 4, st);
   if (rs) return rs;
   const long long pieces = (long long)L->nq * BP * 32;
   const int xgrid = (int)std::min<long long>((pieces + 255) / 256, (long long)L->sm_count * 8);
@@ -565,7 +576,8 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
   rp.rows_pad = L->rows_pad;
   rp.rows_local = (int)L->rows_local;
   rp.row_tiles = L->row_tiles;
-  rp.splits = splits;
+  rp.kmax = kmax;
+  rp.splits = balanced ? 0 : splits_r;
   rp.batch = (int)batch;
   rp.f16 = L->dev_fdt == 2 ? 1 : 0;
   rp.trace = reinterpret_cast<long long*>(g_dbg_acc);

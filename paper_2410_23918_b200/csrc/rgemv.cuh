@@ -8,7 +8,8 @@
 // tokens on its tensor time exceeds the cost of restoring W' (2.5 ALU ops per element and block
 // plus a K = 16 MMA); the prefill path restores W' once but writes and re-reads it through HBM
 // as an fp16 operand and pads the GEMM to 128 tokens.  Here each CTA owns one 128-row tile and a
-// contiguous range of 128-column units and, per (unit, block):
+// balanced contiguous range of (row tile, 128-channel unit) pairs (row-tile-major; a range can span
+// row-tile segments, each with its own TMEM y buffer and partial slot) and, per (unit, block):
 //   producer warp   TMA tensor copies of the U'_i tile and the V'_i chunk (32-byte swizzle = the
 //                   UMMA K-major layout), one bulk copy of the 128 x 128 sign tile; stage ring
 //   MMA warp        P_i = U'_i V'_i^T (tcgen05 kind::f16, M128 N128 K16: exact products, fp32
@@ -34,14 +35,16 @@ struct RgParams {
   const uint16_t* u;      // [n x kh][rows_pad][16] U' (bf16 / f16 storage)
   const uint16_t* v;      // [n x kh][d_in_pad][16] V'
   const uint8_t* ximg;    // [nq] X' images of BP x 128 tf32 (rg_xprep_kernel)
-  float* part;            // [grid][BP][128] fp32 partial y of each CTA
+  float* part;            // [grid][kmax][BP][128] fp32 partial y of each (CTA, row-tile segment)
   int* counters;          // [row_tiles], zero on entry and on exit
   void* y;
   long long y_stride;
   int y_dtype;            // 0 f32, 1 bf16
   int n;                  // active 16-rank blocks (halves)
   int ksh;                // sign tile of block i is i >> ksh
-  int nq, rows_pad, rows_local, row_tiles, splits, batch, f16;
+  int nq, rows_pad, rows_local, row_tiles, batch, f16;
+  int kmax;               // max row-tile segments per CTA (partial slots per CTA)
+  int splits;             // > 0: CTA b = (row tile b / splits, unit range b % splits of it); 0: balanced
   long long* trace;       // timing build (-DBS_RG_TRACE, scripts/rg_trace.py): per-stage stamps of CTA 0
 };
 
@@ -167,16 +170,33 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
   uint64_t* aempty = afull + 1;               // commit of the unit's GEMV MMAs
   uint64_t* xfull = aempty + 1;               // [2] bulk copy of an X' unit
   uint64_t* xempty = xfull + 2;               // [2] commit of the GEMV that read it
-  uint64_t* yfull = xempty + 2;               // commit of the last GEMV
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yfull + 1);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* yfull = xempty + 2;               // [2] commit of a segment's last GEMV (y buffer seg & 1)
+  uint64_t* yempty = yfull + 2;               // [2] the 4 draining warps read y buffer seg & 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yempty + 2);
+  int* fin = reinterpret_cast<int*>(tmem_slot + 1);   // [kmax + 1] row tiles this CTA finalises
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
-  const int mt = cta / p.splits, sp = cta % p.splits;
-  const int q0 = (int)((long long)p.nq * sp / p.splits), q1 = (int)((long long)p.nq * (sp + 1) / p.splits);
+  // balanced work: the (row tile, unit) pairs in row-tile-major order, a contiguous range per
+  // CTA; a range spans row-tile segments (each with its own partial slot and y buffer)
+  const long long W = (long long)p.row_tiles * p.nq;
+  const int G = gridDim.x;
+  auto range_of = [&](int b, long long& a, long long& e) {   // CTA b's (row tile, unit) range
+    if (p.splits > 0) {
+      const int m = b / p.splits, k = b % p.splits;
+      a = (long long)m * p.nq + (long long)p.nq * k / p.splits;
+      e = (long long)m * p.nq + (long long)p.nq * (k + 1) / p.splits;
+    } else {
+      a = W * b / G;
+      e = W * (b + 1) / G;
+    }
+  };
+  long long w0, w1;
+  range_of(cta, w0, w1);
+  const int U = (int)(w1 - w0);               // units of this CTA
+  const int mt0 = (int)(w0 / p.nq), qa = (int)(w0 % p.nq);
   const int n = p.n;
-  const int T = (q1 - q0) * n;                // stages of this CTA
+  const int T = U * n;                        // stages of this CTA
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRgStages; ++s) {
@@ -201,7 +221,10 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       mbar_init(&xfull[b], 1);
       mbar_init(&xempty[b], 1);
     }
-    mbar_init(yfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&yfull[b], 1);
+      mbar_init(&yempty[b], 4);
+    }
     fence_mbar_init();
   }
   if (warp == kRgWarpProd) tmem_alloc<512>(tmem_slot);
@@ -209,26 +232,27 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  constexpr uint32_t kColY = kRgHV * kRgPBuf * kRgPCols;
+  constexpr uint32_t kColY = kRgHV * kRgPBuf * kRgPCols;   // two y buffers of BP columns
 
   if (warp == kRgWarpProd) {
-    // ================= producer (one lane): stage t = (unit q0 + t / n, block t % n): the U'_i
+    // ================= producer (one lane): stage t = (the CTA's unit t / n, block t % n): the U'_i
     // tile and the V'_i chunk by TMA tensor copies (32-byte swizzle: the UMMA K-major layout),
     // the sign tile by a bulk copy, all completing as tx bytes on full[s]
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       const int dpad = p.nq * 128;
-      auto issue_x = [&](int u) {   // X' unit u of this CTA into buffer u & 1
+      int qx = qa;   // unit (channel chunk) of the next X' load; issue_x is called for u = 0, 1, 2, ...
+      auto issue_x = [&](int u) {   // X' of the CTA's unit u into buffer u & 1
         if (u >= 2) mbar_wait_sleep(&xempty[u & 1], (uint32_t)(((u >> 1) - 1) & 1));
         mbar_arrive_expect_tx(&xfull[u & 1], C::kXImg);
-        bulk_g2s(ximg + (u & 1) * C::kXImg, p.ximg + (long long)(q0 + u) * C::kXImg, C::kXImg, &xfull[u & 1], pol);
+        bulk_g2s(ximg + (u & 1) * C::kXImg, p.ximg + (long long)qx * C::kXImg, C::kXImg, &xfull[u & 1], pol);
+        if (++qx == p.nq) qx = 0;
       };
-      if (q1 > q0) issue_x(0);
-      if (q1 > q0 + 1) issue_x(1);
-      int s = 0, u = 0, i = 0;
+      if (U > 0) issue_x(0);
+      if (U > 1) issue_x(1);
+      int s = 0, u = 0, i = 0, qq = qa, mt = mt0;
       uint32_t sph = 0;
       for (int t = 0; t < T; ++t) {
-        const int qq = q0 + u;
         if (i == 0 && u >= 2) issue_x(u);
         if (t >= kRgStages) RG_WAIT_FAST(&sempty[s], sph ^ 1u);
         RG_TR(t, 0);
@@ -237,7 +261,11 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         tma_2d(st, &p.tmu, 0, i * p.rows_pad + mt * 128, &full[s]);
         tma_2d(st + 4096, &p.tmv, 0, i * dpad + qq * 128, &full[s]);
         bulk_g2s(st + 8192, p.signs + ((long long)(i >> p.ksh) * p.nq + qq) * p.rows_pad + mt * 128, 2048, &full[s], pol);
-        if (++i == n) { i = 0; ++u; }
+        if (++i == n) {
+          i = 0;
+          ++u;
+          if (++qq == p.nq) { qq = 0; ++mt; }
+        }
         if (++s == kRgStages) { s = 0; sph ^= 1u; }
       }
     }
@@ -247,18 +275,26 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     const uint32_t idp = idesc_f16_f32(128, kRgPCols, p.f16 ? 0u : 1u);
     const uint32_t idg = idesc_f16_f32(128, BP, 2u);   // kind::tf32
     int gpend = -1;   // unit (CTA-local) whose GEMV is pending
-    auto gemv = [&](int j) {
+    int gq = qa, gseg = 0;   // channel chunk and segment of the next GEMV (called for j = 0, 1, 2, ...)
+    auto gemv = [&](int j) {   // the CTA's unit j: y buffer of its segment
+      const int seg = gseg;
+      const bool first = j == 0 || gq == 0;
+      const bool last = j == U - 1 || gq == p.nq - 1;
+      if (++gq == p.nq) { gq = 0; ++gseg; }
+      if (first && seg >= 2) RG_WAIT_FAST(&yempty[seg & 1], (uint32_t)(((seg >> 1) - 1) & 1));
       RG_WAIT_FAST(afull, (uint32_t)(j & 1));
       RG_WAIT_FAST(&xfull[j & 1], (uint32_t)((j >> 1) & 1));
       tc_fence_after();
       if (elect_one()) {
         const uint32_t a0 = smem_u32(aimg), x0 = smem_u32(ximg + (j & 1) * C::kXImg);
+        const uint32_t yc = tbase + kColY + (uint32_t)((seg & 1) * BP);
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
-          mma_tf32_ss(tbase + kColY, smem_desc_kmajor(a0 + kk * 256, 128, 4096),
-                      smem_desc_kmajor(x0 + kk * 256, 128, 4096), idg, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_tf32_ss(yc, smem_desc_kmajor(a0 + kk * 256, 128, 4096), smem_desc_kmajor(x0 + kk * 256, 128, 4096), idg,
+                      (!first || kk > 0) ? 1u : 0u);
         mma_commit(aempty);
         mma_commit(&xempty[j & 1]);
+        if (last) mma_commit(&yfull[seg & 1]);
       }
       __syncwarp();
     };
@@ -290,10 +326,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       if (++s == kRgStages) { s = 0; sph ^= 1u; }
       if (++pb == kRgPBuf) { pb = 0; pph ^= 1u; }
     }
-    if (mw == 0) {
-      if (gpend >= 0) gemv(gpend);
-      if (elect_one()) mma_commit(yfull);
-    }
+    if (mw == 0 && gpend >= 0) gemv(gpend);
     __syncwarp();
   } else if (warp < kRgNR) {
     // ================= restore warps: lane quadrant qd, column group h (kRgCols columns)
@@ -306,7 +339,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     float acc[NC];
 #pragma unroll
     for (int l = 0; l < NC; ++l) acc[l] = 0.f;
-    int s = 0, pb = 0, u = 0, i = 0;
+    int s = 0, pb = 0, u = 0, i = 0, uq = qa, useg = 0;
     uint32_t sph = 0, pph = 0;
     for (int t = 0; t < T; ++t) {
 #ifdef BS_RG_SPIN
@@ -383,20 +416,39 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         if (lane == 0) mbar_arrive(afull);
 #pragma unroll
         for (int l = 0; l < NC; ++l) acc[l] = 0.f;
+        if (h == 0 && u != U - 1 && uq == p.nq - 1) {   // a segment ends mid-range: drain it now
+          const int seg = useg;
+          mbar_wait_sleep(&yfull[seg & 1], (uint32_t)((seg >> 1) & 1));
+          tc_fence_after();
+          float* slot = p.part + ((long long)cta * p.kmax + seg) * BP * 128;
+#pragma unroll
+          for (int b0 = 0; b0 < BP; b0 += 16) {
+            uint32_t yv[16];
+            tmem_ld16(tbase + lq + kColY + (uint32_t)((seg & 1) * BP + b0), yv);
+            tmem_ld_wait();
+#pragma unroll
+            for (int b = 0; b < 16; ++b) slot[(b0 + b) * 128 + j] = __uint_as_float(yv[b]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&yempty[seg & 1]);
+        }
         i = 0;
         ++u;
+        if (++uq == p.nq) { uq = 0; ++useg; }
       }
       if (++s == kRgStages) { s = 0; sph ^= 1u; }
       if (++pb == kRgPBuf) { pb = 0; pph ^= 1u; }
     }
-    if (h == 0) {   // y_acc -> this CTA's partial slot
-      mbar_wait_sleep(yfull, 0u);
+    if (h == 0 && U > 0) {   // the range's last segment: y buffer -> partial slot
+      const int seg = (int)((w1 - 1) / p.nq) - mt0;
+      mbar_wait_sleep(&yfull[seg & 1], (uint32_t)((seg >> 1) & 1));
       tc_fence_after();
-      float* slot = p.part + (long long)cta * BP * 128;
+      float* slot = p.part + ((long long)cta * p.kmax + seg) * BP * 128;
 #pragma unroll
       for (int b0 = 0; b0 < BP; b0 += 16) {
         uint32_t yv[16];
-        tmem_ld16(tbase + lq + kColY + (uint32_t)b0, yv);
+        tmem_ld16(tbase + lq + kColY + (uint32_t)((seg & 1) * BP + b0), yv);
         tmem_ld_wait();
 #pragma unroll
         for (int b = 0; b < 16; ++b) slot[(b0 + b) * 128 + j] = __uint_as_float(yv[b]);
@@ -404,26 +456,54 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     }
   }
 
-  // ---- teardown; the row tile's last CTA sums the partial slots in CTA order and writes y
+  // ---- teardown; the last CTA to finish a row tile sums its partial slots in CTA order and writes y
   __threadfence();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == kRgWarpProd) tmem_dealloc<512>(tbase);
+  auto cover = [&](int mt, int& b_lo, int& b_hi) {   // CTAs whose range meets row tile mt
+    if (p.splits > 0) {
+      b_lo = mt * p.splits;
+      b_hi = b_lo + p.splits - 1;
+      return;
+    }
+    const long long a = (long long)mt * p.nq, e = a + p.nq;
+    int b = (int)(a * G / W);
+    while (b > 0 && W * b / G > a) --b;
+    while (W * (b + 1) / G <= a) ++b;
+    b_lo = b;
+    while (b + 1 < G && W * (b + 1) / G < e) ++b;
+    b_hi = b;
+  };
   if (threadIdx.x == 0) {
     __threadfence();
-    const int prev = atomicAdd(p.counters + mt, 1);
-    *last_flag = (prev == p.splits - 1);
+    int nf = 0;
+    const int nseg = U > 0 ? (int)((w1 - 1) / p.nq) - mt0 + 1 : 0;
+    for (int k = 0; k < nseg; ++k) {
+      int b_lo, b_hi;
+      cover(mt0 + k, b_lo, b_hi);
+      const int prev = atomicAdd(p.counters + mt0 + k, 1);
+      if (prev == b_hi - b_lo) fin[1 + nf++] = mt0 + k;
+    }
+    fin[0] = nf;
   }
   __syncthreads();
-  if (*last_flag) {
+  for (int f = 0; f < fin[0]; ++f) {
     __threadfence();
-    const float* base = p.part + (long long)mt * p.splits * BP * 128;
+    const int mt = fin[1 + f];
+    int b_lo, b_hi;
+    cover(mt, b_lo, b_hi);
     for (int e = threadIdx.x; e < 128 * p.batch; e += blockDim.x) {
       const int b = e / 128, r = e % 128;
       const long long row = (long long)mt * 128 + r;
       float a = 0.f;
-      for (int k = 0; k < p.splits; ++k) a += __ldcg(base + (long long)k * BP * 128 + b * 128 + r);
+      for (int c = b_lo; c <= b_hi; ++c) {
+        long long ca, ce;
+        range_of(c, ca, ce);
+        const int seg = mt - (int)(ca / p.nq);
+        a += __ldcg(p.part + ((long long)c * p.kmax + seg) * BP * 128 + b * 128 + r);
+      }
       if (row < p.rows_local) {
         const long long o = (long long)b * p.y_stride + row;
         if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = a;
