@@ -489,21 +489,23 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     fin[0] = nf;
   }
   __syncthreads();
+  long long* slot_base = reinterpret_cast<long long*>(stages);   // the stage ring is idle now
   for (int f = 0; f < fin[0]; ++f) {
     __threadfence();
     const int mt = fin[1 + f];
     int b_lo, b_hi;
     cover(mt, b_lo, b_hi);
+    for (int c = b_lo + (int)threadIdx.x; c <= b_hi; c += blockDim.x) {   // each covering CTA's slot, once
+      long long ca, ce;
+      range_of(c, ca, ce);
+      slot_base[c - b_lo] = ((long long)c * p.kmax + (mt - (int)(ca / p.nq))) * BP * 128;
+    }
+    __syncthreads();
     for (int e = threadIdx.x; e < 128 * p.batch; e += blockDim.x) {
       const int b = e / 128, r = e % 128;
       const long long row = (long long)mt * 128 + r;
       float a = 0.f;
-      for (int c = b_lo; c <= b_hi; ++c) {
-        long long ca, ce;
-        range_of(c, ca, ce);
-        const int seg = mt - (int)(ca / p.nq);
-        a += __ldcg(p.part + ((long long)c * p.kmax + seg) * BP * 128 + b * 128 + r);
-      }
+      for (int c = 0; c <= b_hi - b_lo; ++c) a += __ldcg(p.part + slot_base[c] + b * 128 + r);
       if (row < p.rows_local) {
         const long long o = (long long)b * p.y_stride + row;
         if (p.y_dtype == 0) reinterpret_cast<float*>(p.y)[o] = a;
@@ -511,6 +513,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       }
     }
     if (threadIdx.x == 0) p.counters[mt] = 0;
+    __syncthreads();   // slot_base is rewritten for the next row tile
   }
 }
 
