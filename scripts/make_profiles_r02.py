@@ -147,9 +147,7 @@ def main():
         write("r02_shard_c5.json", "\n".join(json.dumps(d) for d in sh))
     # batch sweeps: AUTO, and each path forced
     parts = []
-    for fname, title in [("bsweep.jsonl", "AUTO path by batch (e4m3 decode B <= 5, restore-and-multiply 6..32, prefill above);\n"
-                          "# the rgemv rows here still carry the earlier issue roofline ('alu'); their TMEM-read\n"
-                          "# fraction is in the forced table below"),
+    for fname, title in [("bsweep.jsonl", "AUTO path by batch (e4m3 decode B <= 5, restore-and-multiply 6..32, prefill above)"),
                          ("bsweep_decode.jsonl", "e4m3 decode forced (bench.py --kernel tc)"),
                          ("bsweep_rgemv.jsonl", "restore-and-multiply forced (bench.py --kernel rgemv)"),
                          ("bsweep_prefill.jsonl", "prefill forced (bench.py --kernel prefill)")]:
