@@ -176,6 +176,8 @@ def main():
                 "r02_ncu_decode_c5.txt", "c5_n12_b1_g1")
     ncu_summary(os.path.join(R02, "prefill_c3_up.ncu-rep"), "C3 up/gate prefill: wtile + GEMM, one launch each",
                 "r02_ncu_prefill_c3_up.txt", "c3_up_n8_b2048_g1", regex="prefill_gemm")
+    ncu_summary(os.path.join(R02, "rg_c5.ncu-rep"), "C5 restore-and-multiply (rgemv_kernel<16>, B=8, balanced ranges), one launch",
+                "r02_ncu_rgemv_c5.txt", "c5_n12_b8_g1_rgemv", regex="rgemv")
     ncu_summary(os.path.join(R02, "rg_c2.ncu-rep"), "C2 restore-and-multiply (rgemv_kernel<16>, B=8), one launch",
                 "r02_ncu_rgemv_c2.txt", "c2_n16_b8_g1_rgemv", regex="rgemv")
     # tests, smoke, sanitizer
