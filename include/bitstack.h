@@ -72,15 +72,14 @@ typedef enum {
 typedef enum {
   BITSTACK_KERNEL_AUTO = 0,   /* bf16 / f16 factors: 1-5 tokens the tcgen05 e4m3 decode kernel; with
                                  >= 128 local rows, 6-32 tokens the restore-and-multiply kernel and
-                                 more the restored-tile GEMM (prefill, n <= 16), else the decode
+                                 more the restored-tile GEMM (prefill), else the decode
                                  kernel; fp32 factors the tcgen05 fp16 decode kernel when supported,
                                  else SIMT */
   BITSTACK_KERNEL_TC = 1,     /* force the tcgen05/TMEM decode kernel (E_UNSUPPORTED if not possible) */
   BITSTACK_KERNEL_SIMT = 2,   /* force the CUDA-core FP32 reference kernel (any shape) */
   BITSTACK_KERNEL_PREFILL = 3,/* force the prefill path: W' = sum_i S_i (.) U_i V_i^T restored per
-                                 tile on tcgen05, then Y = (X diag(1/s)) W'^T on tcgen05 with fp16
-                                 operands (E_UNSUPPORTED unless bf16 / f16 factors,
-                                 n <= 16) */
+                                 128 x 128 unit on tcgen05 into an fp16 operand image, then Y = (X diag(1/s)) W'^T on tcgen05 with fp16
+                                 operands (E_UNSUPPORTED unless bf16 / f16 factors) */
   BITSTACK_KERNEL_RGEMV = 4   /* force the restore-and-multiply path: W' restored per 128 x 128 unit
                                  inside the SM (tcgen05 U'V'^T + sign application), y += W' X'^T on
                                  tcgen05 in tf32; W' never reaches HBM (E_UNSUPPORTED unless bf16 /

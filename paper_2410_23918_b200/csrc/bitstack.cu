@@ -191,7 +191,7 @@ MatmulPath choose_path(bitstack_layer L, int64_t batch) {
   if (L->kernel != BITSTACK_KERNEL_AUTO || !fp16ok) return kPathDecode;
   // (shards of >= one 128-row tile: over a handful of rows the tf32 operand rounding shows most)
   if (batch >= kRgMinBatch && batch <= bs::kRgMaxBatch && L->rows_local >= 128) return kPathRgemv;
-  if (L->n_act * L->kh <= 16 && prefill_auto(L, batch)) return kPathPrefill;
+  if (prefill_auto(L, batch)) return kPathPrefill;
   return kPathDecode;
 }
 
@@ -404,6 +404,8 @@ bitstack_status grow(bitstack_layer L, uint8_t** buf, int64_t* have, int64_t nee
   return BITSTACK_OK;
 }
 
+bitstack_status launch_wrestore(bitstack_layer L, int kc, int rt_img, cudaStream_t st);
+
 // Large-batch path (prefill.cuh): X' image, W' image, GEMM -- three launches on `st`.
 template <int BN, int MH>
 bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
@@ -418,8 +420,6 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
     return BITSTACK_OK;
   });
   if (attr_rs) return attr_rs;
-  if (L->n_act * L->kh > 16)
-    return fail(BITSTACK_E_UNSUPPORTED, "prefill path supports n <= 16 active blocks (n <= 8 for k > 16)");
   const int kc = (int)(L->d_in_pad / bs::kPK);
   const int rt_img = (L->row_tiles + 1) / 2 * 2;
   const int nt = (int)((batch + BN - 1) / BN);
@@ -448,6 +448,15 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   CK(cudaGetLastError());
   CK(cudaEventRecord(L->pf_join, L->pf_side));
 
+  // W' restore: the rgemv pipeline in W'-output mode (TMA operands, balanced ranges), or the
+  // original wtile kernel (BS_PREFILL_WTILE=1, A/B)
+  static const int wtile_env = [] { const char* e = getenv("BS_PREFILL_WTILE"); return e ? atoi(e) : 0; }();
+  if (wtile_env && L->n_act * L->kh > 16)
+    return fail(BITSTACK_E_UNSUPPORTED, "wtile restore supports n <= 16 active blocks (n <= 8 for k > 16)");
+  if (!wtile_env) {
+    rs = launch_wrestore(L, kc, rt_img, st);
+    if (rs) return rs;
+  } else {
   bs::WtileParams wp;
   wp.signs = L->signs;
   wp.u = reinterpret_cast<const uint16_t*>(L->u);
@@ -468,6 +477,7 @@ bitstack_status launch_prefill(bitstack_layer L, const void* x, int xdt, void* y
   bs::wtile_kernel<kWtileG><<<wgrid, WC::kThreads, WC::kSmem(wp.n), st>>>(wp);
   count_launch();
   CK(cudaGetLastError());
+  }
   CK(cudaStreamWaitEvent(st, L->pf_join, 0));
 
   bs::GemmParams gp;
@@ -516,21 +526,12 @@ bitstack_status encode_factor_map(CUtensorMap* map, const void* base, int64_t ro
   return BITSTACK_OK;
 }
 
-// Restore-and-multiply path (rgemv.cuh): X' images, then one kernel; 2 launches on `st`.
-template <int BP>
-bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
-                                cudaStream_t st) {
-  using C = bs::RgCfg<BP>;
-  static std::atomic<unsigned long long> attr_done{0};
-  bitstack_status rs = once_per_device(attr_done, [&]() -> bitstack_status {
-    CK(cudaFuncSetAttribute(bs::rgemv_kernel<BP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-    return BITSTACK_OK;
-  });
-  if (rs) return rs;
-  // CTAs: either each row tile split into `splits` unit ranges (whole row tiles per CTA), or one
-  // CTA per SM over a balanced contiguous range of the row_tiles x nq (row tile, unit) pairs,
-  // whichever has the shorter longest range (a range that spans row tiles costs about one unit
-  // more: a drain and a partial slot per segment); kmax = partial slots per CTA
+// Work partition of the rgemv kernel (rgemv.cuh): either each row tile split into `splits` unit
+// ranges (whole row tiles per CTA), or one CTA per SM over a balanced contiguous range of the
+// row_tiles x nq (row tile, unit) pairs, whichever has the shorter longest range (a range that
+// spans row tiles costs about one unit more: a drain and a partial slot per segment); kmax =
+// partial slots per CTA.  Also builds the TMA maps of U' and V' once per handle.
+bitstack_status rg_setup(bitstack_layer L, int* grid, int* kmax, int* splits) {
   const int64_t W = (int64_t)L->row_tiles * L->nq;
   const int splits_r = (int)std::max<int64_t>(1, std::min<int64_t>(L->sm_count / std::max(1, L->row_tiles), L->nq));
   const int64_t span_r = (L->nq + splits_r - 1) / splits_r;
@@ -538,9 +539,55 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
   const int64_t span_b = (W + grid_b - 1) / grid_b + 1;
   static const int mode_env = [] { const char* e = getenv("BS_RG_MODE"); return e ? atoi(e) : 0; }();   // A/B override
   const bool balanced = mode_env == 2 || (mode_env != 1 && span_b < span_r);
-  const int grid = balanced ? grid_b : L->row_tiles * splits_r;
-  const int kmax = balanced ? (int)((span_b - 1 + L->nq - 1) / L->nq + 1) : 1;
-  if (kmax > 32) return fail(BITSTACK_E_UNSUPPORTED, "restore-and-multiply: too many row tiles per CTA");
+  *grid = balanced ? grid_b : L->row_tiles * splits_r;
+  *kmax = balanced ? (int)((span_b - 1 + L->nq - 1) / L->nq + 1) : 1;
+  *splits = balanced ? 0 : splits_r;
+  if (*kmax > 32) return fail(BITSTACK_E_UNSUPPORTED, "restore-and-multiply: too many row tiles per CTA");
+  if (!L->rg_maps) {
+    bitstack_status rs = encode_factor_map(&L->rg_tmu, L->u, (int64_t)L->n_cap * L->kh * L->rows_pad);
+    if (rs) return rs;
+    rs = encode_factor_map(&L->rg_tmv, L->v, (int64_t)L->n_cap * L->kh * L->d_in_pad);
+    if (rs) return rs;
+    L->rg_maps = true;
+  }
+  return BITSTACK_OK;
+}
+
+bs::RgParams rg_params(bitstack_layer L, int kmax, int splits) {
+  bs::RgParams rp = {};
+  rp.tmu = L->rg_tmu;
+  rp.tmv = L->rg_tmv;
+  rp.signs = L->signs;
+  rp.u = reinterpret_cast<const uint16_t*>(L->u);
+  rp.v = reinterpret_cast<const uint16_t*>(L->v);
+  rp.counters = L->counters;
+  rp.n = L->n_act * L->kh;
+  rp.ksh = L->kh == 2 ? 1 : 0;
+  rp.nq = L->nq;
+  rp.rows_pad = L->rows_pad;
+  rp.rows_local = (int)L->rows_local;
+  rp.row_tiles = L->row_tiles;
+  rp.kmax = kmax;
+  rp.splits = splits;
+  rp.f16 = L->dev_fdt == 2 ? 1 : 0;
+  rp.trace = reinterpret_cast<long long*>(g_dbg_acc);
+  return rp;
+}
+
+// Restore-and-multiply path (rgemv.cuh): X' images, then one kernel; 2 launches on `st`.
+template <int BP>
+bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
+                                cudaStream_t st) {
+  using C = bs::RgCfg<BP>;
+  static std::atomic<unsigned long long> attr_done{0};
+  bitstack_status rs = once_per_device(attr_done, [&]() -> bitstack_status {
+    CK(cudaFuncSetAttribute(bs::rgemv_kernel<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    return BITSTACK_OK;
+  });
+  if (rs) return rs;
+  int grid = 0, kmax = 0, splits = 0;
+  rs = rg_setup(L, &grid, &kmax, &splits);
+  if (rs) return rs;
   rs = grow(L, &L->rg_x, &L->rg_x_bytes, (int64_t)L->nq * C::kXImg, st);
   if (rs) return rs;
   rs = grow(L, &L->rg_part, &L->rg_part_bytes, (int64_t)grid * kmax * BP * 128 * 4, st);
@@ -551,43 +598,48 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
                                             reinterpret_cast<uint4*>(L->rg_x));
   count_launch();
   CK(cudaGetLastError());
-  if (!L->rg_maps) {
-    rs = encode_factor_map(&L->rg_tmu, L->u, (int64_t)L->n_cap * L->kh * L->rows_pad);
-    if (rs) return rs;
-    rs = encode_factor_map(&L->rg_tmv, L->v, (int64_t)L->n_cap * L->kh * L->d_in_pad);
-    if (rs) return rs;
-    L->rg_maps = true;
-  }
-  bs::RgParams rp;
-  rp.tmu = L->rg_tmu;
-  rp.tmv = L->rg_tmv;
-  rp.signs = L->signs;
-  rp.u = reinterpret_cast<const uint16_t*>(L->u);
-  rp.v = reinterpret_cast<const uint16_t*>(L->v);
+  bs::RgParams rp = rg_params(L, kmax, splits);
   rp.ximg = L->rg_x;
   rp.part = reinterpret_cast<float*>(L->rg_part);
-  rp.counters = L->counters;
   rp.y = y;
   rp.y_stride = L->rows_local;
   rp.y_dtype = ydt;
-  rp.n = L->n_act * L->kh;
-  rp.ksh = L->kh == 2 ? 1 : 0;
-  rp.nq = L->nq;
-  rp.rows_pad = L->rows_pad;
-  rp.rows_local = (int)L->rows_local;
-  rp.row_tiles = L->row_tiles;
-  rp.kmax = kmax;
-  rp.splits = balanced ? 0 : splits_r;
   rp.batch = (int)batch;
-  rp.f16 = L->dev_fdt == 2 ? 1 : 0;
-  rp.trace = reinterpret_cast<long long*>(g_dbg_acc);
   int slot = -1;   // measurement hooks bracket the dominant kernel
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
-  bs::rgemv_kernel<BP><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  bs::rgemv_kernel<BP, false><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
   count_launch();
   CK(cudaGetLastError());
   return record_prof(st, false, &slot);
+}
+
+// The prefill's W' restore on the rgemv pipeline (W'-output mode): every (row tile, unit) of W'
+// as the GEMM's scaled fp16 operand image, row scales into pf_rowexp.  Padding row tiles of the
+// image (rt_img > row_tiles) are zeroed.
+bitstack_status launch_wrestore(bitstack_layer L, int kc, int rt_img, cudaStream_t st) {
+  using C = bs::RgCfg<16>;
+  static std::atomic<unsigned long long> attr_done{0};
+  bitstack_status rs = once_per_device(attr_done, [&]() -> bitstack_status {
+    CK(cudaFuncSetAttribute(bs::rgemv_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    return BITSTACK_OK;
+  });
+  if (rs) return rs;
+  int grid = 0, kmax = 0, splits = 0;
+  rs = rg_setup(L, &grid, &kmax, &splits);
+  if (rs) return rs;
+  if (rt_img > L->row_tiles)
+    CK(cudaMemsetAsync(L->pf_w + (int64_t)L->row_tiles * kc * bs::kImgTileA, 0,
+                       (size_t)(rt_img - L->row_tiles) * kc * bs::kImgTileA, st));
+  bs::RgParams rp = rg_params(L, kmax, splits);
+  rp.wimg = L->pf_w;
+  rp.rowexp = L->pf_rowexp;
+  rp.vmaxr = L->vmaxr;
+  rp.kc = kc;
+  bs::rgemv_kernel<16, true><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  count_launch();
+  CK(cudaGetLastError());
+  return BITSTACK_OK;
 }
 
 bitstack_status launch_rgemv(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
@@ -1176,8 +1228,8 @@ static bitstack_status matmul_device(bitstack_layer L, const void* x, bitstack_d
   const MatmulPath path = choose_path(L, batch);
   const bool fp16ok = L->dev_fdt != 0 && L->layout == 1;
   if (path == kPathPrefill) {
-    if (!fp16ok || L->n_act * L->kh > 16)
-      return fail(BITSTACK_E_UNSUPPORTED, "prefill path needs bf16 / f16 factors and n <= 16");
+    if (!fp16ok)
+      return fail(BITSTACK_E_UNSUPPORTED, "prefill path needs bf16 / f16 factors");
     return launch_prefill(L, x, xdt, y, ydt, batch, st);
   }
   if (path == kPathRgemv) {

@@ -25,6 +25,7 @@
 #include <cuda.h>   // CUtensorMap (the encoder is fetched at run time: no libcuda link)
 
 #include "decode_tc.cuh"
+#include "prefill.cuh"
 
 namespace bs {
 
@@ -46,6 +47,12 @@ struct RgParams {
   int kmax;               // max row-tile segments per CTA (partial slots per CTA)
   int splits;             // > 0: CTA b = (row tile b / splits, unit range b % splits of it); 0: balanced
   long long* trace;       // timing build (-DBS_RG_TRACE, scripts/rg_trace.py): per-stage stamps of CTA 0
+  // W'-output mode (the prefill's restore, WOUT = true): each unit's W' goes to the GEMM's fp16
+  // operand image instead of the GEMV, row j scaled by 2^-rowexp[j]
+  uint8_t* wimg;          // [row_tiles_img][kc] tiles of kImgTileA bytes (prefill.cuh img_off layout)
+  int* rowexp;            // [rows_pad]
+  const float* vmaxr;     // [n x kh][16] max_c |V'[c, r]|
+  int kc;                 // 64-column K chunks (d_in_pad / 64)
 };
 
 constexpr int kRgStages = 10;
@@ -153,7 +160,7 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
 #else
 #define RG_WAIT_FAST mbar_wait_sleep
 #endif
-template <int BP>
+template <int BP, bool WOUT>
 __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_constant__ RgParams p) {
   using C = RgCfg<BP>;
   extern __shared__ uint8_t smem_raw[];
@@ -248,12 +255,12 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         bulk_g2s(ximg + (u & 1) * C::kXImg, p.ximg + (long long)qx * C::kXImg, C::kXImg, &xfull[u & 1], pol);
         if (++qx == p.nq) qx = 0;
       };
-      if (U > 0) issue_x(0);
-      if (U > 1) issue_x(1);
+      if (!WOUT && U > 0) issue_x(0);
+      if (!WOUT && U > 1) issue_x(1);
       int s = 0, u = 0, i = 0, qq = qa, mt = mt0;
       uint32_t sph = 0;
       for (int t = 0; t < T; ++t) {
-        if (i == 0 && u >= 2) issue_x(u);
+        if (!WOUT && i == 0 && u >= 2) issue_x(u);
         if (t >= kRgStages) RG_WAIT_FAST(&sempty[s], sph ^ 1u);
         RG_TR(t, 0);
         uint8_t* st = stages + s * kRgStage;
@@ -318,7 +325,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         }
         __syncwarp();
       }
-      if (mw == 0 && gpend >= 0) {   // the previous unit's GEMV, once the next unit's first product is queued
+      if (!WOUT && mw == 0 && gpend >= 0) {   // the previous unit's GEMV, once the next unit's first product is queued
         gemv(gpend);
         gpend = -1;
       }
@@ -326,7 +333,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       if (++s == kRgStages) { s = 0; sph ^= 1u; }
       if (++pb == kRgPBuf) { pb = 0; pph ^= 1u; }
     }
-    if (mw == 0 && gpend >= 0) gemv(gpend);
+    if (!WOUT && mw == 0 && gpend >= 0) gemv(gpend);
     __syncwarp();
   } else if (warp < kRgNR) {
     // ================= restore warps: lane quadrant qd, column group h (kRgCols columns)
@@ -340,7 +347,10 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
 #pragma unroll
     for (int l = 0; l < NC; ++l) acc[l] = 0.f;
     int s = 0, pb = 0, u = 0, i = 0, uq = qa, useg = 0;
+    int wseg = -1;       // WOUT: row-tile segment whose row scale wsc holds
+    float wsc = 1.f;
     uint32_t sph = 0, pph = 0;
+    static_assert(!WOUT || NC == 32, "W'-output mode: 32 columns per restore warp");
     for (int t = 0; t < T; ++t) {
 #ifdef BS_RG_SPIN
       mbar_wait(&pfull[hv * kRgPBuf + pb], pph);
@@ -401,7 +411,46 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       }
 #endif
       if (lane == 0 && (warp == 0 || warp == kRgNR - 1)) RG_TR(t, warp == 0 ? 5 : 7);
-      if (++i == n) {   // W'[j, unit] complete: tf32 A image (after the previous GEMV read it)
+      if (WOUT && i + 1 == n) {   // W'[j, unit] complete: scaled fp16 into the GEMM's operand image
+        if (useg != wseg) {   // a new row tile: its row scale 2^-re with sum |U'| max |V'| < 2^15
+          wseg = useg;
+          const long long row = (long long)(mt0 + useg) * 128 + j;
+          float bound = 0.f;
+          for (int bi = 0; bi < n; ++bi) {
+            const uint4* up = reinterpret_cast<const uint4*>(p.u + ((long long)bi * p.rows_pad + row) * 16);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const uint4 raw = __ldg(up + kk);
+              const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+              for (int e2 = 0; e2 < 4; ++e2) {
+                const float2 f = p.f16 ? __half22float2(*reinterpret_cast<const __half2*>(&wv[e2]))
+                                       : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e2]));
+                const int r = kk * 8 + 2 * e2;
+                bound += fabsf(f.x) * __ldg(p.vmaxr + bi * 16 + r) + fabsf(f.y) * __ldg(p.vmaxr + bi * 16 + r + 1);
+              }
+            }
+          }
+          int re = 0;
+          if (bound > 0.f && bound < __int_as_float(0x7f800000)) re = xs_exp(__float_as_uint(bound), 15);
+          if (h == 0) p.rowexp[row] = re;
+          wsc = exp2i(-re);
+        }
+        const int c = 2 * uq + (h >> 1), k0 = (h & 1) * 32;
+        uint8_t* dst = p.wimg + ((long long)(mt0 + useg) * p.kc + c) * kImgTileA;
+#pragma unroll
+        for (int mq = 0; mq < 4; ++mq)
+          *reinterpret_cast<uint4*>(dst + img_off(j, k0 + 8 * mq)) =
+              make_uint4(pack_half2(acc[8 * mq + 0] * wsc, acc[8 * mq + 1] * wsc),
+                         pack_half2(acc[8 * mq + 2] * wsc, acc[8 * mq + 3] * wsc),
+                         pack_half2(acc[8 * mq + 4] * wsc, acc[8 * mq + 5] * wsc),
+                         pack_half2(acc[8 * mq + 6] * wsc, acc[8 * mq + 7] * wsc));
+#pragma unroll
+        for (int l = 0; l < NC; ++l) acc[l] = 0.f;
+        i = 0;
+        ++u;
+        if (++uq == p.nq) { uq = 0; ++useg; }
+      } else if (++i == n) {   // W'[j, unit] complete: tf32 A image (after the previous GEMV read it)
         if (u > 0) mbar_wait_sleep(aempty, (uint32_t)((u - 1) & 1));
 #pragma unroll
         for (int mq = 0; mq < NC / 4; ++mq) {
@@ -440,7 +489,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
       if (++s == kRgStages) { s = 0; sph ^= 1u; }
       if (++pb == kRgPBuf) { pb = 0; pph ^= 1u; }
     }
-    if (h == 0 && U > 0) {   // the range's last segment: y buffer -> partial slot
+    if (!WOUT && h == 0 && U > 0) {   // the range's last segment: y buffer -> partial slot
       const int seg = (int)((w1 - 1) / p.nq) - mt0;
       mbar_wait_sleep(&yfull[seg & 1], (uint32_t)((seg >> 1) & 1));
       tc_fence_after();
@@ -476,6 +525,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     while (b + 1 < G && W * (b + 1) / G < e) ++b;
     b_hi = b;
   };
+  if (WOUT) return;   // the image tiles are disjoint: no split-K
   if (threadIdx.x == 0) {
     __threadfence();
     int nf = 0;

@@ -839,3 +839,17 @@ def test_outputs_stay_inside_y(bs, kernel, batch, dtype):
     assert torch.isnan(buf[:guard]).all() and torch.isnan(buf[guard + batch * 300:]).all()
     ref = oracle_y(blocks, s32, 3, x.double().cpu().numpy())
     assert O.relative_l2(y.double().cpu().numpy(), ref) <= (1e-5 if dtype == "f32" else 1e-3)
+
+
+def test_prefill_more_than_16_blocks(bs):
+    """The prefill's W' restore runs on the restore-and-multiply pipeline, which has no block-count
+    limit: 20 blocks (and 12 k = 32 blocks = 24 halves) at 40 tokens take the prefill path and
+    match the oracle."""
+    for (d_out, d_in, n, k) in [(384, 512, 20, 16), (256, 384, 12, 32)]:
+        g, s32, blocks = compress_case(d_out, d_in, n, "bf16", 9700 + n, k=k)
+        lay = make_layer(bs, d_out, d_in, blocks, s32, "bf16")
+        x = make_x(40, g, 91)
+        c0 = bs.launch_count()
+        y, xr = gpu_y(lay, x)
+        assert bs.launch_count() - c0 == 4          # absmax + xprep + W' restore + GEMM
+        assert O.relative_l2(y, oracle_y(blocks, s32, n, xr)) <= 1e-3
