@@ -125,7 +125,7 @@ def main():
     os.makedirs(PROF, exist_ok=True)
     # bench lines, verbatim
     for name in ["bench_c2_driver", "bench_c2", "bench_ref", "bench_c5", "bench_c4", "bench_c4_ungrouped", "bench_load",
-                 "bench_compress", "bench_c3_up", "bench_c3_down"]:
+                 "bench_compress", "bench_c3_up", "bench_c3_down", "bench_c2_b48"]:
         src = os.path.join(R02, name + ".json")
         ls = json_lines(src)
         if ls:
@@ -174,7 +174,7 @@ def main():
                 "r02_ncu_decode_c2.txt", "c2_n16_b1_g1")
     ncu_summary(os.path.join(R02, "decode_c5.ncu-rep"), "C5 decode pair (zq_mx + decode_mx), one launch each",
                 "r02_ncu_decode_c5.txt", "c5_n12_b1_g1")
-    ncu_summary(os.path.join(R02, "prefill_c3_up.ncu-rep"), "C3 up/gate prefill: wtile + GEMM, one launch each",
+    ncu_summary(os.path.join(R02, "prefill_c3_up.ncu-rep"), "C3 up/gate prefill: W' restore (rgemv_kernel<16, true>) + GEMM, one launch each",
                 "r02_ncu_prefill_c3_up.txt", "c3_up_n8_b2048_g1", regex="prefill_gemm")
     ncu_summary(os.path.join(R02, "rg_c5.ncu-rep"), "C5 restore-and-multiply (rgemv_kernel<16>, B=8, balanced ranges), one launch",
                 "r02_ncu_rgemv_c5.txt", "c5_n12_b8_g1_rgemv", regex="rgemv")

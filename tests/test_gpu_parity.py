@@ -625,7 +625,7 @@ def test_prefill_parity_ragged(bs, shape):
     lay.set_kernel("prefill")
     c0 = bs.launch_count()
     gpu_y(lay, make_x(2, g, 1))
-    assert bs.launch_count() - c0 == 4          # absmax + xprep + wtile + gemm: the prefill kernels ran
+    assert bs.launch_count() - c0 == 4          # absmax + xprep + W' restore + gemm: the prefill kernels ran
     for batch in (1, 17, 256, 300, 600):
         x = make_x(batch, g, 300 + batch)
         for n in (1, 2, 5):
