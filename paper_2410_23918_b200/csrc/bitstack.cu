@@ -24,6 +24,7 @@
 #include "decode_tc.cuh"
 #include "prefill.cuh"
 #include "rgemv.cuh"
+#include "wrestore.cuh"
 
 struct bitstack_layer_s {
   int64_t d_out = 0, d_in = 0, row_begin = 0, row_end = 0, rows_local = 0;
@@ -636,6 +637,25 @@ bitstack_status launch_wrestore(bitstack_layer L, int kc, int rt_img, cudaStream
   rp.rowexp = L->pf_rowexp;
   rp.vmaxr = L->vmaxr;
   rp.kc = kc;
+  // default: tcgen05 products read back from TMEM (rgemv_kernel<16, true>); BS_WRESTORE_HMMA=1: the
+  // products in registers (wrestore.cuh, mma.sync) -- measured slower (C3 up/gate restore 130 vs 106
+  // us: ALU-issue bound at ~2 instructions per element and block), kept for A/B runs
+  static const int hm_env = [] { const char* e = getenv("BS_WRESTORE_HMMA"); return e ? atoi(e) : 0; }();
+  if (hm_env) {
+    static std::atomic<unsigned long long> hm_done{0};
+    rs = once_per_device(hm_done, [&]() -> bitstack_status {
+      CK(cudaFuncSetAttribute(bs::wrestore_hmma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs::kWrSmem));
+      CK(cudaFuncSetAttribute(bs::wrestore_hmma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bs::kWrSmem));
+      return BITSTACK_OK;
+    });
+    if (rs) return rs;
+    const int hgrid = (int)std::min<int64_t>((int64_t)L->row_tiles * L->nq, (int64_t)L->sm_count * 2);
+    if (rp.f16) bs::wrestore_hmma_kernel<false><<<hgrid, bs::kWrThreads, bs::kWrSmem, st>>>(rp);
+    else bs::wrestore_hmma_kernel<true><<<hgrid, bs::kWrThreads, bs::kWrSmem, st>>>(rp);
+    count_launch();
+    CK(cudaGetLastError());
+    return BITSTACK_OK;
+  }
   bs::rgemv_kernel<16, true><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
   count_launch();
   CK(cudaGetLastError());

@@ -853,3 +853,17 @@ def test_prefill_more_than_16_blocks(bs):
         y, xr = gpu_y(lay, x)
         assert bs.launch_count() - c0 == 4          # absmax + xprep + W' restore + GEMM
         assert O.relative_l2(y, oracle_y(blocks, s32, n, xr)) <= 1e-3
+
+
+def test_prefill_register_product_restore_variant():
+    """The opt-in W' restore with the products in registers (BS_WRESTORE_HMMA=1, csrc/wrestore.cuh)
+    passes the prefill parity tests too (a fresh process: the switch is read once per process)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BS_WRESTORE_HMMA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "tests/test_gpu_parity.py",
+                        "-k", "prefill_parity_ragged or prefill_more_than or prefill_dtypes"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
