@@ -576,13 +576,21 @@ bs::RgParams rg_params(bitstack_layer L, int kmax, int splits) {
 }
 
 // Restore-and-multiply path (rgemv.cuh): X' images, then one kernel; 2 launches on `st`.
+// Restore-and-multiply channel half 1 with register products (mma.sync) instead of TMEM reads:
+// BS_RG_HYB=1 (opt-in; measured slower -- C5 at 8 tokens 631 -> 777 us)
+static bool rg_hybrid() {
+  static const int v = [] { const char* e = getenv("BS_RG_HYB"); return e ? atoi(e) : 0; }();
+  return v != 0;
+}
+
 template <int BP>
 bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* y, int ydt, int64_t batch,
                                 cudaStream_t st) {
   using C = bs::RgCfg<BP>;
   static std::atomic<unsigned long long> attr_done{0};
   bitstack_status rs = once_per_device(attr_done, [&]() -> bitstack_status {
-    CK(cudaFuncSetAttribute(bs::rgemv_kernel<BP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    CK(cudaFuncSetAttribute(bs::rgemv_kernel<BP, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    CK(cudaFuncSetAttribute(bs::rgemv_kernel<BP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     return BITSTACK_OK;
   });
   if (rs) return rs;
@@ -609,7 +617,8 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
   int slot = -1;   // measurement hooks bracket the dominant kernel
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
-  bs::rgemv_kernel<BP, false><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  if (rg_hybrid()) bs::rgemv_kernel<BP, false, true><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  else bs::rgemv_kernel<BP, false, false><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
   count_launch();
   CK(cudaGetLastError());
   return record_prof(st, false, &slot);
@@ -622,7 +631,8 @@ bitstack_status launch_wrestore(bitstack_layer L, int kc, int rt_img, cudaStream
   using C = bs::RgCfg<16>;
   static std::atomic<unsigned long long> attr_done{0};
   bitstack_status rs = once_per_device(attr_done, [&]() -> bitstack_status {
-    CK(cudaFuncSetAttribute(bs::rgemv_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    CK(cudaFuncSetAttribute(bs::rgemv_kernel<16, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    CK(cudaFuncSetAttribute(bs::rgemv_kernel<16, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     return BITSTACK_OK;
   });
   if (rs) return rs;
@@ -656,7 +666,8 @@ bitstack_status launch_wrestore(bitstack_layer L, int kc, int rt_img, cudaStream
     CK(cudaGetLastError());
     return BITSTACK_OK;
   }
-  bs::rgemv_kernel<16, true><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  if (rg_hybrid()) bs::rgemv_kernel<16, true, true><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  else bs::rgemv_kernel<16, true, false><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
   count_launch();
   CK(cudaGetLastError());
   return BITSTACK_OK;

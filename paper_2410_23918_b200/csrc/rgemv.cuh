@@ -148,6 +148,52 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
       : "memory");
 }
 
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+
+template <bool BF16>
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if (BF16)
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%10,%10,%10,%10};"
+                 : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
+  else
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%10,%10,%10,%10};"
+                 : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
+}
+
+// byte offset of 16-byte chunk `ch` of row r in a [128][16] 16-bit tile written by TMA with the
+// 32-byte swizzle (address bit 4 ^= bit 7; the tile is 256-byte aligned)
+__device__ __forceinline__ uint32_t sw32_off(int r, int ch) { return (uint32_t)(r * 32 + ((ch ^ (r >> 2)) & 1) * 16); }
+
+// W' row bound sum_i sum_r |U'_i[row, r]| max_c |V'_i[c, r]| of the W'-output mode.  Not inlined, so
+// every caller (TMEM restore warps, register-product warps) rounds it identically: the two halves
+// of a row must pick the same power-of-two scale.
+__device__ __noinline__ float rg_row_bound(const uint16_t* __restrict__ u, const float* __restrict__ vmaxr, long long rows_pad,
+                                           long long row, int n, int f16) {
+  float bound = 0.f;
+  for (int bi = 0; bi < n; ++bi) {
+    const uint4* up = reinterpret_cast<const uint4*>(u + ((long long)bi * rows_pad + row) * 16);
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint4 raw = __ldg(up + kk);
+      const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
+      for (int e2 = 0; e2 < 4; ++e2) {
+        const float2 f = f16 ? __half22float2(*reinterpret_cast<const __half2*>(&wv[e2]))
+                             : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e2]));
+        const int r = kk * 8 + 2 * e2;
+        bound = __fadd_rn(bound, __fadd_rn(__fmul_rn(fabsf(f.x), __ldg(vmaxr + bi * 16 + r)),
+                                           __fmul_rn(fabsf(f.y), __ldg(vmaxr + bi * 16 + r + 1))));
+      }
+    }
+  }
+  return bound;
+}
+
 #ifdef BS_RG_TRACE
 #define RG_TR(t_, c_) do { if (p.trace && blockIdx.x == 0 && (t_) < 2048) p.trace[(t_) * 8 + (c_)] = clock64(); } while (0)
 #else
@@ -160,7 +206,7 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, ui
 #else
 #define RG_WAIT_FAST mbar_wait_sleep
 #endif
-template <int BP, bool WOUT>
+template <int BP, bool WOUT, bool HYB>
 __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_constant__ RgParams p) {
   using C = RgCfg<BP>;
   extern __shared__ uint8_t smem_raw[];
@@ -313,6 +359,11 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
 #pragma unroll
       for (int hv = 0; hv < kRgHV; ++hv) {
         if (kRgMmaWarps > 1 && hv % kRgMmaWarps != mw) continue;
+        if (HYB && hv == 1) {   // this half's products are formed by its restore warps (mma.sync)
+          if (lane == 0) mbar_arrive(&sempty[s]);
+          __syncwarp();
+          continue;
+        }
         if (t >= kRgPBuf) RG_WAIT_FAST(&pempty[hv * kRgPBuf + pb], pph ^ 1u);
         if (lane == 0 && hv == 0) RG_TR(t, 3);
         tc_fence_after();
@@ -343,6 +394,118 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
     const int pcol = (h * NC) % kRgPCols;              // its columns inside the half's P buffer
     const int j = qd * 32 + lane;
     const uint32_t lq = (uint32_t)(qd * 32) << 16;
+    if (HYB && hv == 1) {
+      // ---- channel half 1 with the products in registers: this warp's 32 x 32 share (rows 32 qd..,
+      // channels 64 + 32 (h & 1)..) of P_i = U'_i V'_i^T by mma.sync m16n8k16 from the stage's
+      // U' / V' tiles, so only half 0's products are read back from TMEM
+      const int g = lane >> 2, t4 = lane & 3, hq = h & 1;
+      const int ssh = 16 * (t4 & 1) + (t4 >> 1);   // channel 8 ni + 2 t4 + e of the sign word -> bit 8 e + 2 ni
+      const uint32_t a_off = sw32_off(32 * qd + (lane & 15), lane >> 4);
+      const uint32_t b_off = 4096 + sw32_off(64 + 32 * hq + (lane & 7) + 8 * (lane >> 4), (lane >> 3) & 1);
+      const uint32_t s_off = 8192 + (32 * qd + g) * 16 + h * 4;
+      float ha[2][4][4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ha[a][b][e] = 0.f;
+      int s = 0, u = 0, i = 0, uq = qa, useg = 0, wseg = -1;
+      uint32_t sph = 0;
+      float wsc[2][2] = {{1.f, 1.f}, {1.f, 1.f}};
+      for (int t = 0; t < T; ++t) {
+        mbar_wait_sleep(&full[s], sph);
+        const uint32_t sb = smem_u32(stages + s * kRgStage);
+        uint32_t af[2][4], bfr[2][4], sw[2][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) ldsm_x4(sb + a_off + 512 * mi, af[mi][0], af[mi][1], af[mi][2], af[mi][3]);
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) ldsm_x4(sb + b_off + 512 * nb, bfr[nb][0], bfr[nb][1], bfr[nb][2], bfr[nb][3]);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t x;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(sb + s_off + (16 * mi + 8 * hh) * 16));
+            sw[mi][hh] = x >> ssh;   // clear bit = negative sign
+          }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[s]);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            float d[4];
+            if (p.f16) mma16816<false>(d, af[mi], bfr[ni >> 1][(ni & 1) * 2], bfr[ni >> 1][(ni & 1) * 2 + 1]);
+            else mma16816<true>(d, af[mi], bfr[ni >> 1][(ni & 1) * 2], bfr[ni >> 1][(ni & 1) * 2 + 1]);
+            const int bb = 2 * ni;
+            const uint32_t s0 = sw[mi][0], s1 = sw[mi][1];
+            const float2 lo = make_float2(__uint_as_float(__float_as_uint(d[0]) ^ (~(s0 << (31 - bb)) & 0x80000000u)),
+                                          __uint_as_float(__float_as_uint(d[1]) ^ (~(s0 << (23 - bb)) & 0x80000000u)));
+            const float2 hi = make_float2(__uint_as_float(__float_as_uint(d[2]) ^ (~(s1 << (31 - bb)) & 0x80000000u)),
+                                          __uint_as_float(__float_as_uint(d[3]) ^ (~(s1 << (23 - bb)) & 0x80000000u)));
+            const float2 a0 = __fadd2_rn(make_float2(ha[mi][ni][0], ha[mi][ni][1]), lo);
+            const float2 a1 = __fadd2_rn(make_float2(ha[mi][ni][2], ha[mi][ni][3]), hi);
+            ha[mi][ni][0] = a0.x;
+            ha[mi][ni][1] = a0.y;
+            ha[mi][ni][2] = a1.x;
+            ha[mi][ni][3] = a1.y;
+          }
+        if (++s == kRgStages) { s = 0; sph ^= 1u; }
+        if (++i < n) continue;
+        i = 0;
+        if (WOUT) {   // W'[rows, unit] complete: scaled fp16 into the GEMM's operand image (chunk 2 uq + 1)
+          if (useg != wseg) {
+            wseg = useg;
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int hh = 0; hh < 2; ++hh) {
+                const long long row = (long long)(mt0 + useg) * 128 + 32 * qd + 16 * mi + 8 * hh + g;
+                const float bound = rg_row_bound(p.u, p.vmaxr, p.rows_pad, row, n, p.f16);
+                int re = 0;
+                if (bound > 0.f && bound < __int_as_float(0x7f800000)) re = xs_exp(__float_as_uint(bound), 15);
+                wsc[mi][hh] = exp2i(-re);
+              }
+          }
+          uint8_t* dst = p.wimg + ((long long)(mt0 + useg) * p.kc + 2 * uq + 1) * kImgTileA;
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni)
+                *reinterpret_cast<uint32_t*>(dst + img_off(32 * qd + 16 * mi + 8 * hh + g, 32 * hq + 8 * ni + 2 * t4)) =
+                    pack_half2(ha[mi][ni][2 * hh] * wsc[mi][hh], ha[mi][ni][2 * hh + 1] * wsc[mi][hh]);
+        } else {      // tf32 A image (after the previous GEMV read it)
+          if (u > 0) mbar_wait_sleep(aempty, (uint32_t)((u - 1) & 1));
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni) {
+                const int r = 32 * qd + 16 * mi + 8 * hh + g, c = 64 + 32 * hq + 8 * ni + 2 * t4;
+                uint32_t o0, o1;
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(o0) : "f"(ha[mi][ni][2 * hh]));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(o1) : "f"(ha[mi][ni][2 * hh + 1]));
+                *reinterpret_cast<uint2*>(aimg + ((r >> 3) * 32 + (c >> 2)) * 128 + (r & 7) * 16 + (c & 3) * 4) =
+                    make_uint2(o0, o1);
+              }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(afull);
+        }
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ha[a][b][e] = 0.f;
+        ++u;
+        if (++uq == p.nq) { uq = 0; ++useg; }
+      }
+    } else {
     float acc[NC];
 #pragma unroll
     for (int l = 0; l < NC; ++l) acc[l] = 0.f;
@@ -415,22 +578,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         if (useg != wseg) {   // a new row tile: its row scale 2^-re with sum |U'| max |V'| < 2^15
           wseg = useg;
           const long long row = (long long)(mt0 + useg) * 128 + j;
-          float bound = 0.f;
-          for (int bi = 0; bi < n; ++bi) {
-            const uint4* up = reinterpret_cast<const uint4*>(p.u + ((long long)bi * p.rows_pad + row) * 16);
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-              const uint4 raw = __ldg(up + kk);
-              const uint32_t wv[4] = {raw.x, raw.y, raw.z, raw.w};
-#pragma unroll
-              for (int e2 = 0; e2 < 4; ++e2) {
-                const float2 f = p.f16 ? __half22float2(*reinterpret_cast<const __half2*>(&wv[e2]))
-                                       : __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e2]));
-                const int r = kk * 8 + 2 * e2;
-                bound += fabsf(f.x) * __ldg(p.vmaxr + bi * 16 + r) + fabsf(f.y) * __ldg(p.vmaxr + bi * 16 + r + 1);
-              }
-            }
-          }
+          const float bound = rg_row_bound(p.u, p.vmaxr, p.rows_pad, row, n, p.f16);
           int re = 0;
           if (bound > 0.f && bound < __int_as_float(0x7f800000)) re = xs_exp(__float_as_uint(bound), 15);
           if (h == 0) p.rowexp[row] = re;
@@ -503,6 +651,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         for (int b = 0; b < 16; ++b) slot[(b0 + b) * 128 + j] = __uint_as_float(yv[b]);
       }
     }
+    }   // !(HYB && hv == 1)
   }
 
   // ---- teardown; the last CTA to finish a row tile sums its partial slots in CTA order and writes y

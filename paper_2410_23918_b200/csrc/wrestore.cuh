@@ -28,29 +28,6 @@ constexpr int kWrThreads = kWrConsumers * 32;
 constexpr int kWrBarOff = kWrStages * kRgStage;
 constexpr int kWrSmem = kWrBarOff + 2 * kWrStages * 8 + 1024;   // + alignment slack
 
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
-}
-
-template <bool BF16>
-__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  if (BF16)
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%10,%10,%10,%10};"
-                 : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
-  else
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%10,%10,%10,%10};"
-                 : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.f));
-}
-
-// byte offset of 16-byte chunk `ch` of row r in a [128][16] 16-bit tile written by TMA with the
-// 32-byte swizzle (address bit 4 ^= bit 7; the tile is 256-byte aligned)
-__device__ __forceinline__ uint32_t sw32_off(int r, int ch) { return (uint32_t)(r * 32 + ((ch ^ (r >> 2)) & 1) * 16); }
-
 template <bool BF16>
 __global__ void __launch_bounds__(kWrThreads, 2) wrestore_hmma_kernel(const __grid_constant__ RgParams p) {
   extern __shared__ uint8_t smem_raw[];

@@ -867,3 +867,17 @@ def test_prefill_register_product_restore_variant():
                        cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout
+
+
+def test_rgemv_hybrid_register_products_variant():
+    """The opt-in restore-and-multiply / W' restore variant whose channel half 1 forms its products
+    with mma.sync in registers (BS_RG_HYB=1) passes the rgemv and prefill parity tests (fresh process)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BS_RG_HYB="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "tests/test_gpu_parity.py",
+                        "-k", "rgemv_parity or prefill_parity_ragged or prefill_more_than"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
