@@ -617,8 +617,19 @@ bitstack_status launch_rgemv_bp(bitstack_layer L, const void* x, int xdt, void* 
   int slot = -1;   // measurement hooks bracket the dominant kernel
   bitstack_status ps = record_prof(st, true, &slot);
   if (ps) return ps;
-  if (rg_hybrid()) bs::rgemv_kernel<BP, false, true><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
-  else bs::rgemv_kernel<BP, false, false><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  // programmatic dependent launch after rg_xprep (BS_RG_PDL=0: plain launch): the U' / V' / sign
+  // stages stream in while the X' image is written; only the X' loads wait
+  static const int pdl_env = [] { const char* e = getenv("BS_RG_PDL"); return e ? atoi(e) : 1; }();
+  if (pdl_env) {
+    cudaLaunchAttribute attr[1];
+    cudaLaunchConfig_t cfg = pdl_config(grid, bs::kRgWarps * 32, C::kSmem, st, attr);
+    if (rg_hybrid()) CK(cudaLaunchKernelEx(&cfg, bs::rgemv_kernel<BP, false, true>, rp));
+    else CK(cudaLaunchKernelEx(&cfg, bs::rgemv_kernel<BP, false, false>, rp));
+  } else if (rg_hybrid()) {
+    bs::rgemv_kernel<BP, false, true><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  } else {
+    bs::rgemv_kernel<BP, false, false><<<grid, bs::kRgWarps * 32, C::kSmem, st>>>(rp);
+  }
   count_launch();
   CK(cudaGetLastError());
   return record_prof(st, false, &slot);

@@ -98,6 +98,9 @@ template <int BP> struct RgCfg {
 __global__ void __launch_bounds__(256) rg_xprep_kernel(const void* __restrict__ x, int x_dtype, long long x_stride,
                                                       const float* __restrict__ inv_s, int batch, int d_in, int nq,
                                                       int bp, uint4* __restrict__ img) {
+  // the rgemv launch that follows (programmatic dependent launch) may start its restore pipeline now:
+  // only its X' loads wait for this grid (griddepcontrol.wait in its producer)
+  asm volatile("griddepcontrol.launch_dependents;");
   const long long pieces = (long long)nq * bp * 32;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < pieces;
        e += (long long)gridDim.x * blockDim.x) {
@@ -301,6 +304,7 @@ __global__ void __launch_bounds__(kRgWarps * 32, 1) rgemv_kernel(const __grid_co
         bulk_g2s(ximg + (u & 1) * C::kXImg, p.ximg + (long long)qx * C::kXImg, C::kXImg, &xfull[u & 1], pol);
         if (++qx == p.nq) qx = 0;
       };
+      if (!WOUT) asm volatile("griddepcontrol.wait;" ::: "memory");   // this call's X' image is complete
       if (!WOUT && U > 0) issue_x(0);
       if (!WOUT && U > 1) issue_x(1);
       int s = 0, u = 0, i = 0, qq = qa, mt = mt0;
